@@ -1,0 +1,891 @@
+/*
+ * halp_oracle.c -- CPU restatement of the reference HALP hot path.
+ * TEST INFRASTRUCTURE ONLY (see halp_oracle.h for the contract and the
+ * reference file:line map).  Compiled with -ffp-contract=off so that no
+ * a*b+c is fused unless written as fma() (MIRROR mode only).
+ */
+#define _GNU_SOURCE
+#include "halp_oracle.h"
+
+#include <math.h>
+#include <pthread.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+#include <time.h>
+
+static __thread char g_err[512];
+static void set_err(const char* m) { snprintf(g_err, sizeof g_err, "%s", m); }
+const char* oq_last_error(void) { return g_err; }
+
+/* ------------------------------------------------------------------ RNG */
+/* rng.hpp:12-18 split_mix */
+static uint64_t split_mix(uint64_t x) {
+  x += 0x9E3779B97F4A7C15ULL;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBULL;
+  return x ^ (x >> 31);
+}
+/* rng.hpp:29-32 */
+void oq_rng_init(oq_rng* r, uint64_t seed, uint64_t stream) {
+  r->state = split_mix(seed ^ split_mix(stream ^ 0xA5A5A5A5A5A5A5A5ULL));
+  if (r->state == 0) r->state = 0x9E3779B97F4A7C15ULL;
+}
+/* rng.hpp:34-39 */
+uint64_t oq_next_u64(oq_rng* r) {
+  uint64_t s = r->state;
+  s ^= s >> 12;
+  s ^= s << 25;
+  s ^= s >> 27;
+  r->state = s;
+  return s * 0x2545F4914F6CDD1DULL;
+}
+/* rng.hpp:42-44 */
+double oq_next_uniform(oq_rng* r) { return (double)(oq_next_u64(r) >> 11) * 0x1.0p-53; }
+/* rng.hpp:48-51 */
+uint64_t oq_next_index(oq_rng* r, uint64_t n) {
+  unsigned __int128 p = (unsigned __int128)oq_next_u64(r) * (unsigned __int128)n;
+  return (uint64_t)(p >> 64);
+}
+/* rng.hpp:55-60 (std::numbers::pi == M_PI; 2.0 * pi * u2 evaluates left to right) */
+double oq_next_normal(oq_rng* r) {
+  const double u1 = oq_next_uniform(r);
+  const double u2 = oq_next_uniform(r);
+  const double rr = sqrt(-2.0 * log1p(-u1));
+  return rr * cos(2.0 * M_PI * u2);
+}
+void oq_fill_u64(uint64_t seed, uint64_t stream, uint64_t skip, uint64_t* out, int64_t count) {
+  oq_rng r;
+  oq_rng_init(&r, seed, stream);
+  for (uint64_t i = 0; i < skip; ++i) (void)oq_next_u64(&r);
+  for (int64_t i = 0; i < count; ++i) out[i] = oq_next_u64(&r);
+}
+
+/* ------------------------------------------------------------ quantizer */
+/* fixed_point.cpp:14-22 */
+static int64_t min_code_for(int bits) { return bits == 64 ? INT64_MIN : -((int64_t)1 << (bits - 1)); }
+static int64_t max_code_for(int bits) { return bits == 64 ? INT64_MAX : ((int64_t)1 << (bits - 1)) - 1; }
+
+/* fixed_point.cpp:30-50 quantize_code */
+int64_t oq_quantize_code(double x, double delta, int bits, double u, int* err) {
+  if (!isfinite(x)) { if (err) *err = 1; return 0; }
+  const double t = x / delta;
+  const double hi = (double)max_code_for(bits);
+  const double lo = (double)min_code_for(bits);
+  if (t >= hi) return max_code_for(bits);
+  if (t <= lo) return min_code_for(bits);
+  const double snapped = nearbyint(t);
+  if (snapped * delta == x) return (int64_t)snapped;
+  const double fl = floor(t);
+  const double frac = t - fl;
+  int64_t code = (int64_t)fl;
+  if (frac > 0.0 && u < frac) ++code;
+  return code;
+}
+
+/* theory.cpp:33-35 code_span, :93-102 halp_scale */
+double oq_halp_scale(double grad_norm, double mu, int bits) {
+  if (!(isfinite(grad_norm) && grad_norm >= 0.0)) return -1.0;
+  if (!(isfinite(mu) && mu > 0.0)) return -1.0;
+  if (bits < 2 || bits > 64) return -1.0;
+  const double span = ldexp(1.0, bits - 1) - 1.0;
+  return grad_norm / (mu * span);
+}
+
+/* ----------------------------------------------------------------- data */
+/* objectives.cpp:27-45 make_regression (fill_gaussian_rowwise :17-23) */
+int oq_make_regression(int64_t n, int d, double noise_sd, uint64_t seed, double* X, double* y) {
+  if (n < 1 || d < 1) { set_err("make_regression: n and d must be positive"); return OQ_INVALID_INPUT; }
+  if (!(isfinite(noise_sd) && noise_sd >= 0.0)) {
+    set_err("make_regression: noise_sd must be finite and >= 0");
+    return OQ_INVALID_INPUT;
+  }
+  oq_rng rng;
+  oq_rng_init(&rng, seed, 0);
+  for (int64_t i = 0; i < n; ++i)
+    for (int j = 0; j < d; ++j) X[i * d + j] = oq_next_normal(&rng);
+  double* wt = (double*)malloc(sizeof(double) * (size_t)d);
+  for (int j = 0; j < d; ++j) wt[j] = oq_next_normal(&rng);
+  for (int64_t i = 0; i < n; ++i) {
+    double acc = 0.0;
+    for (int j = 0; j < d; ++j) acc += X[i * d + j] * wt[j];
+    y[i] = acc;
+  }
+  if (noise_sd > 0.0)
+    for (int64_t i = 0; i < n; ++i) y[i] += noise_sd * oq_next_normal(&rng);
+  free(wt);
+  return OQ_OK;
+}
+
+static inline double bf16_to_double(uint16_t b) {
+  uint32_t u = (uint32_t)b << 16;
+  float f;
+  memcpy(&f, &u, 4);
+  return (double)f;
+}
+/* load row i of X into out[0..d) as doubles (exact upcast) */
+static void load_row(const oq_objective* o, int64_t i, double* out) {
+  const int d = o->d;
+  if (o->dtype == OQ_F64) {
+    memcpy(out, (const double*)o->X + i * d, sizeof(double) * (size_t)d);
+  } else if (o->dtype == OQ_F32) {
+    const float* p = (const float*)o->X + i * d;
+    for (int j = 0; j < d; ++j) out[j] = (double)p[j];
+  } else {
+    const uint16_t* p = (const uint16_t*)o->X + i * d;
+    for (int j = 0; j < d; ++j) out[j] = bf16_to_double(p[j]);
+  }
+}
+
+static int check_objective(const oq_objective* o) {
+  if (!(isfinite(o->l2) && o->l2 >= 0.0)) { set_err("Objective: l2 must be finite and >= 0"); return OQ_INVALID_INPUT; }
+  if (o->n < 1) { set_err("Objective: dataset is empty"); return OQ_INVALID_INPUT; }
+  if (o->loss == OQ_SQUARED) {
+    if (!o->y || o->C != 1) { set_err("Objective: squared loss needs one target per row"); return OQ_INVALID_INPUT; }
+  } else {
+    if (o->C < 2 || !o->labels) { set_err("Objective: softmax loss needs labels and classes"); return OQ_INVALID_INPUT; }
+    for (int64_t i = 0; i < o->n; ++i)
+      if (o->labels[i] < 0 || o->labels[i] >= o->C) {
+        set_err("Objective: label outside [0, num_classes)");
+        return OQ_INVALID_INPUT;
+      }
+  }
+  return OQ_OK;
+}
+
+/* ======================================================================
+ * MIRROR-mode arithmetic helpers (the B200 kernels' operation order).
+ * ====================================================================== */
+
+/* Deterministic exp/log built only from IEEE +,-,*,/,fma, rint and
+ * exponent manipulation; the device code (csrc/halp_math.cuh) performs the
+ * identical sequence, so results agree bit for bit. */
+double oq_mexp(double x) {
+  if (!(x == x)) return x;
+  if (x > 709.782712893384) return INFINITY;
+  if (x < -745.1332191019412) return 0.0;
+  const double kf = rint(x * 1.4426950408889634);
+  const double r1 = fma(-kf, 6.93147180369123816490e-01, x);
+  const double r = fma(-kf, 1.90821492927058770002e-10, r1);
+  double p = 1.60590438368216145994e-10;             /* 1/13! */
+  p = fma(p, r, 2.08767569878680989792e-09);         /* 1/12! */
+  p = fma(p, r, 2.50521083854417187751e-08);         /* 1/11! */
+  p = fma(p, r, 2.75573192239858906526e-07);
+  p = fma(p, r, 2.75573192239858906526e-06);
+  p = fma(p, r, 2.48015873015873015873e-05);
+  p = fma(p, r, 1.98412698412698412698e-04);
+  p = fma(p, r, 1.38888888888888888889e-03);
+  p = fma(p, r, 8.33333333333333333333e-03);
+  p = fma(p, r, 4.16666666666666666667e-02);
+  p = fma(p, r, 1.66666666666666666667e-01);
+  p = fma(p, r, 0.5);
+  p = fma(p, r, 1.0);
+  p = fma(p, r, 1.0);
+  const int k = (int)kf;
+  /* scale by 2^k in two steps so subnormal results round once */
+  if (k > -1000) {
+    const int k1 = k / 2, k2 = k - k1;
+    double s1, s2;
+    uint64_t b1 = (uint64_t)(k1 + 1023) << 52, b2 = (uint64_t)(k2 + 1023) << 52;
+    memcpy(&s1, &b1, 8);
+    memcpy(&s2, &b2, 8);
+    return (p * s1) * s2;
+  }
+  {
+    double s1, s2;
+    uint64_t b1 = (uint64_t)(k + 600 + 1023) << 52, b2 = (uint64_t)(-600 + 1023) << 52;
+    memcpy(&s1, &b1, 8);
+    memcpy(&s2, &b2, 8);
+    return (p * s1) * s2;
+  }
+}
+
+/* log for x > 0 finite: x = m * 2^e with m in [sqrt(1/2), sqrt(2)),
+ * log(m) = 2 atanh(f), f = (m-1)/(m+1), odd polynomial in f. */
+double oq_mlog(double x) {
+  if (!(x == x) || x < 0.0) return NAN;
+  if (x == 0.0) return -INFINITY;
+  if (isinf(x)) return x;
+  uint64_t b;
+  memcpy(&b, &x, 8);
+  int e = (int)((b >> 52) & 0x7FF);
+  if (e == 0) { /* subnormal: normalise */
+    x = x * 0x1.0p54;
+    memcpy(&b, &x, 8);
+    e = (int)((b >> 52) & 0x7FF) - 54;
+  }
+  e -= 1023;
+  uint64_t mb = (b & 0x000FFFFFFFFFFFFFULL) | 0x3FF0000000000000ULL;
+  double m;
+  memcpy(&m, &mb, 8);
+  if (m > 1.4142135623730951) { m = m * 0.5; e += 1; }
+  const double f = (m - 1.0) / (m + 1.0);
+  const double f2 = f * f;
+  double p = 1.0 / 23.0;
+  p = fma(p, f2, 1.0 / 21.0);
+  p = fma(p, f2, 1.0 / 19.0);
+  p = fma(p, f2, 1.0 / 17.0);
+  p = fma(p, f2, 1.0 / 15.0);
+  p = fma(p, f2, 1.0 / 13.0);
+  p = fma(p, f2, 1.0 / 11.0);
+  p = fma(p, f2, 1.0 / 9.0);
+  p = fma(p, f2, 1.0 / 7.0);
+  p = fma(p, f2, 1.0 / 5.0);
+  p = fma(p, f2, 1.0 / 3.0);
+  const double s = (2.0 * f) * (f2 * p);           /* 2 f^3 P(f^2) */
+  const double ef = (double)e;
+  const double hi = fma(ef, 6.93147180369123816490e-01, 2.0 * f);
+  return hi + fma(ef, 1.90821492927058770002e-10, s);
+}
+
+/* ======================================================================
+ * REF mode: the reference's structure with sequential inner reductions.
+ * ====================================================================== */
+#define REF_BLOCK 1024 /* objectives.cpp:13 kBlock */
+
+/* packet width of the reference build's Eigen kernels: 1 = scalar,
+ * 2 = SSE2 (Packet2d), 4 = AVX (Packet4d).  Selected by pinning against the
+ * golden traces (tests/test_oracle_golden.py). */
+static int g_ref_lanes = 2;
+void oq_set_ref_lanes(int lanes) { g_ref_lanes = lanes; }
+
+/* logits for one row, REF order: sequential over features, which is what
+ * Eigen's column-major GEMV kernel does per output row when d < 128
+ * (GeneralMatrixVector.h block_cols == cols).  W is d x C column-major
+ * (objectives.hpp:56-58). */
+static void ref_row_logits(const double* x, const double* w, int d, int C, double* logits) {
+  for (int c = 0; c < C; ++c) {
+    double acc = 0.0;
+    const double* wc = w + (size_t)c * d;
+    for (int j = 0; j < d; ++j) acc += x[j] * wc[j];
+    logits[c] = acc;
+  }
+}
+
+/* softmax derivative in place (objectives.cpp:277-283 / :241-245) */
+static void ref_softmax_dl(double* l, int C, int label) {
+  double mx = l[0];
+  for (int c = 1; c < C; ++c) if (l[c] > mx) mx = l[c];
+  double s = 0.0;
+  for (int c = 0; c < C; ++c) { l[c] = exp(l[c] - mx); }
+  for (int c = 0; c < C; ++c) s += l[c];
+  for (int c = 0; c < C; ++c) l[c] = l[c] / s;
+  l[label] -= 1.0;
+}
+
+static double ref_softmax_loss(const double* l, int C, int label) {
+  double mx = l[0];
+  for (int c = 1; c < C; ++c) if (l[c] > mx) mx = l[c];
+  double s = 0.0;
+  for (int c = 0; c < C; ++c) s += exp(l[c] - mx);
+  const double lse = mx + log(s);
+  return lse - l[label];
+}
+
+/* Eigen's LinearVectorizedTraversal redux of squaredNorm() on an aligned
+ * VectorXd (Eigen/src/Core/Redux.h) with P-double packets: two packet
+ * accumulators over blocks of 2P, combined lane-wise, a trailing packet,
+ * the horizontal add (predux), then the scalar tail. */
+static double predux(const double* p, int P) {
+  if (P == 1) return p[0];
+  if (P == 2) return p[0] + p[1];
+  return (p[0] + p[2]) + (p[1] + p[3]);
+}
+static double ref_sqnorm(const double* v, int64_t len) {
+  const int P = g_ref_lanes;
+  if (P == 1 || len < P) {
+    double s = len ? v[0] * v[0] : 0.0;
+    for (int64_t i = 1; i < len; ++i) s = s + v[i] * v[i];
+    return s;
+  }
+  const int64_t a1 = (len / P) * P, a2 = (len / (2 * P)) * (2 * P);
+  double p0[4], p1[4];
+  for (int l = 0; l < P; ++l) p0[l] = v[l] * v[l];
+  if (a1 > P) {
+    for (int l = 0; l < P; ++l) p1[l] = v[P + l] * v[P + l];
+    for (int64_t i = 2 * P; i < a2; i += 2 * P)
+      for (int l = 0; l < P; ++l) {
+        p0[l] = p0[l] + v[i + l] * v[i + l];
+        p1[l] = p1[l] + v[i + P + l] * v[i + P + l];
+      }
+    for (int l = 0; l < P; ++l) p0[l] = p0[l] + p1[l];
+    if (a1 > a2)
+      for (int l = 0; l < P; ++l) p0[l] = p0[l] + v[a2 + l] * v[a2 + l];
+  }
+  double res = predux(p0, P);
+  for (int64_t i = a1; i < len; ++i) res = res + v[i] * v[i];
+  return res;
+}
+
+/* objectives.cpp:193-223 Objective::loss */
+static double ref_loss(const oq_objective* o, const double* w) {
+  const int d = o->d, C = o->C;
+  const int64_t n = o->n;
+  double* x = (double*)malloc(sizeof(double) * (size_t)d);
+  double lg[64];
+  double acc = 0.0;
+  for (int64_t r0 = 0; r0 < n; r0 += REF_BLOCK) {
+    const int64_t m = (n - r0) < REF_BLOCK ? (n - r0) : REF_BLOCK;
+    double blk = 0.0;
+    for (int64_t r = 0; r < m; ++r) {
+      load_row(o, r0 + r, x);
+      ref_row_logits(x, w, d, C, lg);
+      if (o->loss == OQ_SQUARED) {
+        const double e = lg[0] - o->y[r0 + r];
+        blk += 0.5 * e * e;
+      } else {
+        blk += ref_softmax_loss(lg, C, o->labels[r0 + r]);
+      }
+    }
+    acc += blk;
+  }
+  free(x);
+  return acc / (double)n + 0.5 * o->l2 * ref_sqnorm(w, (int64_t)d * C);
+}
+
+/* one block of objectives.cpp:271-287: partial = X_blk^T dl */
+static void ref_block_partial(const oq_objective* o, const double* w, int64_t b, double* partial,
+                              double* x, double* dl) {
+  const int d = o->d, C = o->C;
+  const int64_t r0 = b * REF_BLOCK;
+  const int64_t m = (o->n - r0) < REF_BLOCK ? (o->n - r0) : REF_BLOCK;
+  for (int64_t r = 0; r < m; ++r) {
+    load_row(o, r0 + r, x);
+    ref_row_logits(x, w, d, C, dl + r * C);
+    if (o->loss == OQ_SQUARED) dl[r] -= o->y[r0 + r];
+    else ref_softmax_dl(dl + r * C, C, o->labels[r0 + r]);
+  }
+  /* partial(j,c) = X_blk(:,j) . dl(:,c).  Eigen evaluates X_blk^T * dl with
+   * the row-major GEMV kernel (GeneralMatrixVector.h): one P-lane packet
+   * accumulator per output (lane l sums rows r = l mod P), a horizontal add
+   * (predux), then the scalar tail over the last m mod P rows. */
+  const int P = g_ref_lanes;
+  const size_t DC = (size_t)d * C;
+  double* acc = (double*)calloc(DC * (size_t)P, sizeof(double));
+  const int64_t mp = (m / P) * P;
+  for (int64_t r = 0; r < mp; ++r) {
+    load_row(o, r0 + r, x);
+    double* a = acc + (size_t)(r % P) * DC;
+    for (int c = 0; c < C; ++c) {
+      const double dv = dl[r * C + c];
+      double* pc = a + (size_t)c * d;
+      for (int j = 0; j < d; ++j) pc[j] = pc[j] + x[j] * dv;
+    }
+  }
+  for (size_t k = 0; k < DC; ++k) {
+    double lanes[4];
+    for (int l = 0; l < P; ++l) lanes[l] = acc[(size_t)l * DC + k];
+    partial[k] = predux(lanes, P);
+  }
+  for (int64_t r = mp; r < m; ++r) {
+    load_row(o, r0 + r, x);
+    for (int c = 0; c < C; ++c) {
+      const double dv = dl[r * C + c];
+      double* pc = partial + (size_t)c * d;
+      for (int j = 0; j < d; ++j) pc[j] = pc[j] + x[j] * dv;
+    }
+  }
+  free(acc);
+}
+
+typedef struct {
+  const oq_objective* o;
+  const double* w;
+  double* partials;
+  int64_t nblk;
+  int tid, nth;
+} fg_job;
+
+static void* fg_worker(void* arg) {
+  fg_job* j = (fg_job*)arg;
+  const int d = j->o->d, C = j->o->C;
+  double* x = (double*)malloc(sizeof(double) * (size_t)d);
+  double* dl = (double*)malloc(sizeof(double) * REF_BLOCK * (size_t)C);
+  for (int64_t b = j->tid; b < j->nblk; b += j->nth)
+    ref_block_partial(j->o, j->w, b, j->partials + (size_t)b * d * C, x, dl);
+  free(x);
+  free(dl);
+  return NULL;
+}
+
+/* objectives.cpp:258-311 Objective::full_gradient (threads over blocks,
+ * partials combined in block order => independent of num_threads) */
+static void ref_full_gradient(const oq_objective* o, const double* w, int num_threads, double* g) {
+  const int D = o->d * o->C;
+  const int64_t nblk = (o->n + REF_BLOCK - 1) / REF_BLOCK;
+  double* partials = (double*)malloc(sizeof(double) * (size_t)D * (size_t)nblk);
+  int nth = num_threads < 1 ? 1 : num_threads;
+  if (nth > nblk) nth = (int)nblk;
+  fg_job* jobs = (fg_job*)calloc((size_t)nth, sizeof(fg_job));
+  pthread_t* th = (pthread_t*)calloc((size_t)nth, sizeof(pthread_t));
+  for (int t = 0; t < nth; ++t) {
+    jobs[t] = (fg_job){o, w, partials, nblk, t, nth};
+    if (nth > 1) pthread_create(&th[t], NULL, fg_worker, &jobs[t]);
+  }
+  if (nth == 1) fg_worker(&jobs[0]);
+  else for (int t = 0; t < nth; ++t) pthread_join(th[t], NULL);
+  for (int k = 0; k < D; ++k) g[k] = 0.0;
+  for (int64_t b = 0; b < nblk; ++b)
+    for (int k = 0; k < D; ++k) g[k] += partials[(size_t)b * D + k];
+  for (int k = 0; k < D; ++k) g[k] = g[k] / (double)o->n;
+  for (int k = 0; k < D; ++k) g[k] += o->l2 * w[k];
+  free(partials);
+  free(jobs);
+  free(th);
+}
+
+/* objectives.cpp:225-250 component_gradient_into, REF order */
+static void ref_component_gradient(const oq_objective* o, const double* x, int64_t i, const double* w,
+                                   double* out) {
+  const int d = o->d, C = o->C;
+  if (o->loss == OQ_SQUARED) {
+    double acc = 0.0;
+    for (int j = 0; j < d; ++j) acc += x[j] * w[j];
+    const double e = acc - o->y[i];
+    for (int j = 0; j < d; ++j) out[j] = e * x[j];
+  } else {
+    double p[64];
+    ref_row_logits(x, w, d, C, p);
+    ref_softmax_dl(p, C, o->labels[i]);
+    for (int c = 0; c < C; ++c)
+      for (int j = 0; j < d; ++j) out[(size_t)c * d + j] = x[j] * p[c];
+  }
+  for (int k = 0; k < d * C; ++k) out[k] += o->l2 * w[k];
+}
+
+/* ======================================================================
+ * MIRROR mode: the B200 kernels' order.
+ * ====================================================================== */
+
+/* xor-butterfly over 32 lanes, bits 16,8,4,2,1: lane 0's final value */
+static double warp_butterfly(double* v /*[32], destroyed*/) {
+  for (int b = 16; b >= 1; b >>= 1) {
+    double nv[32];
+    for (int l = 0; l < 32; ++l) nv[l] = v[l] + v[l ^ b];
+    memcpy(v, nv, sizeof nv);
+  }
+  return v[0];
+}
+
+/* K1 row dot: thread t owns feature groups t, t+T, ... of width V;
+ * sequential fma within a thread, warp butterfly, warps summed in order. */
+static double mirror_fg_dot(const double* x, const double* w, int d, int T, int V) {
+  double warpsum[64] = {0};
+  const int nw = T / 32;
+  for (int wi = 0; wi < nw; ++wi) {
+    double v[32];
+    for (int l = 0; l < 32; ++l) {
+      const int t = wi * 32 + l;
+      double acc = 0.0;
+      for (int g = t; g * V < d; g += T)
+        for (int q = 0; q < V && g * V + q < d; ++q) acc = fma(x[g * V + q], w[g * V + q], acc);
+      v[l] = acc;
+    }
+    warpsum[wi] = warp_butterfly(v);
+  }
+  double s = warpsum[0];
+  for (int wi = 1; wi < nw; ++wi) s = s + warpsum[wi];
+  return s;
+}
+
+static void mirror_softmax_dl(double* l, int C, int label) {
+  double mx = l[0];
+  for (int c = 1; c < C; ++c) if (l[c] > mx) mx = l[c];
+  double s = 0.0;
+  for (int c = 0; c < C; ++c) l[c] = oq_mexp(l[c] - mx);
+  for (int c = 0; c < C; ++c) s = s + l[c];
+  for (int c = 0; c < C; ++c) l[c] = l[c] / s;
+  l[label] = l[label] - 1.0;
+}
+
+static double mirror_softmax_loss(const double* l, int C, int label) {
+  double mx = l[0];
+  for (int c = 1; c < C; ++c) if (l[c] > mx) mx = l[c];
+  double s = 0.0;
+  for (int c = 0; c < C; ++c) s = s + oq_mexp(l[c] - mx);
+  return (mx + oq_mlog(s)) - l[label];
+}
+
+/* pairwise tree over n items (split at the largest power of two < n) */
+static double tree_sum(const double* v, int64_t stride, int64_t n) {
+  if (n == 1) return v[0];
+  int64_t h = 1;
+  while (h * 2 < n) h *= 2;
+  return tree_sum(v, stride, h) + tree_sum(v + h * stride, stride, n - h);
+}
+
+/* K1 fused pass: per split, gradient columns accumulated by sequential fma
+ * over the split's rows, per-row loss summed sequentially; splits combined
+ * by a pairwise tree; then g = sum/n + l2*w, loss = tree/n + (0.5*l2)*|w|^2
+ * with |w|^2 and |g|^2 computed by the finalize kernel's order. */
+static void mirror_fullpass(const oq_objective* o, const double* w, const oq_plan* pl, double* g,
+                            double* loss_out) {
+  const int d = o->d, C = o->C, D = d * C;
+  const int64_t n = o->n;
+  const int S = pl->fg_splits;
+  double* part = (double*)calloc((size_t)S * D, sizeof(double));
+  double* lpart = (double*)calloc((size_t)S, sizeof(double));
+  double* x = (double*)malloc(sizeof(double) * (size_t)d);
+  double lg[64];
+  for (int s = 0; s < S; ++s) {
+    const int64_t r0 = (int64_t)((__int128)n * s / S), r1 = (int64_t)((__int128)n * (s + 1) / S);
+    double* ps = part + (size_t)s * D;
+    double la = 0.0;
+    for (int64_t r = r0; r < r1; ++r) {
+      load_row(o, r, x);
+      for (int c = 0; c < C; ++c) lg[c] = mirror_fg_dot(x, w + (size_t)c * d, d, pl->fg_threads, pl->fg_vec);
+      if (o->loss == OQ_SQUARED) {
+        const double e = lg[0] - o->y[r];
+        la = la + (0.5 * e) * e;
+        for (int j = 0; j < d; ++j) ps[j] = fma(e, x[j], ps[j]);
+      } else {
+        const int y = o->labels[r];
+        la = la + mirror_softmax_loss(lg, C, y);
+        mirror_softmax_dl(lg, C, y);
+        for (int c = 0; c < C; ++c)
+          for (int j = 0; j < d; ++j) ps[(size_t)c * d + j] = fma(lg[c], x[j], ps[(size_t)c * d + j]);
+      }
+    }
+    lpart[s] = la;
+  }
+  for (int k = 0; k < D; ++k) {
+    const double sum = tree_sum(part + k, D, S);
+    g[k] = sum / (double)n + o->l2 * w[k];
+  }
+  if (loss_out) {
+    /* finalize kernel: |w|^2 by the 256-thread strided + butterfly order */
+    double v[256];
+    for (int t = 0; t < 256; ++t) {
+      double a = 0.0;
+      for (int k = t; k < D; k += 256) a = fma(w[k], w[k], a);
+      v[t] = a;
+    }
+    double ws[8];
+    for (int wi = 0; wi < 8; ++wi) ws[wi] = warp_butterfly(v + wi * 32);
+    double sq = ws[0];
+    for (int wi = 1; wi < 8; ++wi) sq = sq + ws[wi];
+    *loss_out = tree_sum(lpart, 1, S) / (double)n + (0.5 * o->l2) * sq;
+  }
+  free(part);
+  free(lpart);
+  free(x);
+}
+
+/* finalize kernel order for |g| */
+static double mirror_norm(const double* g, int D) {
+  double v[256];
+  for (int t = 0; t < 256; ++t) {
+    double a = 0.0;
+    for (int k = t; k < D; k += 256) a = fma(g[k], g[k], a);
+    v[t] = a;
+  }
+  double ws[8];
+  for (int wi = 0; wi < 8; ++wi) ws[wi] = warp_butterfly(v + wi * 32);
+  double sq = ws[0];
+  for (int wi = 1; wi < 8; ++wi) sq = sq + ws[wi];
+  return sqrt(sq);
+}
+
+/* K3 dot order for one class c of the flat D = d*C coordinate vector:
+ * global thread tau = cta*T + tid owns flat coords [tau*m, (tau+1)*m);
+ * its partial for class c is a sequential fma over its coords of that
+ * class; lanes are combined by the warp butterfly, warps of a CTA summed in
+ * order, CTAs summed in order. */
+static void mirror_inner_dots(const double* x, const double* wa, const double* wb, int d, int C,
+                              const oq_plan* pl, double* la, double* lb) {
+  const int D = d * C, T = pl->in_threads, m = pl->in_per, NC = pl->in_ctas;
+  const int nw = T / 32;
+  for (int c = 0; c < C; ++c) {
+    double ca = 0.0, cb = 0.0;
+    for (int cta = 0; cta < NC; ++cta) {
+      double wa_s = 0.0, wb_s = 0.0;
+      for (int wi = 0; wi < nw; ++wi) {
+        double va[32], vb[32];
+        for (int l = 0; l < 32; ++l) {
+          const int64_t tau = (int64_t)cta * T + wi * 32 + l;
+          double aa = 0.0, ab = 0.0;
+          for (int64_t k = tau * m; k < (tau + 1) * m && k < D; ++k) {
+            if (k / d != c) continue;
+            const int j = (int)(k % d);
+            aa = fma(x[j], wa[k], aa);
+            ab = fma(x[j], wb[k], ab);
+          }
+          va[l] = aa;
+          vb[l] = ab;
+        }
+        const double sa = warp_butterfly(va), sb = warp_butterfly(vb);
+        wa_s = wi == 0 ? sa : wa_s + sa;
+        wb_s = wi == 0 ? sb : wb_s + sb;
+      }
+      ca = cta == 0 ? wa_s : ca + wa_s;
+      cb = cta == 0 ? wb_s : cb + wb_s;
+    }
+    la[c] = ca;
+    lb[c] = cb;
+  }
+}
+
+/* ------------------------------------------------------------ public API */
+int oq_loss(const oq_objective* o, const double* w, const oq_plan* plan, double* out) {
+  int rc = check_objective(o);
+  if (rc) return rc;
+  if (!plan) { *out = ref_loss(o, w); return OQ_OK; }
+  double* g = (double*)malloc(sizeof(double) * (size_t)o->d * o->C);
+  mirror_fullpass(o, w, plan, g, out);
+  free(g);
+  return OQ_OK;
+}
+
+int oq_full_gradient(const oq_objective* o, const double* w, int num_threads, const oq_plan* plan,
+                     double* g) {
+  int rc = check_objective(o);
+  if (rc) return rc;
+  if (num_threads < 1) { set_err("full_gradient: num_threads must be >= 1"); return OQ_INVALID_INPUT; }
+  if (!plan) ref_full_gradient(o, w, num_threads, g);
+  else mirror_fullpass(o, w, plan, g, NULL);
+  return OQ_OK;
+}
+
+int oq_component_gradient(const oq_objective* o, int64_t i, const double* w, const oq_plan* plan,
+                          double* out) {
+  int rc = check_objective(o);
+  if (rc) return rc;
+  if (i < 0 || i >= o->n) { set_err("component_gradient: index out of range"); return OQ_INVALID_INPUT; }
+  double* x = (double*)malloc(sizeof(double) * (size_t)o->d);
+  load_row(o, i, x);
+  (void)plan;
+  ref_component_gradient(o, x, i, w, out);
+  free(x);
+  return OQ_OK;
+}
+
+/* optimizers.cpp:209-216 */
+int64_t oq_resolve_inner_steps(const oq_config* cfg, int64_t n) {
+  const int64_t t = cfg->inner_steps > 0 ? cfg->inner_steps : (int64_t)cfg->full_grad_period * n;
+  return t < 1 ? -1 : t;
+}
+
+/* optimizers.cpp:218-227 FNV-1a over the iterate's bytes */
+uint64_t oq_hash_vector(const double* v, int64_t len) {
+  uint64_t h = 1469598103934665603ULL;
+  const unsigned char* p = (const unsigned char*)v;
+  const size_t nb = sizeof(double) * (size_t)len;
+  for (size_t i = 0; i < nb; ++i) {
+    h ^= p[i];
+    h *= 1099511628211ULL;
+  }
+  return h;
+}
+
+/* optimizers.cpp:36-97 (the HALP-relevant checks) */
+static int validate_config(const oq_objective* o, const oq_config* c) {
+  (void)o;
+  if (!(isfinite(c->alpha) && c->alpha >= 0.0)) { set_err("optimizer: alpha must be finite and >= 0"); return OQ_INVALID_INPUT; }
+  if (c->epochs < 0) { set_err("optimizer: epochs must be >= 0"); return OQ_INVALID_INPUT; }
+  if (c->inner_steps < 0) { set_err("optimizer: inner_steps must be >= 0"); return OQ_INVALID_INPUT; }
+  if (c->full_grad_period < 1) { set_err("optimizer: full_grad_period must be >= 1"); return OQ_INVALID_INPUT; }
+  if (!(isfinite(c->metric_every_passes) && c->metric_every_passes >= 0.0)) {
+    set_err("optimizer: metric_every_passes must be finite and >= 0");
+    return OQ_INVALID_INPUT;
+  }
+  if (!(isfinite(c->divergence_limit) && c->divergence_limit > 0.0)) {
+    set_err("optimizer: divergence_limit must be positive");
+    return OQ_INVALID_INPUT;
+  }
+  if (!(isfinite(c->delta_min) && c->delta_min > 0.0)) { set_err("optimizer: delta_min must be positive"); return OQ_INVALID_INPUT; }
+  if (c->bits < 2 || c->bits > 64) { set_err("optimizer: bits must be in [2, 64]"); return OQ_INVALID_INPUT; }
+  if (!(isfinite(c->mu) && c->mu > 0.0)) { set_err("optimizer: mu must be positive for bit-centered runs"); return OQ_INVALID_INPUT; }
+  return OQ_OK;
+}
+
+static double now_s(void) {
+  struct timespec ts;
+  clock_gettime(CLOCK_MONOTONIC, &ts);
+  return (double)ts.tv_sec + 1e-9 * (double)ts.tv_nsec;
+}
+
+/* optimizers.cpp:104-167 Recorder */
+typedef struct {
+  const oq_config* cfg;
+  oq_record* rec;
+  double t0, next_pass;
+  int D;
+} recorder;
+
+static int rec_due(const recorder* r, double pass, int forced) {
+  return forced || r->cfg->metric_every_passes <= 0.0 || pass + 1e-9 >= r->next_pass;
+}
+
+/* returns OQ_DIVERGED if the guard fired (record finalised) */
+static int rec_boundary(recorder* r, double pass, const double* w, double loss, double gn, double delta,
+                        int forced) {
+  const int bad = !(isfinite(loss) && isfinite(gn)) || loss > r->cfg->divergence_limit ||
+                  gn > r->cfg->divergence_limit;
+  if (rec_due(r, pass, forced) || bad) {
+    if (r->rec->rows_n >= r->rec->rows_cap) { set_err("oracle: rows capacity exceeded"); return OQ_CAPACITY; }
+    oq_row* row = &r->rec->rows[r->rec->rows_n++];
+    row->pass = pass;
+    row->seconds = now_s() - r->t0;
+    row->loss = loss;
+    row->grad_norm = gn;
+    row->delta = delta;
+    row->iterate_hash = oq_hash_vector(w, r->D);
+    if (r->cfg->metric_every_passes > 0.0) r->next_pass = pass + r->cfg->metric_every_passes;
+  }
+  if (bad) {
+    r->rec->status = OQ_STATUS_DIVERGED;
+    memcpy(r->rec->final_iterate, w, sizeof(double) * (size_t)r->D);
+    char m[128];
+    snprintf(m, sizeof m, "run diverged near pass %f", pass);
+    set_err(m);
+    return OQ_DIVERGED;
+  }
+  return OQ_OK;
+}
+
+/* one epoch-boundary measurement: gradient, norm, delta, loss */
+static void measure(const oq_objective* o, const double* wt, const oq_config* cfg, const oq_plan* plan,
+                    int fg_threads, double* gt, double* gn, double* delta, double* loss, double* tsec) {
+  const double t0 = now_s();
+  if (!plan) {
+    ref_full_gradient(o, wt, fg_threads, gt);
+    *gn = sqrt(ref_sqnorm(gt, (int64_t)o->d * o->C));
+  } else {
+    mirror_fullpass(o, wt, plan, gt, loss);
+    *gn = mirror_norm(gt, o->d * o->C);
+  }
+  *delta = 0.0;
+  if (isfinite(*gn) && *gn > 0.0) {
+    double s = oq_halp_scale(*gn, cfg->mu, cfg->bits);
+    *delta = s > cfg->delta_min ? s : cfg->delta_min;
+  }
+  if (!plan) *loss = ref_loss(o, wt);
+  *tsec += now_s() - t0;
+}
+
+/* optimizers.cpp:387-459 run_halp */
+int oq_run_halp(const oq_objective* o, const oq_config* cfg, const oq_plan* plan, oq_record* rec) {
+  int rc = check_objective(o);
+  if (rc) return rc;
+  rc = validate_config(o, cfg);
+  if (rc) return rc;
+  const int d = o->d, C = o->C, D = d * C;
+  const int64_t n = o->n;
+  const int64_t T = oq_resolve_inner_steps(cfg, n);
+  if (T < 1) { set_err("optimizer: epoch length must be >= 1"); return OQ_INVALID_INPUT; }
+  oq_rng sample, rounder;
+  oq_rng_init(&sample, cfg->seed, 0);  /* kSampleStream, optimizers.cpp:17 */
+  oq_rng_init(&rounder, cfg->seed, 1); /* kRoundStream,  optimizers.cpp:18 */
+
+  double* wt = (double*)calloc((size_t)D, sizeof(double));
+  if (cfg->init) memcpy(wt, cfg->init, sizeof(double) * (size_t)D);
+  double* z = (double*)calloc((size_t)D, sizeof(double));
+  double* wz = (double*)malloc(sizeof(double) * (size_t)D);
+  double* u = (double*)malloc(sizeof(double) * (size_t)D);
+  double* g1 = (double*)malloc(sizeof(double) * (size_t)D);
+  double* g2 = (double*)malloc(sizeof(double) * (size_t)D);
+  double* gt = (double*)malloc(sizeof(double) * (size_t)D);
+  double* x = (double*)malloc(sizeof(double) * (size_t)d);
+  int64_t* code = (int64_t*)calloc((size_t)D, sizeof(int64_t));
+  int64_t* snap = (int64_t*)calloc((size_t)D, sizeof(int64_t));
+
+  rec->rows_n = 0;
+  rec->status = OQ_STATUS_OK;
+  rec->steps_taken = 0;
+  rec->inner_fp_vector_ops = 0;
+  rec->fullgrad_seconds = 0.0;
+  rec->inner_seconds = 0.0;
+  recorder r = {cfg, rec, now_s(), 0.0, D};
+  int64_t steps = 0, traced = 0;
+  int converged = 0;
+  const int fgth = rec->fullgrad_threads > 0 ? rec->fullgrad_threads : 1;
+  rc = OQ_OK;
+
+  for (int k = 0; k < cfg->epochs && !converged; ++k) {
+    double gn, delta, loss;
+    measure(o, wt, cfg, plan, fgth, gt, &gn, &delta, &loss, &rec->fullgrad_seconds);
+    rc = rec_boundary(&r, (double)steps / (double)n, wt, loss, gn, delta, k == 0 || gn == 0.0);
+    if (rc) goto done;
+    if (gn == 0.0) { rec->status = OQ_STATUS_CONVERGED; converged = 1; break; }
+    /* z = Q(0): D draws, all codes 0 (optimizers.cpp:414-417) */
+    for (int q = 0; q < D; ++q) {
+      const double uu = oq_next_uniform(&rounder);
+      code[q] = oq_quantize_code(0.0, delta, cfg->bits, uu, NULL);
+      snap[q] = code[q];
+    }
+    for (int q = 0; q < D; ++q) z[q] = (double)code[q] * delta;
+    int64_t t_pick = -1;
+    if (cfg->option == 1) t_pick = (int64_t)oq_next_index(&sample, (uint64_t)T);
+    const double ti0 = now_s();
+    for (int64_t t = 0; t < T; ++t) {
+      if (t == t_pick) memcpy(snap, code, sizeof(int64_t) * (size_t)D);
+      const int64_t i = (int64_t)oq_next_index(&sample, (uint64_t)n);
+      for (int q = 0; q < D; ++q) wz[q] = wt[q] + z[q];
+      load_row(o, i, x);
+      if (!plan) {
+        ref_component_gradient(o, x, i, wz, g1);
+        ref_component_gradient(o, x, i, wt, g2);
+      } else {
+        double la[64], lb[64];
+        mirror_inner_dots(x, wz, wt, d, C, plan, la, lb);
+        if (o->loss == OQ_SQUARED) {
+          const double e1 = la[0] - o->y[i], e2 = lb[0] - o->y[i];
+          for (int j = 0; j < d; ++j) {
+            g1[j] = e1 * x[j] + o->l2 * wz[j];
+            g2[j] = e2 * x[j] + o->l2 * wt[j];
+          }
+        } else {
+          const int y = o->labels[i];
+          mirror_softmax_dl(la, C, y);
+          mirror_softmax_dl(lb, C, y);
+          for (int c = 0; c < C; ++c)
+            for (int j = 0; j < d; ++j) {
+              const size_t q = (size_t)c * d + j;
+              g1[q] = x[j] * la[c] + o->l2 * wz[q];
+              g2[q] = x[j] * lb[c] + o->l2 * wt[q];
+            }
+        }
+      }
+      int finite = 1;
+      for (int q = 0; q < D; ++q) {
+        u[q] = z[q] - cfg->alpha * ((g1[q] - g2[q]) + gt[q]);
+        if (!isfinite(u[q])) finite = 0;
+      }
+      if (!finite) {
+        /* Recorder::blowup (optimizers.cpp:156-160, 432-434) */
+        rc = rec_boundary(&r, (double)(steps + t + 1) / (double)n, u, INFINITY, INFINITY, delta, 1);
+        goto done;
+      }
+      for (int q = 0; q < D; ++q) {
+        const double uu = oq_next_uniform(&rounder);
+        code[q] = oq_quantize_code(u[q], delta, cfg->bits, uu, NULL);
+      }
+      for (int q = 0; q < D; ++q) z[q] = (double)code[q] * delta;
+      if (rec->trace_codes && traced + D <= rec->trace_cap) {
+        memcpy(rec->trace_codes + traced, code, sizeof(int64_t) * (size_t)D);
+        traced += D;
+      }
+    }
+    rec->inner_seconds += now_s() - ti0;
+    rec->inner_fp_vector_ops += (uint64_t)(8 * T);
+    if (cfg->option == 1)
+      for (int q = 0; q < D; ++q) z[q] = (double)snap[q] * delta;
+    for (int q = 0; q < D; ++q) wt[q] += z[q];
+    steps += T;
+  }
+  if (!converged) {
+    double gn, delta, loss;
+    measure(o, wt, cfg, plan, fgth, gt, &gn, &delta, &loss, &rec->fullgrad_seconds);
+    rc = rec_boundary(&r, (double)steps / (double)n, wt, loss, gn, delta, 1);
+    if (rc) goto done;
+    if (gn == 0.0) rec->status = OQ_STATUS_CONVERGED;
+  }
+  memcpy(rec->final_iterate, wt, sizeof(double) * (size_t)D);
+  rec->steps_taken = steps;
+done:
+  /* a DivergenceError's partial record keeps steps_taken == 0: the
+   * reference only assigns it after the loop (optimizers.cpp:457) */
+  if (rc == OQ_DIVERGED) rec->steps_taken = 0;
+  free(wt); free(z); free(wz); free(u); free(g1); free(g2); free(gt); free(x); free(code); free(snap);
+  return rc;
+}
