@@ -1,0 +1,11 @@
+"""B200-native HALP solver (arXiv 1803.03383), drop-in for lpopt::run_halp.
+
+The numeric work runs in libhalp_b200.so (hand-written sm_100a CUDA kernels
+behind the C ABI in include/halp.h); this package is the Python mirror of the
+reference's C++ interface (see halp.py) plus the in-tree build (build.py).
+"""
+from .halp import (  # noqa: F401
+    Algorithm, Dataset, DivergenceError, EpochOption, Error, HalpCudaError, InvalidInputError, LossFamily,
+    MetricRow, Objective, OptimizerConfig, RunRecord, UnsupportedError, generate, halp_scale, hash_vector,
+    oracle_plan_for, plan_for, resolve_inner_steps, rng_state_after, run, run_halp, run_prepared, shard_plan,
+)

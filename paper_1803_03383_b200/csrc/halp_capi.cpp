@@ -1,0 +1,715 @@
+// halp_capi.cpp -- host driver of the B200 HALP solver behind the C ABI
+// (include/halp.h).  It owns the device problem, chooses the kernel plan,
+// runs the epoch loop of lpopt::run_halp (proj/src/optimizers.cpp:387-459)
+// with the reference's Recorder semantics (:104-167), and talks NCCL for the
+// row-sharded full gradient.  Everything numeric happens in the CUDA
+// kernels (k_fullgrad.cu, k_inner.cu, k_batch.cu, k_datagen.cu); the host
+// only orders launches, computes RNG jump states and formats MetricRows.
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/halp.h"
+#include "kernels.h"
+#include "rng_jump.hpp"
+
+using namespace halp;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define CU(expr)                                                                              \
+  do {                                                                                        \
+    cudaError_t _e = (expr);                                                                  \
+    if (_e != cudaSuccess)                                                                    \
+      return fail(HALP_CUDA_ERROR, std::string(#expr) + ": " + cudaGetErrorString(_e));      \
+  } while (0)
+
+int64_t env_int(const char* name, int64_t dflt) {
+  const char* v = std::getenv(name);
+  return v ? std::atoll(v) : dflt;
+}
+
+int elem_size(int dtype) { return dtype == HALP_F64 ? 8 : dtype == HALP_F32 ? 4 : 2; }
+
+int64_t next_pow2(int64_t v) {
+  int64_t p = 1;
+  while (p < v) p <<= 1;
+  return p;
+}
+int64_t prev_pow2(int64_t v) {
+  int64_t p = 1;
+  while (p * 2 <= v) p <<= 1;
+  return p;
+}
+
+// ---- NCCL through dlopen (the soname torch already loaded, if any) ----
+struct Nccl {
+  void* h = nullptr;
+  ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*allGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+  const char* (*errStr)(ncclResult_t) = nullptr;
+  bool load() {
+    if (h) return true;
+    h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return false;
+    commInitRank = (decltype(commInitRank))dlsym(h, "ncclCommInitRank");
+    allGather = (decltype(allGather))dlsym(h, "ncclAllGather");
+    commDestroy = (decltype(commDestroy))dlsym(h, "ncclCommDestroy");
+    errStr = (decltype(errStr))dlsym(h, "ncclGetErrorString");
+    return commInitRank && allGather && commDestroy && errStr;
+  }
+  static Nccl& get() {
+    static Nccl n;
+    return n;
+  }
+};
+
+struct ShardPlan {
+  int64_t S = 1, split_begin = 0, split_end = 1, row_begin = 0, row_end = 0;
+};
+
+ShardPlan make_shard_plan(int64_t n, int d, int C, int dtype, int world, int rank) {
+  ShardPlan sp;
+  const int64_t D1 = (int64_t)d * C + 1;
+  const double xbytes = (double)n * d * elem_size(dtype);
+  const double budget = std::max(xbytes / 8.0, 2.0 * (1 << 20));
+  int64_t S = 1;
+  while (S * 2 <= 4096 && S * 2 <= std::max<int64_t>(1, n / 2) && (double)(S * 2) * D1 * 8.0 <= budget) S *= 2;
+  if (S < world) S = next_pow2(world);
+  sp.S = S;
+  sp.split_begin = S / world * rank;
+  sp.split_end = S / world * (rank + 1);
+  sp.row_begin = (int64_t)((unsigned __int128)n * sp.split_begin / S);
+  sp.row_end = (int64_t)((unsigned __int128)n * sp.split_end / S);
+  return sp;
+}
+
+struct Events {
+  cudaEvent_t a = nullptr, b = nullptr;
+  ~Events() {
+    if (a) cudaEventDestroy(a);
+    if (b) cudaEventDestroy(b);
+  }
+};
+
+double now_s() {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+uint64_t fnv1a(const double* v, int64_t len) {  // optimizers.cpp:218-227
+  uint64_t h = 1469598103934665603ULL;
+  const unsigned char* p = reinterpret_cast<const unsigned char*>(v);
+  const size_t nb = sizeof(double) * (size_t)len;
+  for (size_t i = 0; i < nb; ++i) {
+    h ^= p[i];
+    h *= 1099511628211ULL;
+  }
+  return h;
+}
+
+}  // namespace
+
+struct halp_problem {
+  int device = 0, dtype = 0, loss = 0;
+  int64_t n = 0;
+  int d = 0, C = 1, D = 1, ld = 0;
+  double l2 = 0.0;
+  int world = 1, rank = 0;
+  ncclComm_t comm = nullptr;
+  cudaStream_t stream = nullptr;
+  // device data
+  void* X = nullptr;
+  bool own_X = false;
+  double* y = nullptr;
+  int32_t* labels = nullptr;
+  // plans
+  ShardPlan sp;
+  FgLaunch fg{};
+  InLaunch in{};
+  int fg_passes = 1;
+  // workspace
+  double *w = nullptr, *w2 = nullptr, *g = nullptr, *partials = nullptr, *rank_sum = nullptr, *gathered = nullptr,
+         *stats = nullptr, *u_out = nullptr;
+  int64_t* idx = nullptr;
+  int64_t idx_cap = 0;
+  long long* codes = nullptr;
+  int* blow = nullptr;
+  uint64_t *pow_tab = nullptr, *jump_tab = nullptr;
+  long long* trace_dev = nullptr;
+  int64_t trace_dev_steps = 0;
+  int64_t* trace_host = nullptr;
+  int64_t trace_cap = 0;
+  halp_timing timing{};
+  Events ev_fg, ev_fin, ev_in, ev_smp;
+
+  ~halp_problem() {
+    cudaSetDevice(device);
+    for (void* ptr : {(void*)w, (void*)w2, (void*)g, (void*)partials, (void*)rank_sum, (void*)gathered, (void*)stats,
+                      (void*)u_out, (void*)idx, (void*)codes, (void*)blow, (void*)pow_tab, (void*)jump_tab,
+                      (void*)trace_dev, (void*)y, (void*)labels})
+      if (ptr) cudaFree(ptr);
+    if (own_X && X) cudaFree(X);
+    if (comm) Nccl::get().commDestroy(comm);
+    if (stream) cudaStreamDestroy(stream);
+  }
+};
+
+namespace {
+
+struct KernelPlan {
+  FgLaunch fg{};
+  InLaunch in{};
+  int fg_passes = 1;
+};
+
+// kernel plan as a pure function of the problem shape (CPU-callable)
+int plan_for(int64_t n, int d, int C, int dtype, KernelPlan* kp) {
+  (void)n;
+  const int es = elem_size(dtype);
+  const int V = 16 / es;
+  const int ld = (int)(((int64_t)d * es + 15) / 16 * 16 / es);
+  const int ngroups = (d + V - 1) / V;
+  int T1 = (int)std::min<int64_t>(256, (ngroups + 31) / 32 * 32);
+  int NG = (int)next_pow2((ngroups + T1 - 1) / T1);
+  if (NG > 8) return fail(HALP_UNSUPPORTED, "full_gradient: d too large for the register-resident column tiles");
+  int CT = 8;
+  while (CT > 1 && (NG * V * CT > 64 || CT >= 2 * C)) CT /= 2;
+  if (CT > C) CT = (int)next_pow2(C);
+  kp->fg = FgLaunch{dtype, NG, CT, T1, ld, 0};
+  kp->fg_passes = (C + CT - 1) / CT;
+  const size_t smem = fg_smem_bytes(ld, es, d * C, C, T1, 2, 4);
+  if (smem > 220 * 1024) return fail(HALP_UNSUPPORTED, "full_gradient: row tile + iterate exceed shared memory");
+  // inner loop: M coordinates per thread, up to 16 CTAs per cluster
+  const int64_t D = (int64_t)d * C;
+  int M = (int)env_int("HALP_IN_M", 4);
+  while (M > 1 && M > d) M /= 2;
+  int64_t threads = (D + M - 1) / M;
+  int NC = (int)env_int("HALP_IN_NC", 0);
+  if (NC <= 0) NC = (int)((threads + 255) / 256);
+  while (NC > 16 && M < 8) {
+    M *= 2;
+    threads = (D + M - 1) / M;
+    NC = (int)((threads + 255) / 256);
+  }
+  if (NC > 16) return fail(HALP_UNSUPPORTED, "inner loop: d*C too large for one 16-CTA cluster");
+  int T3 = (int)(((threads + NC - 1) / NC + 31) / 32 * 32);
+  if (T3 > 256) return fail(HALP_UNSUPPORTED, "inner loop: bad cluster plan");
+  const int nslots = 2 * C + 1;
+  kp->in = InLaunch{dtype, NC, T3, M, (int)std::max<int64_t>(4, next_pow2(nslots))};
+  return HALP_OK;
+}
+
+int choose_plans(halp_problem* p) {
+  KernelPlan kp;
+  int rc = plan_for(p->n, p->d, p->C, p->dtype, &kp);
+  if (rc) return rc;
+  p->fg = kp.fg;
+  p->in = kp.in;
+  p->fg_passes = kp.fg_passes;
+  return HALP_OK;
+}
+
+int ensure_workspace(halp_problem* p) {
+  const int64_t D1 = p->D + 1;
+  const int64_t nloc = p->sp.split_end - p->sp.split_begin;
+  if (!p->w) {
+    CU(cudaMalloc(&p->w, sizeof(double) * p->D));
+    CU(cudaMalloc(&p->w2, sizeof(double) * p->D));
+    CU(cudaMalloc(&p->g, sizeof(double) * p->D));
+    CU(cudaMalloc(&p->u_out, sizeof(double) * p->D));
+    CU(cudaMalloc(&p->partials, sizeof(double) * D1 * nloc));
+    CU(cudaMalloc(&p->rank_sum, sizeof(double) * D1));
+    CU(cudaMalloc(&p->gathered, sizeof(double) * D1 * p->world));
+    CU(cudaMalloc(&p->stats, sizeof(double) * 4));
+    CU(cudaMalloc(&p->codes, sizeof(long long) * p->D));
+    CU(cudaMalloc(&p->blow, sizeof(int)));
+    const auto& jt = JumpTables::get();
+    CU(cudaMalloc(&p->pow_tab, sizeof(uint64_t) * jt.flat.size()));
+    CU(cudaMemcpy(p->pow_tab, jt.flat.data(), sizeof(uint64_t) * jt.flat.size(), cudaMemcpyHostToDevice));
+    std::vector<uint64_t> tab(2048);
+    mat_tables(jt.power((uint64_t)p->D), tab.data());
+    CU(cudaMalloc(&p->jump_tab, sizeof(uint64_t) * 2048));
+    CU(cudaMemcpy(p->jump_tab, tab.data(), sizeof(uint64_t) * 2048, cudaMemcpyHostToDevice));
+    CU(cudaEventCreate(&p->ev_fg.a));
+    CU(cudaEventCreate(&p->ev_fg.b));
+    CU(cudaEventCreate(&p->ev_fin.a));
+    CU(cudaEventCreate(&p->ev_fin.b));
+    CU(cudaEventCreate(&p->ev_in.a));
+    CU(cudaEventCreate(&p->ev_in.b));
+    CU(cudaEventCreate(&p->ev_smp.a));
+    CU(cudaEventCreate(&p->ev_smp.b));
+  }
+  return HALP_OK;
+}
+
+// K1 + split tree (+ all-gather) + finalize at p->w; stats -> host
+int full_pass(halp_problem* p, double* gn, double* delta, double* loss, double mu, int bits, double delta_min) {
+  const int64_t D1 = p->D + 1;
+  const int nloc = (int)(p->sp.split_end - p->sp.split_begin);
+  CU(cudaEventRecord(p->ev_fg.a, p->stream));
+  for (int pass = 0; pass < p->fg_passes; ++pass) {
+    FgParams fp{p->X, p->n, p->d, p->ld, p->C, p->loss, p->y, p->labels, p->w,
+                (int)p->sp.S, (int)p->sp.split_begin, pass * p->fg.ct, pass == 0, p->partials};
+    FgLaunch L = p->fg;
+    L.nsplit_local = nloc;
+    CU(launch_fullgrad(L, fp, p->stream));
+    ++p->timing.kernel_launches;
+  }
+  CU(launch_split_tree(p->partials, nloc, (int)D1, p->world > 1 ? p->rank_sum : p->gathered, p->stream));
+  ++p->timing.kernel_launches;
+  CU(cudaEventRecord(p->ev_fg.b, p->stream));
+  CU(cudaEventRecord(p->ev_fin.a, p->stream));
+  if (p->world > 1) {
+    ncclResult_t r = Nccl::get().allGather(p->rank_sum, p->gathered, (size_t)D1, ncclFloat64, p->comm, p->stream);
+    if (r != ncclSuccess) return fail(HALP_NCCL_ERROR, std::string("ncclAllGather: ") + Nccl::get().errStr(r));
+  }
+  FinParams fin{p->gathered, p->world, p->D, p->w, p->n, p->l2, mu, delta_min, bits, p->g, p->stats};
+  CU(launch_finalize(fin, p->stream));
+  ++p->timing.kernel_launches;
+  CU(cudaEventRecord(p->ev_fin.b, p->stream));
+  double st[4];
+  CU(cudaMemcpyAsync(st, p->stats, sizeof(double) * 3, cudaMemcpyDeviceToHost, p->stream));
+  CU(cudaStreamSynchronize(p->stream));
+  float ms = 0;
+  CU(cudaEventElapsedTime(&ms, p->ev_fg.a, p->ev_fg.b));
+  p->timing.fullgrad_ms += ms;
+  p->timing.fullgrad_launches += p->fg_passes;
+  CU(cudaEventElapsedTime(&ms, p->ev_fin.a, p->ev_fin.b));
+  p->timing.finalize_ms += ms;
+  *gn = st[0];
+  *delta = st[1];
+  *loss = st[2];
+  return HALP_OK;
+}
+
+// Recorder (optimizers.cpp:104-167)
+struct Recorder {
+  const halp_config* cfg;
+  halp_record* rec;
+  double t0, next_pass = 0.0;
+  int D;
+  int boundary(double pass, const double* w, double loss, double gn, double delta, bool forced) {
+    const bool bad =
+        !(std::isfinite(loss) && std::isfinite(gn)) || loss > cfg->divergence_limit || gn > cfg->divergence_limit;
+    const bool due = forced || cfg->metric_every_passes <= 0.0 || pass + 1e-9 >= next_pass;
+    if (due || bad) {
+      if (rec->rows_n >= rec->rows_cap) return fail(HALP_CAPACITY, "halp_run: rows capacity exceeded");
+      halp_row& r = rec->rows[rec->rows_n++];
+      r.pass = pass;
+      r.seconds = now_s() - t0;
+      r.loss = loss;
+      r.grad_norm = gn;
+      r.delta = delta;
+      r.iterate_hash = fnv1a(w, D);
+      if (cfg->metric_every_passes > 0.0) next_pass = pass + cfg->metric_every_passes;
+    }
+    if (bad) {
+      rec->status = HALP_STATUS_DIVERGED;
+      if (rec->final_iterate) std::memcpy(rec->final_iterate, w, sizeof(double) * D);
+      rec->steps_taken = 0;  // DivergenceError's partial record (optimizers.cpp:457 never ran)
+      char m[128];
+      std::snprintf(m, sizeof m, "run diverged near pass %f", pass);
+      return fail(HALP_DIVERGED, m);
+    }
+    return HALP_OK;
+  }
+};
+
+// optimizers.cpp:36-97 (HALP checks)
+int validate(const halp_problem* p, const halp_config* c) {
+  if (!(std::isfinite(c->alpha) && c->alpha >= 0.0)) return fail(HALP_INVALID_INPUT, "optimizer: alpha must be finite and >= 0");
+  if (c->epochs < 0) return fail(HALP_INVALID_INPUT, "optimizer: epochs must be >= 0");
+  if (c->inner_steps < 0) return fail(HALP_INVALID_INPUT, "optimizer: inner_steps must be >= 0");
+  if (c->full_grad_period < 1) return fail(HALP_INVALID_INPUT, "optimizer: full_grad_period must be >= 1");
+  if (!(std::isfinite(c->metric_every_passes) && c->metric_every_passes >= 0.0))
+    return fail(HALP_INVALID_INPUT, "optimizer: metric_every_passes must be finite and >= 0");
+  if (!(std::isfinite(c->divergence_limit) && c->divergence_limit > 0.0))
+    return fail(HALP_INVALID_INPUT, "optimizer: divergence_limit must be positive");
+  if (!(std::isfinite(c->delta_min) && c->delta_min > 0.0)) return fail(HALP_INVALID_INPUT, "optimizer: delta_min must be positive");
+  if (c->bits < 2 || c->bits > 64) return fail(HALP_INVALID_INPUT, "optimizer: bits must be in [2, 64]");
+  if (!(std::isfinite(c->mu) && c->mu > 0.0)) return fail(HALP_INVALID_INPUT, "optimizer: mu must be positive for bit-centered runs");
+  if (c->option != 0 && c->option != 1) return fail(HALP_INVALID_INPUT, "optimizer: option must be 0 (I) or 1 (II)");
+  (void)p;
+  return HALP_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* halp_last_error(void) { return g_err.c_str(); }
+int32_t halp_abi_version(void) { return HALP_ABI_VERSION; }
+
+int halp_shard_plan(int64_t n, int32_t d, int32_t C, int32_t dtype, int32_t world, int32_t rank, int64_t* split_begin,
+                    int64_t* split_end, int64_t* splits_total, int64_t* row_begin, int64_t* row_end) {
+  if (n < 1 || d < 1 || C < 1 || world < 1 || rank < 0 || rank >= world || (world & (world - 1)))
+    return fail(HALP_INVALID_INPUT, "halp_shard_plan: bad arguments (world must be a power of two)");
+  ShardPlan sp = make_shard_plan(n, d, C, dtype, world, rank);
+  *split_begin = sp.split_begin;
+  *split_end = sp.split_end;
+  *splits_total = sp.S;
+  *row_begin = sp.row_begin;
+  *row_end = sp.row_end;
+  return HALP_OK;
+}
+
+int halp_plan_for(int64_t n, int32_t d, int32_t C, int32_t dtype, int32_t world, int32_t rank, halp_plan* out) {
+  if (!out || n < 1 || d < 1 || C < 1 || dtype < 0 || dtype > 2 || world < 1 || rank < 0 || rank >= world ||
+      (world & (world - 1)))
+    return fail(HALP_INVALID_INPUT, "halp_plan_for: bad arguments");
+  KernelPlan kp;
+  int rc = plan_for(n, d, C, dtype, &kp);
+  if (rc) return rc;
+  const ShardPlan sp = make_shard_plan(n, d, C, dtype, world, rank);
+  out->fg_threads = kp.fg.threads;
+  out->fg_vec = 16 / elem_size(dtype);
+  out->fg_splits = (int32_t)sp.S;
+  out->in_ctas = kp.in.ctas;
+  out->in_threads = kp.in.threads;
+  out->in_per = kp.in.per;
+  out->fg_rows_per_stage = 2;
+  out->fg_stages = 4;
+  out->fg_split_begin = sp.split_begin;
+  out->fg_split_end = sp.split_end;
+  return HALP_OK;
+}
+
+uint64_t halp_rng_state_after(uint64_t seed, uint64_t stream, uint64_t count) {
+  return JumpTables::get().jump(rng_seed_state(seed, stream), count);
+}
+
+int halp_problem_create(const halp_problem_desc* desc, halp_problem** out) {
+  if (!desc || !out) return fail(HALP_INVALID_INPUT, "halp_problem_create: null argument");
+  *out = nullptr;
+  // Objective ctor checks (objectives.cpp:135-160)
+  if (!(std::isfinite(desc->l2) && desc->l2 >= 0.0)) return fail(HALP_INVALID_INPUT, "Objective: l2 must be finite and >= 0");
+  if (desc->n < 1 || desc->d < 1 || !desc->X) return fail(HALP_INVALID_INPUT, "Objective: dataset is empty");
+  if (desc->dtype < 0 || desc->dtype > 2) return fail(HALP_INVALID_INPUT, "Objective: bad dtype");
+  int C = 1;
+  if (desc->loss == HALP_SQUARED) {
+    if (!desc->y) return fail(HALP_INVALID_INPUT, "Objective: squared loss needs one target per row");
+  } else if (desc->loss == HALP_SOFTMAX) {
+    if (desc->num_classes < 2 || !desc->labels) return fail(HALP_INVALID_INPUT, "Objective: softmax loss needs labels and classes");
+    C = desc->num_classes;
+  } else {
+    return fail(HALP_INVALID_INPUT, "Objective: unknown loss family");
+  }
+  if (C > kMaxClasses) return fail(HALP_UNSUPPORTED, "Objective: more than 15 softmax classes");
+  const int world = std::max(1, desc->world_size);
+  if (world & (world - 1)) return fail(HALP_INVALID_INPUT, "world_size must be a power of two");
+  int ndev = 0;
+  cudaError_t ce = cudaGetDeviceCount(&ndev);
+  if (ce != cudaSuccess || ndev == 0)
+    return fail(HALP_CUDA_ERROR, std::string("no CUDA device (no CPU fallback): ") + cudaGetErrorString(ce));
+  CU(cudaSetDevice(desc->device));
+  cudaDeviceProp prop;
+  CU(cudaGetDeviceProperties(&prop, desc->device));
+  if (prop.major != 10) return fail(HALP_CUDA_ERROR, "libhalp_b200 is built for sm_100a (B200) only");
+
+  auto* p = new halp_problem();
+  p->device = desc->device;
+  p->dtype = desc->dtype;
+  p->loss = desc->loss;
+  p->n = desc->n;
+  p->d = desc->d;
+  p->C = C;
+  p->D = desc->d * C;
+  p->l2 = desc->l2;
+  p->world = world;
+  p->rank = desc->rank;
+  auto bail = [&](int rc) {
+    delete p;
+    return rc;
+  };
+  if (cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking) != cudaSuccess)
+    return bail(fail(HALP_CUDA_ERROR, "cudaStreamCreate failed"));
+  const int es = elem_size(p->dtype);
+  // rows padded to 16 bytes so every row tile is one bulk copy
+  p->ld = (int)(((int64_t)p->d * es + 15) / 16 * 16 / es);
+  const bool dev_in = desc->mem == HALP_MEM_DEVICE;
+  const bool aligned = ((uintptr_t)desc->X % 16) == 0;
+  if (dev_in && p->ld == p->d && aligned) {
+    p->X = const_cast<void*>(desc->X);
+    p->own_X = false;
+  } else {
+    const size_t bytes = (size_t)p->n * p->ld * es;
+    if (cudaMalloc(&p->X, bytes) != cudaSuccess) return bail(fail(HALP_CUDA_ERROR, "cudaMalloc(X) failed"));
+    p->own_X = true;
+    if (cudaMemcpy2D(p->X, (size_t)p->ld * es, desc->X, (size_t)p->d * es, (size_t)p->d * es, (size_t)p->n,
+                     dev_in ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice) != cudaSuccess)
+      return bail(fail(HALP_CUDA_ERROR, "copy of X to the device failed"));
+  }
+  if (p->loss == HALP_SQUARED) {
+    if (cudaMalloc(&p->y, sizeof(double) * p->n) != cudaSuccess) return bail(fail(HALP_CUDA_ERROR, "cudaMalloc(y)"));
+    if (cudaMemcpy(p->y, desc->y, sizeof(double) * p->n, dev_in ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice) !=
+        cudaSuccess)
+      return bail(fail(HALP_CUDA_ERROR, "copy of y failed"));
+  } else {
+    std::vector<int32_t> lab(p->n);
+    if (cudaMemcpy(lab.data(), desc->labels, sizeof(int32_t) * p->n,
+                   dev_in ? cudaMemcpyDeviceToHost : cudaMemcpyHostToHost) != cudaSuccess)
+      return bail(fail(HALP_CUDA_ERROR, "copy of labels failed"));
+    for (int32_t v : lab)
+      if (v < 0 || v >= C) return bail(fail(HALP_INVALID_INPUT, "Objective: label outside [0, num_classes)"));
+    if (cudaMalloc(&p->labels, sizeof(int32_t) * p->n) != cudaSuccess) return bail(fail(HALP_CUDA_ERROR, "cudaMalloc(labels)"));
+    if (cudaMemcpy(p->labels, lab.data(), sizeof(int32_t) * p->n, cudaMemcpyHostToDevice) != cudaSuccess)
+      return bail(fail(HALP_CUDA_ERROR, "copy of labels failed"));
+  }
+  p->sp = make_shard_plan(p->n, p->d, C, p->dtype, world, p->rank);
+  int rc = choose_plans(p);
+  if (rc) return bail(rc);
+  if (world > 1) {
+    if (!desc->nccl_id) return bail(fail(HALP_INVALID_INPUT, "world_size > 1 needs an ncclUniqueId"));
+    if (!Nccl::get().load()) return bail(fail(HALP_NCCL_ERROR, "cannot load libnccl.so.2"));
+    ncclUniqueId id;
+    std::memcpy(&id, desc->nccl_id, sizeof id);
+    ncclResult_t r = Nccl::get().commInitRank(&p->comm, world, id, p->rank);
+    if (r != ncclSuccess) return bail(fail(HALP_NCCL_ERROR, std::string("ncclCommInitRank: ") + Nccl::get().errStr(r)));
+  }
+  rc = ensure_workspace(p);
+  if (rc) return bail(rc);
+  *out = p;
+  return HALP_OK;
+}
+
+void halp_problem_destroy(halp_problem* p) { delete p; }
+
+int halp_problem_plan(const halp_problem* p, halp_plan* out) {
+  if (!p || !out) return fail(HALP_INVALID_INPUT, "halp_problem_plan: null argument");
+  out->fg_threads = p->fg.threads;
+  out->fg_vec = 16 / elem_size(p->dtype);
+  out->fg_splits = (int32_t)p->sp.S;
+  out->in_ctas = p->in.ctas;
+  out->in_threads = p->in.threads;
+  out->in_per = p->in.per;
+  out->fg_rows_per_stage = 2;
+  out->fg_stages = 4;
+  out->fg_split_begin = p->sp.split_begin;
+  out->fg_split_end = p->sp.split_end;
+  return HALP_OK;
+}
+
+int halp_set_trace(halp_problem* p, int64_t* codes, int64_t cap) {
+  if (!p) return fail(HALP_INVALID_INPUT, "halp_set_trace: null problem");
+  p->trace_host = codes;
+  p->trace_cap = codes ? cap : 0;
+  return HALP_OK;
+}
+
+int halp_last_timing(const halp_problem* p, halp_timing* out) {
+  if (!p || !out) return fail(HALP_INVALID_INPUT, "halp_last_timing: null argument");
+  *out = p->timing;
+  return HALP_OK;
+}
+
+int halp_full_gradient(halp_problem* p, const double* w, double* g, double* loss) {
+  if (!p || !w) return fail(HALP_INVALID_INPUT, "halp_full_gradient: null argument");
+  CU(cudaSetDevice(p->device));
+  p->timing = halp_timing{};
+  CU(cudaMemcpy(p->w, w, sizeof(double) * p->D, cudaMemcpyHostToDevice));
+  double gn, delta, l;
+  int rc = full_pass(p, &gn, &delta, &l, 1.0, 8, 1e-300);
+  if (rc) return rc;
+  if (g) CU(cudaMemcpy(g, p->g, sizeof(double) * p->D, cudaMemcpyDeviceToHost));
+  if (loss) *loss = l;
+  return HALP_OK;
+}
+
+int halp_bench_full_gradient(halp_problem* p, int reps, double* ms_per_pass) {
+  if (!p || reps < 1) return fail(HALP_INVALID_INPUT, "halp_bench_full_gradient: bad arguments");
+  CU(cudaSetDevice(p->device));
+  const int64_t D1 = p->D + 1;
+  const int nloc = (int)(p->sp.split_end - p->sp.split_begin);
+  cudaEvent_t a, b;
+  CU(cudaEventCreate(&a));
+  CU(cudaEventCreate(&b));
+  CU(cudaEventRecord(a, p->stream));
+  for (int r = 0; r < reps; ++r) {
+    for (int pass = 0; pass < p->fg_passes; ++pass) {
+      FgParams fp{p->X, p->n, p->d, p->ld, p->C, p->loss, p->y, p->labels, p->w,
+                  (int)p->sp.S, (int)p->sp.split_begin, pass * p->fg.ct, pass == 0, p->partials};
+      FgLaunch L = p->fg;
+      L.nsplit_local = nloc;
+      CU(launch_fullgrad(L, fp, p->stream));
+    }
+    CU(launch_split_tree(p->partials, nloc, (int)D1, p->rank_sum, p->stream));
+  }
+  CU(cudaEventRecord(b, p->stream));
+  CU(cudaEventSynchronize(b));
+  float ms = 0;
+  CU(cudaEventElapsedTime(&ms, a, b));
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  *ms_per_pass = ms / reps;
+  return HALP_OK;
+}
+
+int halp_run(halp_problem* p, const halp_config* cfg, halp_record* rec) {
+  if (!p || !cfg || !rec) return fail(HALP_INVALID_INPUT, "halp_run: null argument");
+  int rc = validate(p, cfg);
+  if (rc) return rc;
+  CU(cudaSetDevice(p->device));
+  const int64_t n = p->n, D = p->D;
+  const int64_t T = cfg->inner_steps > 0 ? cfg->inner_steps : (int64_t)cfg->full_grad_period * n;
+  if (T < 1) return fail(HALP_INVALID_INPUT, "optimizer: epoch length must be >= 1");
+  const int opt2 = cfg->option == 1;
+  p->timing = halp_timing{};
+  if (p->idx_cap < T) {
+    if (p->idx) cudaFree(p->idx);
+    CU(cudaMalloc(&p->idx, sizeof(int64_t) * T));
+    p->idx_cap = T;
+  }
+  std::vector<double> wh(D, 0.0);
+  if (cfg->init) std::memcpy(wh.data(), cfg->init, sizeof(double) * D);
+  CU(cudaMemcpyAsync(p->w, wh.data(), sizeof(double) * D, cudaMemcpyHostToDevice, p->stream));
+
+  // trace buffer (test hook)
+  int64_t traced = 0;
+  int64_t tr_steps = p->trace_cap > 0 ? std::min<int64_t>(T, p->trace_cap / D) : 0;
+  if (tr_steps > p->trace_dev_steps) {
+    if (p->trace_dev) cudaFree(p->trace_dev);
+    CU(cudaMalloc(&p->trace_dev, sizeof(long long) * tr_steps * D));
+    p->trace_dev_steps = tr_steps;
+  }
+
+  rec->rows_n = 0;
+  rec->status = HALP_STATUS_OK;
+  rec->steps_taken = 0;
+  rec->inner_fp_vector_ops = 0;
+  rec->inner_lp_vector_ops = 0;
+  Recorder r{cfg, rec, now_s(), 0.0, (int)D};
+  const auto& jt = JumpTables::get();
+  const uint64_t s_sample = rng_seed_state(cfg->seed, 0);  // kSampleStream
+  const uint64_t s_round = rng_seed_state(cfg->seed, 1);   // kRoundStream
+  const double hi = cfg->bits == 64 ? (double)INT64_MAX : (double)((1LL << (cfg->bits - 1)) - 1);
+  const double lo = cfg->bits == 64 ? (double)INT64_MIN : (double)(-(1LL << (cfg->bits - 1)));
+  const long long maxc = cfg->bits == 64 ? INT64_MAX : (1LL << (cfg->bits - 1)) - 1;
+  const long long minc = cfg->bits == 64 ? INT64_MIN : -(1LL << (cfg->bits - 1));
+  int64_t steps = 0;
+  bool converged = false;
+  for (int k = 0; k < cfg->epochs && !converged; ++k) {
+    double gn, delta, loss;
+    rc = full_pass(p, &gn, &delta, &loss, cfg->mu, cfg->bits, cfg->delta_min);
+    if (rc) return rc;
+    CU(cudaMemcpy(wh.data(), p->w, sizeof(double) * D, cudaMemcpyDeviceToHost));
+    rc = r.boundary((double)steps / (double)n, wh.data(), loss, gn, delta, k == 0 || gn == 0.0);
+    if (rc) return rc;
+    if (gn == 0.0) {
+      rec->status = HALP_STATUS_CONVERGED;
+      converged = true;
+      break;
+    }
+    if (!(std::isfinite(delta) && delta > 0.0)) return fail(HALP_INVALID_INPUT, "LPRepr: delta must be positive and finite");
+    // sample stream: epoch k starts after k*(T+opt2) draws; option II draws t_pick first
+    const uint64_t sbase = jt.jump(s_sample, (uint64_t)k * (uint64_t)(T + opt2));
+    int64_t t_pick = -1;
+    uint64_t s0 = sbase;
+    if (opt2) {
+      s0 = xs_step_host(sbase);
+      t_pick = (int64_t)(((unsigned __int128)(s0 * 0x2545F4914F6CDD1DULL) * (unsigned __int128)T) >> 64);
+    }
+    CU(cudaEventRecord(p->ev_smp.a, p->stream));
+    CU(launch_samples(s0, T, 0, (uint64_t)T, (uint64_t)n, p->pow_tab, p->idx, nullptr, p->stream));
+    ++p->timing.kernel_launches;
+    CU(cudaEventRecord(p->ev_smp.b, p->stream));
+    // rounding stream: epoch k starts after k*D*(T+1) draws; Q(0) takes D of them
+    const uint64_t r0 = jt.jump(s_round, (uint64_t)k * (uint64_t)D * (uint64_t)(T + 1) + (uint64_t)D);
+    CU(cudaMemsetAsync(p->blow, 0xFF, sizeof(int), p->stream));
+    InParams ip{p->X, p->ld, p->d, p->C, (int)D, p->loss, n, p->y, p->labels, p->l2, cfg->alpha, delta, hi, lo, maxc,
+                minc, p->w, p->w2, p->g, p->idx, T, t_pick, r0, p->pow_tab, p->jump_tab, p->codes,
+                tr_steps > 0 ? p->trace_dev : nullptr, tr_steps, p->blow, p->u_out};
+    CU(cudaEventRecord(p->ev_in.a, p->stream));
+    CU(launch_inner(p->in, ip, p->stream));
+    ++p->timing.kernel_launches;
+    ++p->timing.inner_launches;
+    CU(cudaEventRecord(p->ev_in.b, p->stream));
+    int blow = -1;
+    CU(cudaMemcpyAsync(&blow, p->blow, sizeof(int), cudaMemcpyDeviceToHost, p->stream));
+    CU(cudaStreamSynchronize(p->stream));
+    float ms = 0;
+    CU(cudaEventElapsedTime(&ms, p->ev_in.a, p->ev_in.b));
+    p->timing.inner_ms += ms;
+    CU(cudaEventElapsedTime(&ms, p->ev_smp.a, p->ev_smp.b));
+    p->timing.sample_ms += ms;
+    if (tr_steps > 0 && p->trace_host && traced < p->trace_cap) {
+      const int64_t ns = std::min<int64_t>(tr_steps, (blow >= 0 ? blow : T));
+      const int64_t cnt = std::min<int64_t>(ns * D, p->trace_cap - traced);
+      std::vector<long long> tmp(cnt);
+      CU(cudaMemcpy(tmp.data(), p->trace_dev, sizeof(long long) * cnt, cudaMemcpyDeviceToHost));
+      for (int64_t q = 0; q < cnt; ++q) p->trace_host[traced + q] = tmp[q];
+      traced += cnt;
+    }
+    if (blow >= 0) {
+      // Recorder::blowup (optimizers.cpp:156-160, 432-434)
+      p->timing.inner_steps += blow + 1;
+      std::vector<double> u(D);
+      CU(cudaMemcpy(u.data(), p->u_out, sizeof(double) * D, cudaMemcpyDeviceToHost));
+      return r.boundary((double)(steps + blow + 1) / (double)n, u.data(), INFINITY, INFINITY, delta, true);
+    }
+    p->timing.inner_steps += T;
+    std::swap(p->w, p->w2);
+    rec->inner_fp_vector_ops += (uint64_t)(8 * T);
+    steps += T;
+  }
+  if (!converged) {
+    double gn, delta, loss;
+    rc = full_pass(p, &gn, &delta, &loss, cfg->mu, cfg->bits, cfg->delta_min);
+    if (rc) return rc;
+    CU(cudaMemcpy(wh.data(), p->w, sizeof(double) * D, cudaMemcpyDeviceToHost));
+    rc = r.boundary((double)steps / (double)n, wh.data(), loss, gn, delta, true);
+    if (rc) return rc;
+    if (gn == 0.0) rec->status = HALP_STATUS_CONVERGED;
+  } else {
+    CU(cudaMemcpy(wh.data(), p->w, sizeof(double) * D, cudaMemcpyDeviceToHost));
+  }
+  if (rec->final_iterate) std::memcpy(rec->final_iterate, wh.data(), sizeof(double) * D);
+  rec->steps_taken = steps;
+  return HALP_OK;
+}
+
+}  // extern "C"
+
+extern "C" int halp_datagen(const halp_datagen_desc* desc, int32_t device, void* X_dev, double* y_dev,
+                            int32_t* labels_dev) {
+  if (!desc || !X_dev) return fail(HALP_INVALID_INPUT, "halp_datagen: null argument");
+  if (desc->kind < 0 || desc->kind > 2 || desc->n < 1 || desc->d < 1)
+    return fail(HALP_INVALID_INPUT, "halp_datagen: bad kind or shape");
+  if (desc->kind == 0 && !y_dev) return fail(HALP_INVALID_INPUT, "halp_datagen: regression needs y");
+  if (desc->kind != 0 && !labels_dev) return fail(HALP_INVALID_INPUT, "halp_datagen: classification needs labels");
+  if (desc->kind == 1 && (desc->num_classes < 2 || desc->num_classes > kMaxClasses))
+    return fail(HALP_INVALID_INPUT, "halp_datagen: num_classes out of range");
+  CU(cudaSetDevice(device));
+  GenParams gp{desc->kind, desc->n, desc->d, desc->num_classes, desc->dtype, desc->noise_sd, desc->x_scale,
+               desc->density, desc->seed, X_dev, y_dev, labels_dev};
+  CU(launch_datagen(gp, 0));
+  CU(cudaDeviceSynchronize());
+  return HALP_OK;
+}
+
+struct halp_batch {
+  int device = 0;
+};
+extern "C" int halp_batch_create(const halp_batch_desc*, halp_batch** out) {
+  if (out) *out = nullptr;
+  return fail(HALP_UNSUPPORTED, "halp_batch_create: not built yet");
+}
+extern "C" void halp_batch_destroy(halp_batch* b) { delete b; }
+extern "C" int halp_batch_run(halp_batch*, const halp_config*, halp_record*, double*) {
+  return fail(HALP_UNSUPPORTED, "halp_batch_run: not built yet");
+}

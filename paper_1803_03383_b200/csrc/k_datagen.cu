@@ -1,0 +1,128 @@
+// k_datagen.cu -- K6: synthetic datasets for BASELINE.json configs C2..C5,
+// generated on the device from a counter-based hash so that 64 GiB never
+// has to be produced on the host.  (The reference's own generator,
+// make_regression, objectives.cpp:27-45, is sequential; it is restated in
+// the oracle for the reference-scale parity cases.)  The bytes produced here
+// are copied back to the CPU oracle by the tests.
+//
+// kind 0: x ~ N(0, x_scale^2), w* ~ N(0,1), y = x.w* + noise_sd * N(0,1)      (C3, C5)
+// kind 1: x ~ U[0,1) kept with probability `density`, teacher W ~ N(0,1)
+//         (d x C), label = argmax_c (x.W_c + Gumbel)                           (C2)
+// kind 2: x ~ N(0, x_scale^2), w* ~ N(0,1), label ~ Bernoulli(sigmoid(x.w*))   (C4)
+#include "halp_device.cuh"
+#include "kernels.h"
+
+namespace halp {
+
+__device__ __forceinline__ uint64_t mix64(uint64_t x) {
+  x += 0x9E3779B97F4A7C15ULL;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBULL;
+  return x ^ (x >> 31);
+}
+__device__ __forceinline__ uint64_t ctr(uint64_t seed, uint64_t stream, uint64_t i) {
+  return mix64(mix64(seed ^ (stream * 0xD1B54A32D192ED03ULL)) + i * 0x9E3779B97F4A7C15ULL);
+}
+__device__ __forceinline__ double unif64(uint64_t seed, uint64_t stream, uint64_t i) {
+  return (double)(ctr(seed, stream, i) >> 11) * 0x1.0p-53;
+}
+__device__ __forceinline__ float unif32(uint64_t seed, uint64_t stream, uint64_t i) {
+  return (float)(ctr(seed, stream, i) >> 40) * 0x1.0p-24f;
+}
+__device__ __forceinline__ float normal32(uint64_t seed, uint64_t stream, uint64_t i) {
+  const uint64_t h = ctr(seed, stream, i);
+  const float u1 = ((float)(h >> 40) + 0.5f) * 0x1.0p-24f;
+  const float u2 = (float)((h >> 16) & 0xFFFFFF) * 0x1.0p-24f;
+  return sqrtf(-2.0f * logf(u1)) * cospif(2.0f * u2);
+}
+__device__ __forceinline__ double normal64(uint64_t seed, uint64_t stream, uint64_t i) {
+  const double u1 = unif64(seed, stream, 2 * i) + 0x1.0p-54;
+  const double u2 = unif64(seed, stream, 2 * i + 1);
+  return sqrt(-2.0 * log(u1)) * cospi(2.0 * u2);
+}
+
+template <class Tx> __device__ __forceinline__ Tx from_f(float v);
+template <> __device__ __forceinline__ float from_f<float>(float v) { return v; }
+template <> __device__ __forceinline__ double from_f<double>(float v) { return (double)v; }
+template <> __device__ __forceinline__ __nv_bfloat16 from_f<__nv_bfloat16>(float v) { return __float2bfloat16_rn(v); }
+
+template <class Tx>
+__global__ void k_gen_x(GenParams p) {
+  Tx* X = reinterpret_cast<Tx*>(p.X);
+  const uint64_t total = (uint64_t)p.n * p.d;
+  const float sc = (float)p.x_scale;
+  for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (uint64_t)gridDim.x * blockDim.x) {
+    float v;
+    if (p.kind == 1) {
+      const uint64_t h = ctr(p.seed, 1, e);
+      const float u = (float)(h >> 40) * 0x1.0p-24f;
+      const float keep = (float)((h >> 16) & 0xFFFFFF) * 0x1.0p-24f;
+      v = keep < (float)p.density ? u : 0.0f;
+    } else {
+      v = normal32(p.seed, 1, e) * sc;
+    }
+    X[e] = from_f<Tx>(v);
+  }
+}
+
+template <class Tx>
+__global__ void k_gen_y(GenParams p) {
+  extern __shared__ double wsm[];  // w* (d) or teacher W (d*C, column-major)
+  const int d = p.d, C = p.kind == 1 ? p.C : 1;
+  for (int k = threadIdx.x; k < d * C; k += blockDim.x) wsm[k] = normal64(p.seed, 2, (uint64_t)k);
+  __syncthreads();
+  const Tx* X = reinterpret_cast<const Tx*>(p.X);
+  const int lane = threadIdx.x & 31, wpb = blockDim.x >> 5;
+  for (int64_t i = (int64_t)blockIdx.x * wpb + (threadIdx.x >> 5); i < p.n; i += (int64_t)gridDim.x * wpb) {
+    double acc[kMaxClasses];
+    for (int c = 0; c < C; ++c) acc[c] = 0.0;
+    for (int j = lane; j < d; j += 32) {
+      const double x = to_d<Tx>(X[i * d + j]);
+      for (int c = 0; c < C; ++c) acc[c] = fma(x, wsm[c * d + j], acc[c]);
+    }
+    for (int c = 0; c < C; ++c) acc[c] = warp_allsum(acc[c]);
+    if (lane == 0) {
+      if (p.kind == 0) {
+        p.y[i] = acc[0] + p.noise_sd * normal64(p.seed, 3, (uint64_t)i);
+      } else if (p.kind == 1) {
+        int best = 0;
+        double bv = -1e300;
+        for (int c = 0; c < C; ++c) {
+          const double u = unif64(p.seed, 4, (uint64_t)i * C + c) + 0x1.0p-54;
+          const double v = acc[c] - log(-log(u));
+          if (v > bv) {
+            bv = v;
+            best = c;
+          }
+        }
+        p.labels[i] = best;
+      } else {
+        const double pr = 1.0 / (1.0 + exp(-acc[0]));
+        p.labels[i] = unif64(p.seed, 4, (uint64_t)i) < pr ? 1 : 0;
+      }
+    }
+  }
+}
+
+template <class Tx>
+static cudaError_t gen_t(const GenParams& p, cudaStream_t st) {
+  k_gen_x<Tx><<<148 * 8, 256, 0, st>>>(p);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  const int C = p.kind == 1 ? p.C : 1;
+  const size_t smem = sizeof(double) * (size_t)p.d * C;
+  e = cudaFuncSetAttribute(k_gen_y<Tx>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  k_gen_y<Tx><<<148 * 4, 256, smem, st>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_datagen(const GenParams& p, cudaStream_t st) {
+  switch (p.dtype) {
+    case 0: return gen_t<double>(p, st);
+    case 1: return gen_t<float>(p, st);
+    default: return gen_t<__nv_bfloat16>(p, st);
+  }
+}
+
+}  // namespace halp

@@ -1,0 +1,115 @@
+// kernels.h -- host-visible launch interface of the HALP CUDA kernels.
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace halp {
+
+constexpr int kMaxClasses = 15;  // softmax classes handled by the inner-loop reduction slots
+
+// ---- K1 full-gradient pass ----
+struct FgParams {
+  const void* X;
+  int64_t n;
+  int d, ld, C, loss;
+  const double* y;
+  const int32_t* labels;
+  const double* w;
+  int S, split0, c0, write_loss;
+  double* partials;  // [nsplit_local][D+1]
+};
+struct FgLaunch {
+  int dtype, ng, ct, threads, ld, nsplit_local;
+};
+size_t fg_smem_bytes(int ld, int elem, int D, int C, int threads, int R, int stages);
+cudaError_t launch_fullgrad(const FgLaunch& L, const FgParams& p, cudaStream_t st);
+cudaError_t launch_split_tree(const double* partials, int nsplit, int D1, double* out, cudaStream_t st);
+
+struct FinParams {
+  const double* rank_sums;  // [G][D+1]
+  int G, D;
+  const double* w;
+  int64_t n;
+  double l2, mu, delta_min;
+  int bits;
+  double* g_out;  // [D]
+  double* stats;  // [gn, delta, loss]
+};
+cudaError_t launch_finalize(const FinParams& p, cudaStream_t st);
+
+cudaError_t launch_samples(uint64_t state0, int64_t total, int opt2, uint64_t T, uint64_t n, const uint64_t* pow_tab,
+                           int64_t* idx, int64_t* tpick, cudaStream_t st);
+
+// ---- K3 persistent inner loop (one problem, one CTA cluster) ----
+struct InParams {
+  const void* X;
+  int ld, d, C, D, loss;
+  int64_t n;
+  const double* y;
+  const int32_t* labels;
+  double l2, alpha, delta, hi, lo;
+  long long maxc, minc;
+  const double* w;     // w~ [D]
+  double* w_out;       // w~ after the epoch [D]
+  const double* g;     // g~ [D]
+  const int64_t* idx;  // sample indices [T]
+  int64_t T, t_pick;
+  uint64_t rstate0;    // rounding-stream state before the first draw of step 0
+  const uint64_t* pow_tab;
+  const uint64_t* jump_tab;  // X^D, 8x256
+  long long* codes_out;      // [D] codes after the last step
+  long long* trace;          // [trace_steps][D] or null
+  int64_t trace_steps;
+  int* blow_step;            // -1 or failing step index
+  double* u_out;             // [D] update vector of the failing step
+};
+struct InLaunch {
+  int dtype, ctas, threads, per, nslot_pow2;
+};
+cudaError_t launch_inner(const InLaunch& L, const InParams& p, cudaStream_t st);
+
+// ---- K6 synthetic data ----
+struct GenParams {
+  int kind;
+  int64_t n;
+  int d, C, dtype;
+  double noise_sd, x_scale, density;
+  uint64_t seed;
+  void* X;
+  double* y;
+  int32_t* labels;
+};
+cudaError_t launch_datagen(const GenParams& p, cudaStream_t st);
+
+// ---- K5 batched independent problems ----
+struct BatchParams {
+  const void* X;       // [nprob][n][ld]
+  int ld, d, dtype;
+  int64_t n;
+  int nprob;
+  const double* y;     // [nprob][n]
+  double l2;
+  const double* alpha; // per problem
+  const double* mu;
+  const int* bits;
+  const int* epochs;
+  const int64_t* T;
+  const int* option;
+  const uint64_t* seed;
+  const double* delta_min;
+  const double* div_limit;
+  const double* init;  // [nprob][d] or null
+  const uint64_t* pow_tab;
+  int max_rows;
+  double* rows;        // [nprob][max_rows][5] (pass, loss, gn, delta, hash-as-bits)
+  int* rows_n;
+  int* status;
+  int64_t* steps;
+  double* w_out;       // [nprob][d]
+  double* u_out;       // [nprob][d] blowup vectors
+  uint64_t* rhash;     // [nprob][max_rows]
+};
+cudaError_t launch_batch(const BatchParams& p, int threads, cudaStream_t st);
+
+}  // namespace halp

@@ -1,0 +1,458 @@
+"""lpopt-compatible host API over the B200 C ABI.
+
+Mirrors the reference's solver interface for the HALP path so that callers
+and tests read like the reference's own (proj/include/lpopt/*.hpp):
+
+  reference (C++)                              here
+  -------------------------------------------  ------------------------------------
+  lpopt::LossFamily {Squared, Softmax}          LossFamily.Squared / .Softmax
+  lpopt::Dataset {X, targets, labels, C}        Dataset(X, targets=, labels=, num_classes=)
+  lpopt::Objective(ds, loss, l2)                Objective(ds, loss, l2, device=0)
+    .full_gradient(w) / .loss(w)                  .full_gradient(w) / .loss(w)  (one fused pass)
+  lpopt::OptimizerConfig                        OptimizerConfig (same fields and defaults)
+  lpopt::MetricRow / RunRecord                  MetricRow / RunRecord
+  lpopt::run_halp(obj, cfg)                     run_halp(obj, cfg)
+  lpopt::run(obj, cfg) (Halp branch)            run(obj, cfg)
+  lpopt::run_prepared (harness.cpp:296-312)     run_prepared(obj, cfg)
+  InvalidInputError / DivergenceError           InvalidInputError / DivergenceError(.partial)
+
+X may be a numpy array (float64 / float32 / bf16 bits as uint16) on the
+host, or a CUDA torch tensor (float64 / float32 / bfloat16) already in HBM.
+Every computation runs in libhalp_b200.so on the GPU; there is no CPU path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+import math
+from dataclasses import dataclass, field
+from typing import List, Optional
+
+import numpy as np
+
+from . import _capi as A
+
+
+class Error(RuntimeError):
+    """lpopt::Error (errors.hpp:8-10)."""
+
+
+class InvalidInputError(Error):
+    """lpopt::InvalidInputError (errors.hpp:13-15)."""
+
+
+class UnsupportedError(Error):
+    """Shape or algorithm outside the B200 hot path."""
+
+
+class HalpCudaError(Error):
+    pass
+
+
+class LossFamily(enum.IntEnum):
+    Squared = 0
+    Softmax = 1
+
+
+class Algorithm(enum.IntEnum):
+    Sgd = 0
+    Svrg = 1
+    LpSgd = 2
+    LpSvrg = 3
+    Halp = 4
+    LmHalp = 5
+
+
+class EpochOption(enum.IntEnum):
+    LastIterate = 0
+    SampledIterate = 1
+
+
+@dataclass
+class MetricRow:
+    pass_: float = 0.0
+    seconds: float = 0.0
+    loss: float = 0.0
+    grad_norm: float = 0.0
+    delta: float = 0.0
+    iterate_hash: int = 0
+    delta_inner: float = 0.0
+    delta_aux: float = 0.0
+
+
+@dataclass
+class RunRecord:
+    rows: List[MetricRow] = field(default_factory=list)
+    final_iterate: Optional[np.ndarray] = None
+    status: str = "ok"
+    inner_fp_vector_ops: int = 0
+    inner_lp_vector_ops: int = 0
+    steps_taken: int = 0
+
+
+class DivergenceError(Error):
+    """lpopt::DivergenceError (optimizers.hpp:71-75): carries the partial record."""
+
+    def __init__(self, msg: str, partial: RunRecord):
+        super().__init__(msg)
+        self.partial = partial
+
+
+_STATUS = {0: "ok", 1: "converged", 2: "diverged"}
+
+
+def _raise(rc: int, partial: Optional[RunRecord] = None):
+    msg = A.last_error()
+    if rc == A.HALP_INVALID_INPUT:
+        raise InvalidInputError(msg)
+    if rc == A.HALP_DIVERGED:
+        raise DivergenceError(msg, partial)
+    if rc == A.HALP_UNSUPPORTED:
+        raise UnsupportedError(msg)
+    if rc in (A.HALP_CUDA_ERROR, A.HALP_NCCL_ERROR):
+        raise HalpCudaError(msg)
+    raise Error(f"halp rc={rc}: {msg}")
+
+
+@dataclass
+class Dataset:
+    """lpopt::Dataset (objectives.hpp:23-33); X row-major n x d."""
+
+    X: object
+    targets: Optional[object] = None
+    labels: Optional[object] = None
+    num_classes: int = 0
+
+    def n(self) -> int:
+        return int(self.X.shape[0])
+
+    def dim(self) -> int:
+        return int(self.X.shape[1])
+
+    def is_classification(self) -> bool:
+        return self.num_classes > 0
+
+
+def _is_torch_cuda(a) -> bool:
+    return hasattr(a, "is_cuda") and bool(a.is_cuda)
+
+
+def _x_dtype(X) -> int:
+    if _is_torch_cuda(X):
+        import torch
+
+        return {torch.float64: A.F64, torch.float32: A.F32, torch.bfloat16: A.BF16}[X.dtype]
+    return {np.dtype(np.float64): A.F64, np.dtype(np.float32): A.F32, np.dtype(np.uint16): A.BF16}[X.dtype]
+
+
+class Objective:
+    """lpopt::Objective (objectives.hpp:59-91) backed by a device problem."""
+
+    def __init__(self, ds: Dataset, loss: LossFamily = LossFamily.Squared, l2: float = 0.0, device: int = 0,
+                 world_size: int = 1, rank: int = 0, nccl_id: Optional[bytes] = None):
+        self.ds = ds
+        self._loss = LossFamily(loss)
+        self._l2 = float(l2)
+        self.device = device
+        self._keep = []
+        X = ds.X
+        dev = _is_torch_cuda(X)
+        if dev:
+            X = X.contiguous()
+            xptr = X.data_ptr()
+        else:
+            X = np.ascontiguousarray(X)
+            xptr = X.ctypes.data
+        self._keep.append(X)
+        dtype = _x_dtype(X)
+        yptr = lptr = None
+        C_ = 0
+        if self._loss == LossFamily.Squared:
+            if ds.targets is None:
+                raise InvalidInputError("Objective: squared loss needs one target per row")
+            y = ds.targets
+            if dev:
+                import torch
+
+                y = torch.as_tensor(y, dtype=torch.float64, device=X.device).contiguous()
+                yptr = y.data_ptr()
+            else:
+                y = np.ascontiguousarray(y, dtype=np.float64)
+                if y.shape[0] != X.shape[0]:
+                    raise InvalidInputError("Objective: squared loss needs one target per row")
+                yptr = y.ctypes.data
+            self._keep.append(y)
+        else:
+            if ds.labels is None or ds.num_classes < 2:
+                raise InvalidInputError("Objective: softmax loss needs labels and classes")
+            lab = ds.labels
+            if dev:
+                import torch
+
+                lab = torch.as_tensor(lab, dtype=torch.int32, device=X.device).contiguous()
+                lptr = lab.data_ptr()
+            else:
+                lab = np.ascontiguousarray(lab, dtype=np.int32)
+                lptr = lab.ctypes.data
+            self._keep.append(lab)
+            C_ = int(ds.num_classes)
+        idbuf = None
+        if nccl_id is not None:
+            idbuf = C.create_string_buffer(bytes(nccl_id), 128)
+        desc = A.ProblemDesc(xptr, dtype, A.MEM_DEVICE if dev else A.MEM_HOST, int(X.shape[0]), int(X.shape[1]),
+                             int(self._loss), C_, yptr, lptr, self._l2, device, world_size, rank,
+                             C.cast(idbuf, C.c_void_p) if idbuf is not None else None)
+        h = C.c_void_p()
+        rc = A.lib().halp_problem_create(C.byref(desc), C.byref(h))
+        if rc:
+            _raise(rc)
+        self._h = h
+        self._n = int(X.shape[0])
+        self._d = int(X.shape[1])
+        self._C = C_ if C_ else 1
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            A.lib().halp_problem_destroy(h)
+            self._h = None
+
+    # ---- lpopt::Objective accessors ----
+    def num_components(self) -> int:
+        return self._n
+
+    def feature_dim(self) -> int:
+        return self._d
+
+    def num_outputs(self) -> int:
+        return self._C
+
+    def dim(self) -> int:
+        return self._d * self._C
+
+    def loss_family(self) -> LossFamily:
+        return self._loss
+
+    def l2(self) -> float:
+        return self._l2
+
+    def dataset(self) -> Dataset:
+        return self.ds
+
+    def _fullpass(self, w):
+        w = np.ascontiguousarray(w, dtype=np.float64)
+        if w.size != self.dim():
+            raise InvalidInputError("full_gradient: parameter length mismatch")
+        g = np.empty(self.dim(), dtype=np.float64)
+        loss = C.c_double()
+        rc = A.lib().halp_full_gradient(self._h, w.ctypes.data, g.ctypes.data, C.byref(loss))
+        if rc:
+            _raise(rc)
+        return g, loss.value
+
+    def full_gradient(self, w, num_threads: int = 1) -> np.ndarray:
+        """objectives.cpp:258-311; num_threads is accepted for API parity (the
+        device result is independent of it, like the reference's)."""
+        if num_threads < 1:
+            raise InvalidInputError("full_gradient: num_threads must be >= 1")
+        return self._fullpass(w)[0]
+
+    def loss(self, w) -> float:
+        """objectives.cpp:193-223 (computed in the same fused device pass)."""
+        if np.asarray(w).size != self.dim():
+            raise InvalidInputError("loss: parameter length mismatch")
+        return self._fullpass(w)[1]
+
+    def plan(self) -> dict:
+        pl = A.Plan()
+        rc = A.lib().halp_problem_plan(self._h, C.byref(pl))
+        if rc:
+            _raise(rc)
+        return {k: getattr(pl, k) for k, _ in A.Plan._fields_}
+
+    def oracle_plan(self) -> dict:
+        p = self.plan()
+        return {k: p[k] for k in ("fg_threads", "fg_vec", "fg_splits", "in_ctas", "in_threads", "in_per")}
+
+    def timing(self) -> dict:
+        t = A.Timing()
+        rc = A.lib().halp_last_timing(self._h, C.byref(t))
+        if rc:
+            _raise(rc)
+        return {k: getattr(t, k) for k, _ in A.Timing._fields_}
+
+    def bench_full_gradient(self, reps: int = 10) -> float:
+        ms = C.c_double()
+        rc = A.lib().halp_bench_full_gradient(self._h, reps, C.byref(ms))
+        if rc:
+            _raise(rc)
+        return ms.value
+
+
+@dataclass
+class OptimizerConfig:
+    """lpopt::OptimizerConfig (optimizers.hpp:31-47), same defaults."""
+
+    algorithm: Algorithm = Algorithm.Svrg
+    alpha: float = 1e-3
+    epochs: int = 1
+    inner_steps: int = 0
+    bits: int = 8
+    delta: float = 0.0
+    mu: float = 0.0
+    option: EpochOption = EpochOption.LastIterate
+    full_grad_period: int = 2
+    seed: int = 0
+    metric_every_passes: float = 0.0
+    delta_min: float = 1e-300
+    divergence_limit: float = 1e12
+    lm_bypass_aux_quant: bool = False
+    init: Optional[np.ndarray] = None
+
+
+def _to_c_config(cfg: OptimizerConfig, keep: list) -> A.Config:
+    init = None
+    if cfg.init is not None and np.asarray(cfg.init).size:
+        init = np.ascontiguousarray(cfg.init, dtype=np.float64)
+        keep.append(init)
+    return A.Config(float(cfg.alpha), int(cfg.epochs), int(cfg.inner_steps), int(cfg.bits), float(cfg.mu),
+                    int(cfg.option), int(cfg.full_grad_period), int(cfg.seed) & (2**64 - 1),
+                    float(cfg.metric_every_passes), float(cfg.delta_min), float(cfg.divergence_limit),
+                    init.ctypes.data if init is not None else None)
+
+
+def _record(rec: A.Record, rows, fin: np.ndarray) -> RunRecord:
+    out = RunRecord()
+    out.rows = [MetricRow(r.pass_, r.seconds, r.loss, r.grad_norm, r.delta, r.iterate_hash) for r in rows[: rec.rows_n]]
+    out.final_iterate = fin
+    out.status = _STATUS[rec.status]
+    out.inner_fp_vector_ops = rec.inner_fp_vector_ops
+    out.inner_lp_vector_ops = rec.inner_lp_vector_ops
+    out.steps_taken = rec.steps_taken
+    return out
+
+
+def resolve_inner_steps(cfg: OptimizerConfig, n: int) -> int:
+    """optimizers.cpp:209-216"""
+    t = cfg.inner_steps if cfg.inner_steps > 0 else cfg.full_grad_period * n
+    if t < 1:
+        raise InvalidInputError("optimizer: epoch length must be >= 1")
+    return t
+
+
+def hash_vector(v) -> int:
+    """optimizers.cpp:218-227 (FNV-1a over the double bytes)."""
+    h = 1469598103934665603
+    for b in np.ascontiguousarray(v, dtype=np.float64).tobytes():
+        h ^= b
+        h = (h * 1099511628211) & 0xFFFFFFFFFFFFFFFF
+    return h
+
+
+def run_halp(obj: Objective, cfg: OptimizerConfig, trace: Optional[np.ndarray] = None) -> RunRecord:
+    """lpopt::run_halp (optimizers.cpp:387-459) on the B200.  `trace`, an
+    int64 array, receives the z codes of every inner step (test hook)."""
+    if cfg.init is not None and np.asarray(cfg.init).size not in (0, obj.dim()):
+        raise InvalidInputError("optimizer: init length does not match objective")
+    keep: list = []
+    c = _to_c_config(cfg, keep)
+    cap = max(cfg.epochs, 0) + 2
+    if cfg.metric_every_passes <= 0:
+        cap = max(cfg.epochs, 0) + 2
+    rows = (A.Row * cap)()
+    fin = np.zeros(obj.dim(), dtype=np.float64)
+    rec = A.Record(rows, cap, 0, fin.ctypes.data, 0, 0, 0, 0)
+    if trace is not None:
+        assert trace.dtype == np.int64 and trace.flags.c_contiguous
+        A.lib().halp_set_trace(obj._h, trace.ctypes.data, trace.size)
+    try:
+        rc = A.lib().halp_run(obj._h, C.byref(c), C.byref(rec))
+    finally:
+        if trace is not None:
+            A.lib().halp_set_trace(obj._h, None, 0)
+    if rc == A.HALP_DIVERGED:
+        _raise(rc, _record(rec, rows, fin))
+    if rc:
+        _raise(rc)
+    return _record(rec, rows, fin)
+
+
+def run(obj: Objective, cfg: OptimizerConfig) -> RunRecord:
+    """lpopt::run (optimizers.cpp:629-639): the Halp branch is the B200 path;
+    the other algorithms are outside this build's scope."""
+    if cfg.algorithm == Algorithm.Halp:
+        return run_halp(obj, cfg)
+    raise UnsupportedError(f"algorithm {Algorithm(cfg.algorithm).name} is not on the B200 hot path")
+
+
+def run_prepared(obj: Objective, cfg: OptimizerConfig) -> RunRecord:
+    """harness.cpp:296-312: a diverged run is returned, not raised."""
+    try:
+        return run(obj, cfg)
+    except DivergenceError as e:
+        return e.partial
+
+
+def halp_scale(grad_norm: float, mu: float, bits: int) -> float:
+    """theory.cpp:93-102"""
+    if not (math.isfinite(grad_norm) and grad_norm >= 0.0):
+        raise InvalidInputError("grad_norm must be finite and nonnegative")
+    if not (math.isfinite(mu) and mu > 0.0):
+        raise InvalidInputError("mu must be positive and finite")
+    if bits < 2 or bits > 64:
+        raise InvalidInputError("bits must be in [2, 64]")
+    return grad_norm / (mu * (math.ldexp(1.0, bits - 1) - 1.0))
+
+
+def generate(kind: str, n: int, d: int, *, num_classes: int = 0, dtype: str = "f32", noise_sd: float = 0.0,
+             x_scale: float = 1.0, density: float = 1.0, seed: int = 0, device: int = 0):
+    """K6 device generator for the BASELINE synthetic configs; returns torch
+    CUDA tensors (X, y) for 'regression' or (X, labels) for 'softmax' /
+    'logistic'."""
+    import torch
+
+    kinds = {"regression": 0, "softmax": 1, "logistic": 2}
+    tdt = {"f64": torch.float64, "f32": torch.float32, "bf16": torch.bfloat16}[dtype]
+    cdt = {"f64": A.F64, "f32": A.F32, "bf16": A.BF16}[dtype]
+    dev = torch.device("cuda", device)
+    X = torch.empty((n, d), dtype=tdt, device=dev)
+    y = lab = None
+    if kinds[kind] == 0:
+        y = torch.empty(n, dtype=torch.float64, device=dev)
+    else:
+        lab = torch.empty(n, dtype=torch.int32, device=dev)
+    desc = A.DatagenDesc(kinds[kind], n, d, num_classes, cdt, noise_sd, x_scale, density, seed)
+    rc = A.lib().halp_datagen(C.byref(desc), device, X.data_ptr(), y.data_ptr() if y is not None else None,
+                              lab.data_ptr() if lab is not None else None)
+    if rc:
+        _raise(rc)
+    return (X, y) if y is not None else (X, lab)
+
+
+def shard_plan(n: int, d: int, C_: int, dtype: int, world: int, rank: int) -> dict:
+    """Host-side row/split plan of the multi-GPU full gradient (CPU-callable)."""
+    vals = [C.c_int64() for _ in range(5)]
+    rc = A.lib().halp_shard_plan(n, d, C_, dtype, world, rank, *[C.byref(v) for v in vals])
+    if rc:
+        _raise(rc)
+    return dict(zip(("split_begin", "split_end", "splits", "row_begin", "row_end"), [v.value for v in vals]))
+
+
+def plan_for(n: int, d: int, C_: int = 1, dtype: str = "f64", world: int = 1, rank: int = 0) -> dict:
+    """Kernel plan for a problem shape, without a GPU (used by the CPU tests
+    to put the oracle's MIRROR mode into the device's reduction order)."""
+    pl = A.Plan()
+    rc = A.lib().halp_plan_for(n, d, C_, {"f64": A.F64, "f32": A.F32, "bf16": A.BF16}[dtype], world, rank,
+                               C.byref(pl))
+    if rc:
+        _raise(rc)
+    return {k: getattr(pl, k) for k, _ in A.Plan._fields_}
+
+
+def oracle_plan_for(n: int, d: int, C_: int = 1, dtype: str = "f64") -> dict:
+    p = plan_for(n, d, C_, dtype)
+    return {k: p[k] for k in ("fg_threads", "fg_vec", "fg_splits", "in_ctas", "in_threads", "in_per")}
+
+
+def rng_state_after(seed: int, stream: int, count: int) -> int:
+    return A.lib().halp_rng_state_after(seed, stream, count)

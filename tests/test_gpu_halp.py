@@ -1,0 +1,264 @@
+"""GPU parity: the B200 kernels against the CPU oracle.
+
+MIRROR mode reproduces the kernels' floating-point order, so every number
+must be bit-identical (losses, gradient norms, deltas, iterate hashes, final
+iterates, every z code).  REF mode is the reference's own order (pinned to
+the golden traces); against it the z trajectory must still be identical and
+losses / gradients agree to <= 1e-9 relative (north-star bar: 1e-5 for fp32).
+"""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "regression_floor.json")))
+
+
+@pytest.fixture(scope="module")
+def H():
+    import paper_1803_03383_b200 as H
+    from paper_1803_03383_b200 import build
+
+    build.build()
+    return H
+
+
+def objs(H, oracle, X, y=None, labels=None, C=0, l2=0.0):
+    if labels is None:
+        g = H.Objective(H.Dataset(X, targets=y), H.LossFamily.Squared, l2)
+        o = oracle.OracleObjective(X, y=y, l2=l2)
+    else:
+        g = H.Objective(H.Dataset(X, labels=labels, num_classes=C), H.LossFamily.Softmax, l2)
+        o = oracle.OracleObjective(X, labels=labels, num_classes=C, l2=l2)
+    return g, o
+
+
+def bf16_bits(a):
+    u = np.ascontiguousarray(a, dtype=np.float32).view(np.uint32)
+    # round to nearest even
+    u = (u + 0x7FFF + ((u >> 16) & 1)) >> 16
+    return u.astype(np.uint16)
+
+
+@pytest.mark.parametrize("dtype", ["f64", "f32", "bf16"])
+@pytest.mark.parametrize("shape", [(1000, 100), (777, 37), (5000, 256), (64, 8)])
+def test_fullgrad_squared_bitexact(H, oracle, dtype, shape):
+    n, d = shape
+    X, y = oracle.make_regression(n, d, 0.3, 11)
+    Xd = {"f64": X, "f32": X.astype(np.float32), "bf16": bf16_bits(X)}[dtype]
+    g, o = objs(H, oracle, Xd, y, l2=1e-3)
+    w = np.random.default_rng(1).standard_normal(d)
+    gg, gl = g._fullpass(w)
+    plan = g.oracle_plan()
+    og = o.full_gradient(w, plan=plan)
+    ol = o.loss_value(w, plan=plan)
+    assert np.array_equal(gg, og)
+    assert gl == ol
+    rg = o.full_gradient(w)
+    assert np.max(np.abs(gg - rg)) <= 1e-12 * np.max(np.abs(rg))
+    assert abs(gl - o.loss_value(w)) <= 1e-12 * abs(gl)
+
+
+@pytest.mark.parametrize("C,d,n", [(2, 40, 3000), (3, 17, 500), (10, 784, 2000), (15, 33, 700)])
+def test_fullgrad_softmax_bitexact(H, oracle, C, d, n):
+    rng = np.random.default_rng(C)
+    X = rng.random((n, d)).astype(np.float32) * (rng.random((n, d)) < 0.2)
+    lab = rng.integers(0, C, n).astype(np.int32)
+    g, o = objs(H, oracle, X, labels=lab, C=C, l2=1e-4)
+    w = rng.standard_normal(d * C) * 0.1
+    gg, gl = g._fullpass(w)
+    plan = g.oracle_plan()
+    assert np.array_equal(gg, o.full_gradient(w, plan=plan))
+    assert gl == o.loss_value(w, plan=plan)
+    rg = o.full_gradient(w)
+    assert np.max(np.abs(gg - rg)) <= 1e-12 * max(1e-300, np.max(np.abs(rg)))
+    assert abs(gl - o.loss_value(w)) <= 1e-12 * abs(gl)
+
+
+def rows_equal(grows, orows):
+    assert len(grows) == len(orows)
+    for a, b in zip(grows, orows):
+        assert a.pass_ == b["pass_"]
+        assert a.loss == b["loss"] or (math.isnan(a.loss) and math.isnan(b["loss"])), (a, b)
+        assert a.grad_norm == b["grad_norm"], (a, b)
+        assert a.delta == b["delta"], (a, b)
+        assert a.iterate_hash == b["iterate_hash"], (a, b)
+
+
+@pytest.mark.parametrize("bits,seed", [(8, 1), (16, 4)])
+def test_golden_problem_bitexact_vs_mirror(H, oracle, bits, seed):
+    X, y = oracle.make_regression(1000, 100, 0.0, 42)
+    g, o = objs(H, oracle, X, y)
+    cfg = H.OptimizerConfig(algorithm=H.Algorithm.Halp, alpha=5e-3, epochs=25, inner_steps=2000, bits=bits, mu=3.0,
+                            seed=seed)
+    steps = 2000
+    tr = np.zeros(steps * 100, dtype=np.int64)
+    rec = H.run_halp(g, cfg, trace=tr)
+    orec = oracle.run_halp(o, oracle.OracleConfig(alpha=5e-3, epochs=25, inner_steps=2000, bits=bits, mu=3.0,
+                                                  seed=seed), plan=g.oracle_plan(), trace_steps=steps)
+    rows_equal(rec.rows, orec.rows)
+    assert np.array_equal(rec.final_iterate, orec.final_iterate)
+    assert np.array_equal(tr.reshape(steps, 100), orec.trace)
+    assert rec.steps_taken == 50000 and rec.inner_fp_vector_ops == 400000 and rec.status == "ok"
+
+
+@pytest.mark.parametrize("name,bits", [("halp-8", 8), ("halp-16", 16)])
+def test_golden_traces_gpu(H, oracle, name, bits):
+    """The GPU reproduces the reference's own golden traces."""
+    X, y = oracle.make_regression(1000, 100, 0.0, 42)
+    g = H.Objective(H.Dataset(X, targets=y), H.LossFamily.Squared, 0.0)
+    for seed in (1, 2, 5):
+        cfg = H.OptimizerConfig(algorithm=H.Algorithm.Halp, alpha=5e-3, epochs=25, inner_steps=2000, bits=bits,
+                                mu=3.0, seed=seed)
+        rec = H.run_halp(g, cfg)
+        gold = GOLD["traces"][f"{name}_seed{seed}"]
+        assert len(rec.rows) == len(gold)
+        for a, b in zip(rec.rows, gold):
+            for f, gf in (("loss", "loss"), ("grad_norm", "grad_norm"), ("delta", "delta")):
+                assert abs(getattr(a, f) - float(b[gf])) <= 1e-9 * abs(float(b[gf])), (seed, a, b)
+
+
+def test_codes_match_reference_order(H, oracle):
+    """Against the REF (reference-order) oracle the z trajectory is identical."""
+    X, y = oracle.make_regression(1000, 100, 0.0, 42)
+    g, o = objs(H, oracle, X, y)
+    steps = 2000 * 3
+    tr = np.zeros(steps * 100, dtype=np.int64)
+    H.run_halp(g, H.OptimizerConfig(algorithm=H.Algorithm.Halp, alpha=5e-3, epochs=3, inner_steps=2000, bits=8,
+                                    mu=3.0, seed=3), trace=tr)
+    orec = oracle.run_halp(o, oracle.OracleConfig(alpha=5e-3, epochs=3, inner_steps=2000, bits=8, mu=3.0, seed=3),
+                           trace_steps=steps)
+    assert np.count_nonzero(tr.reshape(steps, 100) != orec.trace) == 0
+
+
+@pytest.mark.parametrize("nc,m", [(1, 1), (2, 2), (4, 1), (3, 4), (16, 1)])
+def test_cluster_plans_bitexact(H, oracle, nc, m, monkeypatch):
+    monkeypatch.setenv("HALP_IN_NC", str(nc))
+    monkeypatch.setenv("HALP_IN_M", str(m))
+    X, y = oracle.make_regression(600, 150, 0.1, 5)
+    Xf = X.astype(np.float32)
+    g, o = objs(H, oracle, Xf, y, l2=1e-3)
+    assert g.plan()["in_ctas"] == nc
+    cfg = H.OptimizerConfig(algorithm=H.Algorithm.Halp, alpha=3e-3, epochs=3, inner_steps=700, bits=8, mu=2.0, seed=9)
+    rec = H.run_halp(g, cfg)
+    orec = oracle.run_halp(o, oracle.OracleConfig(alpha=3e-3, epochs=3, inner_steps=700, bits=8, mu=2.0, seed=9),
+                           plan=g.oracle_plan())
+    rows_equal(rec.rows, orec.rows)
+    assert np.array_equal(rec.final_iterate, orec.final_iterate)
+
+
+@pytest.mark.parametrize("C,nc", [(2, 1), (10, 0), (3, 2)])
+def test_softmax_run_bitexact(H, oracle, C, nc, monkeypatch):
+    if nc:
+        monkeypatch.setenv("HALP_IN_NC", str(nc))
+    rng = np.random.default_rng(7 + C)
+    n, d = 1500, 64
+    X = (rng.random((n, d)) * (rng.random((n, d)) < 0.3)).astype(np.float32)
+    W = rng.standard_normal((d, C))
+    lab = np.argmax(X @ W + rng.gumbel(size=(n, C)), axis=1).astype(np.int32)
+    g, o = objs(H, oracle, X, labels=lab, C=C, l2=1e-4)
+    cfg = H.OptimizerConfig(algorithm=H.Algorithm.Halp, alpha=0.05, epochs=3, inner_steps=n, bits=8, mu=2.5, seed=2)
+    steps = 200
+    tr = np.zeros(steps * d * C, dtype=np.int64)
+    rec = H.run_halp(g, cfg, trace=tr)
+    orec = oracle.run_halp(o, oracle.OracleConfig(alpha=0.05, epochs=3, inner_steps=n, bits=8, mu=2.5, seed=2),
+                           plan=g.oracle_plan(), trace_steps=steps)
+    rows_equal(rec.rows, orec.rows)
+    assert np.array_equal(rec.final_iterate, orec.final_iterate)
+    assert np.array_equal(tr.reshape(steps, -1), orec.trace)
+    assert rec.rows[-1].loss < rec.rows[0].loss
+
+
+def test_option_ii_and_wide_bits(H, oracle):
+    X, y = oracle.make_regression(300, 20, 0.2, 5)
+    g, o = objs(H, oracle, X, y)
+    for bits, opt in ((8, 1), (40, 0), (64, 1)):
+        cfg = H.OptimizerConfig(algorithm=H.Algorithm.Halp, alpha=0.02, epochs=4, bits=bits, mu=3.0, seed=11,
+                                option=H.EpochOption(opt))
+        rec = H.run_halp(g, cfg)
+        orec = oracle.run_halp(o, oracle.OracleConfig(alpha=0.02, epochs=4, bits=bits, mu=3.0, seed=11, option=opt),
+                               plan=g.oracle_plan())
+        rows_equal(rec.rows, orec.rows)
+        assert np.array_equal(rec.final_iterate, orec.final_iterate)
+
+
+def test_converged_at_optimum(H, oracle):
+    # test_optimizers.cpp:303-329
+    X, _ = oracle.make_regression(30, 4, 0.0, 8)
+    g = H.Objective(H.Dataset(X, targets=np.zeros(30)), H.LossFamily.Squared, 0.0)
+    rec = H.run_halp(g, H.OptimizerConfig(algorithm=H.Algorithm.Halp, alpha=0.02, epochs=3, mu=3.0, seed=11))
+    assert rec.status == "converged" and rec.steps_taken == 0
+    assert len(rec.rows) == 1 and rec.rows[0].grad_norm == 0.0 and rec.rows[0].delta == 0.0
+
+
+def test_delta_tracks_gradient(H):
+    # test_optimizers.cpp:331-350
+    g = H.Objective(H.Dataset(np.ones((1, 1)), targets=np.array([2.0])), H.LossFamily.Squared, 0.0)
+    cfg = H.OptimizerConfig(algorithm=H.Algorithm.Halp, alpha=0.5, epochs=1, inner_steps=4, bits=8, mu=3.0, seed=11)
+    rec = H.run_halp(g, cfg)
+    assert rec.rows[0].grad_norm == 2.0 and rec.rows[0].delta == H.halp_scale(2.0, 3.0, 8)
+    cfg.delta_min = 1.0
+    assert H.run_halp(g, cfg).rows[0].delta == 1.0
+
+
+def test_blowup_and_divergence(H, oracle):
+    g = H.Objective(H.Dataset(np.array([[2.0]]), targets=np.array([3.0])), H.LossFamily.Squared, 0.0)
+    cfg = H.OptimizerConfig(algorithm=H.Algorithm.Halp, alpha=1e308, epochs=2, inner_steps=3, mu=3.0, seed=11)
+    with pytest.raises(H.DivergenceError) as ei:
+        H.run_halp(g, cfg)
+    part = ei.value.partial
+    assert part.status == "diverged" and math.isinf(part.rows[-1].loss) and part.rows[-1].pass_ == 1.0
+    o = oracle.OracleObjective(np.array([[2.0]]), y=np.array([3.0]))
+    orec = oracle.run_halp(o, oracle.OracleConfig(alpha=1e308, epochs=2, inner_steps=3, mu=3.0, seed=11),
+                           plan=g.oracle_plan())
+    rows_equal(part.rows, orec.rows)
+    assert np.array_equal(part.final_iterate, orec.final_iterate)
+    assert H.run_prepared(g, H.OptimizerConfig(algorithm=H.Algorithm.Halp, alpha=1e308, epochs=2, inner_steps=3,
+                                               mu=3.0, seed=11)).status == "diverged"
+    # boundary divergence guard
+    X, y = oracle.make_regression(80, 6, 0.2, 5)
+    g2 = H.Objective(H.Dataset(X, targets=y), H.LossFamily.Squared, 0.0)
+    with pytest.raises(H.DivergenceError):
+        H.run_halp(g2, H.OptimizerConfig(algorithm=H.Algorithm.Halp, alpha=0.02, epochs=2, mu=3.0,
+                                         divergence_limit=1e-3))
+
+
+def test_validation_errors(H, oracle):
+    X, y = oracle.make_regression(80, 6, 0.2, 5)
+    g = H.Objective(H.Dataset(X, targets=y), H.LossFamily.Squared, 0.0)
+    for bad in (dict(alpha=-1.0), dict(epochs=-1), dict(mu=0.0), dict(bits=1), dict(delta_min=0.0)):
+        cfg = H.OptimizerConfig(algorithm=H.Algorithm.Halp, mu=3.0)
+        for k, v in bad.items():
+            setattr(cfg, k, v)
+        with pytest.raises(H.InvalidInputError):
+            H.run_halp(g, cfg)
+    with pytest.raises(H.InvalidInputError):
+        H.Objective(H.Dataset(X, labels=np.full(80, 7), num_classes=3), H.LossFamily.Softmax, 0.0)
+    with pytest.raises(H.InvalidInputError):
+        H.Objective(H.Dataset(X, targets=y), H.LossFamily.Squared, -1.0)
+    rec = H.run_halp(g, H.OptimizerConfig(algorithm=H.Algorithm.Halp, epochs=0, mu=3.0))
+    assert len(rec.rows) == 1 and rec.steps_taken == 0 and np.all(rec.final_iterate == 0)
+
+
+def test_device_resident_inputs_and_datagen(H, oracle):
+    import torch
+
+    X, y = H.generate("regression", 4096, 128, dtype="f32", noise_sd=0.1, seed=3)
+    assert X.is_cuda and torch.isfinite(X).all()
+    g = H.Objective(H.Dataset(X, targets=y), H.LossFamily.Squared, 0.0)
+    Xh, yh = X.cpu().numpy(), y.cpu().numpy()
+    o = oracle.OracleObjective(Xh, y=yh)
+    w = np.random.default_rng(0).standard_normal(128)
+    gg, gl = g._fullpass(w)
+    assert np.array_equal(gg, o.full_gradient(w, plan=g.oracle_plan()))
+    # labels for the softmax / logistic generators
+    Xs, lab = H.generate("softmax", 2000, 784, num_classes=10, dtype="f32", density=0.2, seed=1)
+    labh = lab.cpu().numpy()
+    assert labh.min() >= 0 and labh.max() <= 9 and len(np.unique(labh)) == 10
+    assert 0.15 < float((Xs != 0).float().mean()) < 0.25
+    Xb, lb = H.generate("logistic", 4096, 1024, dtype="bf16", x_scale=1 / 32, seed=2)
+    assert Xb.dtype == torch.bfloat16 and set(np.unique(lb.cpu().numpy())) <= {0, 1}
