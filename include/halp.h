@@ -123,6 +123,8 @@ typedef struct {
   int64_t inner_launches;
   int64_t kernel_launches; /* every kernel this library launched */
   int64_t inner_steps;     /* inner steps executed */
+  int64_t h2d_bytes;       /* host->device bytes moved by the call (inputs, iterate upload) */
+  int64_t d2h_bytes;       /* device->host bytes (stats, iterates for the row hashes, result) */
 } halp_timing;
 
 /* Reduction plan of the problem's kernels (consumed by the oracle's MIRROR

@@ -589,40 +589,90 @@ static double mirror_norm(const double* g, int D) {
 /* K3 dot order for one class c of the flat D = d*C coordinate vector:
  * global thread tau = cta*T + tid owns flat coords [tau*m, (tau+1)*m);
  * its partial for class c is a sequential fma over its coords of that
- * class; lanes are combined by the warp butterfly, warps of a CTA summed in
- * order, CTAs summed in order. */
+ * class; lanes are combined by the warp butterfly; the warp sums are then
+ * added sequentially in global warp order (cta-major), which is the same as
+ * skipping the warps that hold no coordinate of class c (their sum is +0). */
 static void mirror_inner_dots(const double* x, const double* wa, const double* wb, int d, int C,
                               const oq_plan* pl, double* la, double* lb) {
   const int D = d * C, T = pl->in_threads, m = pl->in_per, NC = pl->in_ctas;
-  const int nw = T / 32;
+  const int ngw = NC * (T / 32);
+  double wsa[512], wsb[512];
   for (int c = 0; c < C; ++c) {
     double ca = 0.0, cb = 0.0;
-    for (int cta = 0; cta < NC; ++cta) {
-      double wa_s = 0.0, wb_s = 0.0;
-      for (int wi = 0; wi < nw; ++wi) {
-        double va[32], vb[32];
-        for (int l = 0; l < 32; ++l) {
-          const int64_t tau = (int64_t)cta * T + wi * 32 + l;
-          double aa = 0.0, ab = 0.0;
-          for (int64_t k = tau * m; k < (tau + 1) * m && k < D; ++k) {
-            if (k / d != c) continue;
-            const int j = (int)(k % d);
-            aa = fma(x[j], wa[k], aa);
-            ab = fma(x[j], wb[k], ab);
-          }
-          va[l] = aa;
-          vb[l] = ab;
+    int first = 1;
+    for (int gw = 0; gw < ngw; ++gw) {
+      double va[32], vb[32];
+      int any = 0;
+      for (int l = 0; l < 32; ++l) {
+        const int64_t tau = (int64_t)gw * 32 + l;
+        double aa = 0.0, ab = 0.0;
+        for (int64_t k = tau * m; k < (tau + 1) * m && k < D; ++k) {
+          if (k / d != c) continue;
+          const int j = (int)(k % d);
+          aa = fma(x[j], wa[k], aa);
+          ab = fma(x[j], wb[k], ab);
+          any = 1;
         }
-        const double sa = warp_butterfly(va), sb = warp_butterfly(vb);
-        wa_s = wi == 0 ? sa : wa_s + sa;
-        wb_s = wi == 0 ? sb : wb_s + sb;
+        va[l] = aa;
+        vb[l] = ab;
       }
-      ca = cta == 0 ? wa_s : ca + wa_s;
-      cb = cta == 0 ? wb_s : cb + wb_s;
+      if (C == 1) {
+        /* squared loss: every warp's sum is kept, combined below */
+        wsa[gw] = warp_butterfly(va);
+        wsb[gw] = warp_butterfly(vb);
+        continue;
+      }
+      if (!any) continue;
+      const double sa = warp_butterfly(va), sb = warp_butterfly(vb);
+      if (first) { ca = sa; cb = sb; first = 0; }
+      else { ca = ca + sa; cb = cb + sb; }
+    }
+    if (C == 1) {
+      /* lane l sums warps l, l+32, ... sequentially from 0.0; lane butterfly */
+      double va[32], vb[32];
+      for (int l = 0; l < 32; ++l) {
+        double aa = 0.0, ab = 0.0;
+        for (int q = l; q < ngw; q += 32) { aa = aa + wsa[q]; ab = ab + wsb[q]; }
+        va[l] = aa;
+        vb[l] = ab;
+      }
+      ca = warp_butterfly(va);
+      cb = warp_butterfly(vb);
     }
     la[c] = ca;
     lb[c] = cb;
   }
+}
+
+/* Markstein division check used by tests/test_division.py: the device
+ * quantizer computes u/delta as fma(x - q0*delta, rcp, q0) with
+ * q0 = x*rcp, rcp = 1/delta; count mismatches against IEEE division. */
+int64_t oq_div_check(int64_t n, uint64_t seed) {
+  oq_rng r;
+  oq_rng_init(&r, seed, 7);
+  int64_t bad = 0;
+  for (int64_t it = 0; it < n; ++it) {
+    uint64_t mb = oq_next_u64(&r) & 0x000FFFFFFFFFFFFFULL;
+    const int mode = (int)(it % 4);
+    if (mode == 1) mb = 0x000FFFFFFFFFFFFFULL;
+    if (mode == 2) mb &= 0x000FF00000000000ULL;
+    const int e = 1023 + (int)(oq_next_u64(&r) % 120) - 60;
+    const uint64_t db = mb | ((uint64_t)e << 52);
+    double delta;
+    memcpy(&delta, &db, 8);
+    const double t = ldexp((double)(int64_t)(oq_next_u64(&r) >> 11) * 0x1.0p-53 * 2.0 - 1.0,
+                           (int)(oq_next_u64(&r) % 24));
+    double x = t * delta;
+    if (it % 7 == 0) x = nextafter(x, (oq_next_u64(&r) & 1) ? INFINITY : -INFINITY);
+    if (it % 11 == 0) x = (double)((int64_t)(oq_next_u64(&r) % 65536) - 32768) * delta;
+    const double rc = 1.0 / delta;
+    const double q0 = x * rc;
+    const double rem = fma(-q0, delta, x);
+    const double q1 = fma(rem, rc, q0);
+    const double qt = x / delta;
+    if (q1 != qt && !(q1 == 0.0 && qt == 0.0)) ++bad;
+  }
+  return bad;
 }
 
 /* ------------------------------------------------------------ public API */

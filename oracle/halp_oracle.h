@@ -152,6 +152,8 @@ double oq_mexp(double x);
 /* REF-mode Eigen packet width (1, 2 or 4); default pinned by golden traces */
 void oq_set_ref_lanes(int lanes);
 double oq_mlog(double x);
+/* Markstein reciprocal-division check (mismatches vs IEEE x/delta in n cases) */
+int64_t oq_div_check(int64_t n, uint64_t seed);
 
 #ifdef __cplusplus
 }

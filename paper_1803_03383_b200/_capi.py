@@ -52,7 +52,8 @@ class Record(C.Structure):
 
 class Timing(C.Structure):
     _fields_ = [(k, C.c_double) for k in ("fullgrad_ms", "finalize_ms", "inner_ms", "sample_ms")] + [
-        (k, C.c_int64) for k in ("fullgrad_launches", "inner_launches", "kernel_launches", "inner_steps")
+        (k, C.c_int64) for k in ("fullgrad_launches", "inner_launches", "kernel_launches", "inner_steps",
+                                "h2d_bytes", "d2h_bytes")
     ]
 
 

@@ -156,6 +156,7 @@ struct halp_problem {
   int64_t* trace_host = nullptr;
   int64_t trace_cap = 0;
   halp_timing timing{};
+  int64_t create_h2d = 0;  // bytes uploaded by halp_problem_create
   Events ev_fg, ev_fin, ev_in, ev_smp;
 
   ~halp_problem() {
@@ -285,6 +286,7 @@ int full_pass(halp_problem* p, double* gn, double* delta, double* loss, double m
   CU(cudaEventRecord(p->ev_fin.b, p->stream));
   double st[4];
   CU(cudaMemcpyAsync(st, p->stats, sizeof(double) * 3, cudaMemcpyDeviceToHost, p->stream));
+  p->timing.d2h_bytes += sizeof(double) * 3;
   CU(cudaStreamSynchronize(p->stream));
   float ms = 0;
   CU(cudaEventElapsedTime(&ms, p->ev_fg.a, p->ev_fg.b));
@@ -454,12 +456,14 @@ int halp_problem_create(const halp_problem_desc* desc, halp_problem** out) {
     if (cudaMemcpy2D(p->X, (size_t)p->ld * es, desc->X, (size_t)p->d * es, (size_t)p->d * es, (size_t)p->n,
                      dev_in ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice) != cudaSuccess)
       return bail(fail(HALP_CUDA_ERROR, "copy of X to the device failed"));
+    if (!dev_in) p->create_h2d += (int64_t)p->n * p->d * es;
   }
   if (p->loss == HALP_SQUARED) {
     if (cudaMalloc(&p->y, sizeof(double) * p->n) != cudaSuccess) return bail(fail(HALP_CUDA_ERROR, "cudaMalloc(y)"));
     if (cudaMemcpy(p->y, desc->y, sizeof(double) * p->n, dev_in ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice) !=
         cudaSuccess)
       return bail(fail(HALP_CUDA_ERROR, "copy of y failed"));
+    if (!dev_in) p->create_h2d += (int64_t)p->n * 8;
   } else {
     std::vector<int32_t> lab(p->n);
     if (cudaMemcpy(lab.data(), desc->labels, sizeof(int32_t) * p->n,
@@ -470,6 +474,7 @@ int halp_problem_create(const halp_problem_desc* desc, halp_problem** out) {
     if (cudaMalloc(&p->labels, sizeof(int32_t) * p->n) != cudaSuccess) return bail(fail(HALP_CUDA_ERROR, "cudaMalloc(labels)"));
     if (cudaMemcpy(p->labels, lab.data(), sizeof(int32_t) * p->n, cudaMemcpyHostToDevice) != cudaSuccess)
       return bail(fail(HALP_CUDA_ERROR, "copy of labels failed"));
+    p->create_h2d += (int64_t)p->n * 4;
   }
   p->sp = make_shard_plan(p->n, p->d, C, p->dtype, world, p->rank);
   int rc = choose_plans(p);
@@ -484,6 +489,7 @@ int halp_problem_create(const halp_problem_desc* desc, halp_problem** out) {
   }
   rc = ensure_workspace(p);
   if (rc) return bail(rc);
+  p->timing.h2d_bytes = p->create_h2d;
   *out = p;
   return HALP_OK;
 }
@@ -578,6 +584,7 @@ int halp_run(halp_problem* p, const halp_config* cfg, halp_record* rec) {
   std::vector<double> wh(D, 0.0);
   if (cfg->init) std::memcpy(wh.data(), cfg->init, sizeof(double) * D);
   CU(cudaMemcpyAsync(p->w, wh.data(), sizeof(double) * D, cudaMemcpyHostToDevice, p->stream));
+  p->timing.h2d_bytes += sizeof(double) * D;
 
   // trace buffer (test hook)
   int64_t traced = 0;
@@ -608,6 +615,7 @@ int halp_run(halp_problem* p, const halp_config* cfg, halp_record* rec) {
     rc = full_pass(p, &gn, &delta, &loss, cfg->mu, cfg->bits, cfg->delta_min);
     if (rc) return rc;
     CU(cudaMemcpy(wh.data(), p->w, sizeof(double) * D, cudaMemcpyDeviceToHost));
+    p->timing.d2h_bytes += sizeof(double) * D;
     rc = r.boundary((double)steps / (double)n, wh.data(), loss, gn, delta, k == 0 || gn == 0.0);
     if (rc) return rc;
     if (gn == 0.0) {
@@ -631,9 +639,11 @@ int halp_run(halp_problem* p, const halp_config* cfg, halp_record* rec) {
     // rounding stream: epoch k starts after k*D*(T+1) draws; Q(0) takes D of them
     const uint64_t r0 = jt.jump(s_round, (uint64_t)k * (uint64_t)D * (uint64_t)(T + 1) + (uint64_t)D);
     CU(cudaMemsetAsync(p->blow, 0xFF, sizeof(int), p->stream));
+    const double rcp = 1.0 / delta;
     InParams ip{p->X, p->ld, p->d, p->C, (int)D, p->loss, n, p->y, p->labels, p->l2, cfg->alpha, delta, hi, lo, maxc,
-                minc, p->w, p->w2, p->g, p->idx, T, t_pick, r0, p->pow_tab, p->jump_tab, p->codes,
-                tr_steps > 0 ? p->trace_dev : nullptr, tr_steps, p->blow, p->u_out};
+                minc, std::isfinite(rcp) && rcp != 0.0 && env_int("HALP_IEEE_DIV", 0) == 0 ? rcp : 0.0, p->w, p->w2,
+                p->g, p->idx, T, t_pick, r0, p->pow_tab, p->jump_tab, p->codes, tr_steps > 0 ? p->trace_dev : nullptr,
+                tr_steps, p->blow, p->u_out};
     CU(cudaEventRecord(p->ev_in.a, p->stream));
     CU(launch_inner(p->in, ip, p->stream));
     ++p->timing.kernel_launches;
@@ -641,6 +651,7 @@ int halp_run(halp_problem* p, const halp_config* cfg, halp_record* rec) {
     CU(cudaEventRecord(p->ev_in.b, p->stream));
     int blow = -1;
     CU(cudaMemcpyAsync(&blow, p->blow, sizeof(int), cudaMemcpyDeviceToHost, p->stream));
+    p->timing.d2h_bytes += sizeof(int);
     CU(cudaStreamSynchronize(p->stream));
     float ms = 0;
     CU(cudaEventElapsedTime(&ms, p->ev_in.a, p->ev_in.b));
@@ -672,6 +683,7 @@ int halp_run(halp_problem* p, const halp_config* cfg, halp_record* rec) {
     rc = full_pass(p, &gn, &delta, &loss, cfg->mu, cfg->bits, cfg->delta_min);
     if (rc) return rc;
     CU(cudaMemcpy(wh.data(), p->w, sizeof(double) * D, cudaMemcpyDeviceToHost));
+    p->timing.d2h_bytes += sizeof(double) * D;
     rc = r.boundary((double)steps / (double)n, wh.data(), loss, gn, delta, true);
     if (rc) return rc;
     if (gn == 0.0) rec->status = HALP_STATUS_CONVERGED;

@@ -64,6 +64,59 @@ __device__ __forceinline__ long long quantize_code(double x, double delta, doubl
   return code;
 }
 
+// t = x / delta, correctly rounded, from the host's rcp = RN(1/delta):
+// q0 = RN(x*rcp), r = x - q0*delta (exact with fma), q1 = RN(q0 + r*rcp)
+// is the IEEE quotient (Markstein's theorem; tests/test_division.py checks
+// 2e8 cases against x/delta).  Outside the safe range (huge quotient, tiny
+// x, non-finite) the IEEE division is used.
+__device__ __forceinline__ double div_rcp(double x, double delta, double rcp) {
+  const double q0 = __dmul_rn(x, rcp);
+  const double r = fma(-q0, delta, x);
+  const double q1 = fma(r, rcp, q0);
+  const double ax = fabs(x);
+  if (fabs(q0) <= 0x1.0p60 && (ax >= 0x1.0p-960 || ax == 0.0)) return q1;
+  return x / delta;
+}
+
+// quantize_code with the reciprocal division
+__device__ __forceinline__ long long quantize_code_rcp(double x, double delta, double rcp, double hi, double lo,
+                                                       long long maxc, long long minc, double u) {
+  const double t = rcp != 0.0 ? div_rcp(x, delta, rcp) : x / delta;
+  if (t >= hi) return maxc;
+  if (t <= lo) return minc;
+  const double snapped = rint(t);
+  if (__dmul_rn(snapped, delta) == x) return __double2ll_rn(snapped);
+  const double fl = floor(t);
+  const double frac = t - fl;
+  long long code = __double2ll_rn(fl);
+  if (frac > 0.0 && u < frac) ++code;
+  return code;
+}
+
+// Branch-free quantize_code returning the code as an exact double
+// (|code| < 2^53; callers with bits > 53 use quantize_code).  The
+// reference's branches (fixed_point.cpp:37-49) are mutually exclusive, so
+// evaluating every candidate and selecting gives the same code; t comes
+// from div_rcp's fast path and `slow` reports operands that need the IEEE
+// fallback (the caller recomputes those coordinates).
+__device__ __forceinline__ double quantize_fast(double x, double delta, double rcp, double hi, double lo, double u,
+                                                bool& slow) {
+  const double q0 = __dmul_rn(x, rcp);
+  const double r = fma(-q0, delta, x);
+  const double t = fma(r, rcp, q0);
+  const double ax = fabs(x);
+  slow = !(fabs(q0) <= 0x1.0p60 && (ax >= 0x1.0p-960 || ax == 0.0));
+  const double sn = rint(t);
+  const double fl = floor(t);
+  const double frac = t - fl;
+  const bool onlat = __dmul_rn(sn, delta) == x;
+  const bool up = frac > 0.0 && u < frac;
+  double c = onlat ? sn : (up ? fl + 1.0 : fl);
+  c = (t <= lo) ? lo : c;
+  c = (t >= hi) ? hi : c;
+  return c;
+}
+
 template <class T> __device__ __forceinline__ double to_d(T v);
 template <> __device__ __forceinline__ double to_d<double>(double v) { return v; }
 template <> __device__ __forceinline__ double to_d<float>(float v) { return (double)v; }
@@ -214,6 +267,12 @@ __device__ __forceinline__ void st_cluster_f64(const double* local, uint32_t ran
   uint32_t a = smem_u32(local), ra;
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(a), "r"(rank));
   asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(ra), "d"(v) : "memory");
+}
+
+__device__ __forceinline__ void st_cluster_s32(const int* local, uint32_t rank, int v) {
+  uint32_t a = smem_u32(local), ra;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(a), "r"(rank));
+  asm volatile("st.shared::cluster.s32 [%0], %1;" ::"r"(ra), "r"(v) : "memory");
 }
 
 }  // namespace halp

@@ -50,6 +50,7 @@ struct InParams {
   const int32_t* labels;
   double l2, alpha, delta, hi, lo;
   long long maxc, minc;
+  double rcp;          // RN(1/delta), 0 => use IEEE division
   const double* w;     // w~ [D]
   double* w_out;       // w~ after the epoch [D]
   const double* g;     // g~ [D]

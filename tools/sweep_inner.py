@@ -1,0 +1,51 @@
+"""Inner-loop (K3) plan sweep: us/step for cluster size NC and coords/thread M.
+
+    python tools/sweep_inner.py c2|c3|c1 [T]
+"""
+import itertools
+import os
+import subprocess
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+CHILD = r'''
+import os, sys
+sys.path.insert(0, os.environ["ROOT"])
+import paper_1803_03383_b200 as H
+which, T = sys.argv[1], int(sys.argv[2])
+if which == "c2":
+    X, lab = H.generate("softmax", 60000, 784, num_classes=10, dtype="f32", density=0.2, seed=0)
+    obj = H.Objective(H.Dataset(X, labels=lab, num_classes=10), H.LossFamily.Softmax, 1e-4)
+    cfg = dict(alpha=0.01, mu=2.5, bits=8)
+elif which == "c3":
+    X, y = H.generate("regression", 65536, 4096, dtype="f32", noise_sd=0.1, seed=3)
+    obj = H.Objective(H.Dataset(X, targets=y), H.LossFamily.Squared, 0.0)
+    cfg = dict(alpha=5e-5, mu=1.0, bits=16)
+else:
+    X, y = H.generate("regression", 8192, 256, dtype="f32", noise_sd=0.01, seed=0)
+    obj = H.Objective(H.Dataset(X, targets=y), H.LossFamily.Squared, 0.0)
+    cfg = dict(alpha=1e-3, mu=1e3, bits=8)
+H.run_halp(obj, H.OptimizerConfig(algorithm=H.Algorithm.Halp, epochs=1, inner_steps=min(T, 1000), seed=0, **cfg))
+H.run_halp(obj, H.OptimizerConfig(algorithm=H.Algorithm.Halp, epochs=1, inner_steps=T, seed=0, **cfg))
+t = obj.timing(); p = obj.plan()
+print("RESULT", p["in_ctas"], p["in_threads"], p["in_per"], "%.3f" % (1000 * t["inner_ms"] / T))
+'''
+
+
+def main():
+    which = sys.argv[1]
+    T = int(sys.argv[2]) if len(sys.argv) > 2 else 5000
+    grids = {"c2": [(nc, m) for nc in (4, 8, 16) for m in (1, 2, 4, 8)],
+             "c3": [(nc, m) for nc in (1, 2, 4, 8, 16) for m in (1, 2, 4, 8)],
+             "c1": [(nc, m) for nc in (1, 2, 4) for m in (1, 2, 4, 8)]}[which]
+    env = dict(os.environ, ROOT=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    for nc, m in grids:
+        env["HALP_IN_NC"], env["HALP_IN_M"] = str(nc), str(m)
+        r = subprocess.run([sys.executable, "-c", CHILD, which, str(T)], env=env, capture_output=True, text=True)
+        line = [l for l in r.stdout.splitlines() if l.startswith("RESULT")]
+        print(which, "NC", nc, "M", m, line[0] if line else ("ERR " + r.stderr.strip().splitlines()[-1][:150] if r.stderr.strip() else "ERR"), flush=True)
+
+
+if __name__ == "__main__":
+    main()
