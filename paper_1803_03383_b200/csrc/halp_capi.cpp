@@ -145,7 +145,7 @@ struct halp_problem {
   int fg_passes = 1;
   // workspace
   double *w = nullptr, *w2 = nullptr, *g = nullptr, *partials = nullptr, *rank_sum = nullptr, *gathered = nullptr,
-         *stats = nullptr, *u_out = nullptr;
+         *stats = nullptr, *u_out = nullptr, *tree_scratch = nullptr;
   int64_t* idx = nullptr;
   int64_t idx_cap = 0;
   long long* codes = nullptr;
@@ -163,7 +163,7 @@ struct halp_problem {
     cudaSetDevice(device);
     for (void* ptr : {(void*)w, (void*)w2, (void*)g, (void*)partials, (void*)rank_sum, (void*)gathered, (void*)stats,
                       (void*)u_out, (void*)idx, (void*)codes, (void*)blow, (void*)pow_tab, (void*)jump_tab,
-                      (void*)trace_dev, (void*)y, (void*)labels})
+                      (void*)trace_dev, (void*)y, (void*)labels, (void*)tree_scratch})
       if (ptr) cudaFree(ptr);
     if (own_X && X) cudaFree(X);
     if (comm) Nccl::get().commDestroy(comm);
@@ -192,10 +192,41 @@ int plan_for(int64_t n, int d, int C, int dtype, KernelPlan* kp) {
   int CT = 8;
   while (CT > 1 && (NG * V * CT > 64 || CT >= 2 * C)) CT /= 2;
   if (CT > C) CT = (int)next_pow2(C);
-  kp->fg = FgLaunch{dtype, NG, CT, T1, ld, 0};
+  kp->fg = FgLaunch{dtype, NG, CT, T1, ld, 0, 0, 2, 4};
   kp->fg_passes = (C + CT - 1) / CT;
-  const size_t smem = fg_smem_bytes(ld, es, d * C, C, T1, 2, 4);
-  if (smem > 220 * 1024) return fail(HALP_UNSUPPORTED, "full_gradient: row tile + iterate exceed shared memory");
+  // fast register-resident path: C <= 2 and the iterate slice fits in registers
+  if (C <= 2 && NG * V * C <= 32 && env_int("HALP_FG_GENERIC", 0) == 0) {
+    const int row_bytes = ld * es;
+    int R = 1;  // rows per tile: tiles of <= 16 KB, at most 8 rows, <= 32 reduction slots
+    while (R < 8 && R * 2 * row_bytes <= 16 * 1024 && R * 2 * C <= 32 && NG * R * 2 <= 8) R *= 2;
+    if (env_int("HALP_FG_ROWS", 0) > 0) R = (int)env_int("HALP_FG_ROWS", 0);
+    int stages = 6;
+    if (fast_smem_bytes(ld, es, T1, R, C, stages) > 110 * 1024) stages = 3;
+    if (env_int("HALP_FG_STAGES", 0) > 0) stages = (int)env_int("HALP_FG_STAGES", 0);
+    kp->fg.fast = 1;
+    kp->fg.rows = R;
+    kp->fg.stages = stages;
+    kp->fg_passes = 1;
+    // register-tile kernel (512-thread CTAs): plan its own threads / rows
+    if (env_int("HALP_FG_KERNEL", 2) == 2) {
+      const int T2 = (int)std::min<int64_t>(512, (ngroups + 31) / 32 * 32);
+      const int NG2 = (int)next_pow2((ngroups + T2 - 1) / T2);
+      int R2 = (int)env_int("HALP_FG_ROWS", 0);
+      if (R2 <= 0) {
+        R2 = 1;
+        while (R2 < 8 && R2 * 2 * row_bytes <= 32 * 1024 && R2 * 2 * C <= 32 && NG2 * V * R2 * 2 <= 32) R2 *= 2;
+      }
+      if (NG2 * V * C <= 32 && NG2 <= 4) {
+        kp->fg = FgLaunch{dtype, NG2, CT, T2, ld, 0, 2, R2, 4};
+        if (fast_smem_bytes(ld, es, T2, R2, C, 4) > 220 * 1024) kp->fg.stages = 0;
+      }
+    }
+    if (fast_smem_bytes(ld, es, T1, R, C, stages) > 220 * 1024)
+      return fail(HALP_UNSUPPORTED, "full_gradient: row tile exceeds shared memory");
+  } else {
+    const size_t smem = fg_smem_bytes(ld, es, d * C, C, T1, 2, 4);
+    if (smem > 220 * 1024) return fail(HALP_UNSUPPORTED, "full_gradient: row tile + iterate exceed shared memory");
+  }
   // inner loop: M coordinates per thread, up to 16 CTAs per cluster
   const int64_t D = (int64_t)d * C;
   int M = (int)env_int("HALP_IN_M", 4);
@@ -235,6 +266,7 @@ int ensure_workspace(halp_problem* p) {
     CU(cudaMalloc(&p->g, sizeof(double) * p->D));
     CU(cudaMalloc(&p->u_out, sizeof(double) * p->D));
     CU(cudaMalloc(&p->partials, sizeof(double) * D1 * nloc));
+    CU(cudaMalloc(&p->tree_scratch, sizeof(double) * D1 * std::max<int64_t>(1, nloc / 64)));
     CU(cudaMalloc(&p->rank_sum, sizeof(double) * D1));
     CU(cudaMalloc(&p->gathered, sizeof(double) * D1 * p->world));
     CU(cudaMalloc(&p->stats, sizeof(double) * 4));
@@ -272,7 +304,8 @@ int full_pass(halp_problem* p, double* gn, double* delta, double* loss, double m
     CU(launch_fullgrad(L, fp, p->stream));
     ++p->timing.kernel_launches;
   }
-  CU(launch_split_tree(p->partials, nloc, (int)D1, p->world > 1 ? p->rank_sum : p->gathered, p->stream));
+  CU(launch_split_tree(p->partials, nloc, (int)D1, p->world > 1 ? p->rank_sum : p->gathered, p->tree_scratch,
+                        p->stream));
   ++p->timing.kernel_launches;
   CU(cudaEventRecord(p->ev_fg.b, p->stream));
   CU(cudaEventRecord(p->ev_fin.a, p->stream));
@@ -385,8 +418,8 @@ int halp_plan_for(int64_t n, int32_t d, int32_t C, int32_t dtype, int32_t world,
   out->in_ctas = kp.in.ctas;
   out->in_threads = kp.in.threads;
   out->in_per = kp.in.per;
-  out->fg_rows_per_stage = 2;
-  out->fg_stages = 4;
+  out->fg_rows_per_stage = kp.fg.fast ? kp.fg.rows : 2;
+  out->fg_stages = kp.fg.fast ? kp.fg.stages : 4;
   out->fg_split_begin = sp.split_begin;
   out->fg_split_end = sp.split_end;
   return HALP_OK;
@@ -453,6 +486,9 @@ int halp_problem_create(const halp_problem_desc* desc, halp_problem** out) {
     const size_t bytes = (size_t)p->n * p->ld * es;
     if (cudaMalloc(&p->X, bytes) != cudaSuccess) return bail(fail(HALP_CUDA_ERROR, "cudaMalloc(X) failed"));
     p->own_X = true;
+    // padding columns must be zero: kernels process whole 16-byte groups
+    if (p->ld != p->d && cudaMemset(p->X, 0, bytes) != cudaSuccess)
+      return bail(fail(HALP_CUDA_ERROR, "cudaMemset(X) failed"));
     if (cudaMemcpy2D(p->X, (size_t)p->ld * es, desc->X, (size_t)p->d * es, (size_t)p->d * es, (size_t)p->n,
                      dev_in ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice) != cudaSuccess)
       return bail(fail(HALP_CUDA_ERROR, "copy of X to the device failed"));
@@ -504,8 +540,8 @@ int halp_problem_plan(const halp_problem* p, halp_plan* out) {
   out->in_ctas = p->in.ctas;
   out->in_threads = p->in.threads;
   out->in_per = p->in.per;
-  out->fg_rows_per_stage = 2;
-  out->fg_stages = 4;
+  out->fg_rows_per_stage = p->fg.fast ? p->fg.rows : 2;
+  out->fg_stages = p->fg.fast ? p->fg.stages : 4;
   out->fg_split_begin = p->sp.split_begin;
   out->fg_split_end = p->sp.split_end;
   return HALP_OK;
@@ -554,7 +590,7 @@ int halp_bench_full_gradient(halp_problem* p, int reps, double* ms_per_pass) {
       L.nsplit_local = nloc;
       CU(launch_fullgrad(L, fp, p->stream));
     }
-    CU(launch_split_tree(p->partials, nloc, (int)D1, p->rank_sum, p->stream));
+    CU(launch_split_tree(p->partials, nloc, (int)D1, p->rank_sum, p->tree_scratch, p->stream));
   }
   CU(cudaEventRecord(b, p->stream));
   CU(cudaEventSynchronize(b));

@@ -21,10 +21,13 @@ struct FgParams {
 };
 struct FgLaunch {
   int dtype, ng, ct, threads, ld, nsplit_local;
+  int fast, rows, stages;  // fast: register-resident path for C <= 2, `rows` rows per tile, ring depth
 };
 size_t fg_smem_bytes(int ld, int elem, int D, int C, int threads, int R, int stages);
+size_t fast_smem_bytes(int ld, int elem, int threads, int R, int CC, int stages);
 cudaError_t launch_fullgrad(const FgLaunch& L, const FgParams& p, cudaStream_t st);
-cudaError_t launch_split_tree(const double* partials, int nsplit, int D1, double* out, cudaStream_t st);
+cudaError_t launch_split_tree(const double* partials, int nsplit, int D1, double* out, double* scratch,
+                              cudaStream_t st);
 
 struct FinParams {
   const double* rank_sums;  // [G][D+1]
