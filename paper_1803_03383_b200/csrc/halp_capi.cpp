@@ -216,7 +216,9 @@ int plan_for(int64_t n, int d, int C, int dtype, KernelPlan* kp) {
         R2 = 1;
         while (R2 < 8 && R2 * 2 * row_bytes <= 32 * 1024 && R2 * 2 * C <= 32 && NG2 * V * R2 * 2 <= 32) R2 *= 2;
       }
-      if (NG2 * V * C <= 32 && NG2 <= 4) {
+      const int64_t S_ = make_shard_plan(n, d, C, dtype, 1, 0).S;
+      const int64_t split_rows = (n + S_ - 1) / S_ + 1;  // targets staged in shared memory
+      if (NG2 * V * C <= 32 && NG2 <= 4 && split_rows * 8 <= 64 * 1024 && env_int("HALP_FG_KERNEL", 2) == 2) {
         kp->fg = FgLaunch{dtype, NG2, CT, T2, ld, 0, 2, R2, 4};
         if (fast_smem_bytes(ld, es, T2, R2, C, 4) > 220 * 1024) kp->fg.stages = 0;
       }

@@ -419,16 +419,17 @@ __global__ void __launch_bounds__(TB, TB <= 128 ? 3 : 1) k1_reg(FgParams p) {
   const int ngroups = (d + V - 1) / V;
   const size_t stage_elems = (size_t)R * ld;
   Tx* stages = reinterpret_cast<Tx*>(smem);
-  double* red = reinterpret_cast<double*>(smem + STAGES * stage_elems * sizeof(Tx));  // [NW][NV]
-  double* dl_s = red + NW * NV;                                                        // [R][CC]
-  double* lterm = dl_s + NV;                                                           // [R]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(lterm + R);
+  double* red = reinterpret_cast<double*>(smem + STAGES * stage_elems * sizeof(Tx));  // [2][NW][NV]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(red + 2 * NW * NV);
+  double* ysm = reinterpret_cast<double*>(bars + STAGES);  // targets of the split
 
   const int s = p.split0 + blockIdx.x;
   const int64_t r0 = (int64_t)(((unsigned long long)p.n * (unsigned long long)s) / (unsigned long long)p.S);
   const int64_t r1 = (int64_t)(((unsigned long long)p.n * (unsigned long long)(s + 1)) / (unsigned long long)p.S);
   const int64_t ntile = (r1 - r0 + R - 1) / R;
   const Tx* X = reinterpret_cast<const Tx*>(p.X);
+  for (int64_t q = tid; q < r1 - r0; q += T1)
+    ysm[q] = p.loss == 0 ? p.y[r0 + q] : (double)p.labels[r0 + q];
 
   double wr[NG][V][CC];
 #pragma unroll
@@ -464,31 +465,18 @@ __global__ void __launch_bounds__(TB, TB <= 128 ? 3 : 1) k1_reg(FgParams p) {
 #pragma unroll
       for (int c = 0; c < CC; ++c) gacc[k][q][c] = 0.0;
   double la = 0.0;
-  // per-group validity (only the last group of a thread may be beyond d)
   bool gval[NG];
 #pragma unroll
   for (int k = 0; k < NG; ++k) gval[k] = FULLG || (tid + k * T1 < ngroups);
+  // every warp evaluates the loss derivatives itself: lane (fr, fc) = (row, class)
+  const int fr = lane / CC, fc = lane % CC;
 
   for (int64_t i = 0; i < ntile; ++i) {
     const int st = (int)(i % STAGES);
     const int64_t rowb = r0 + i * R;
     const int nr = (int)((r1 - rowb) < R ? (r1 - rowb) : R);
-    // finisher targets (lane 0 of warp r % NW owns row r), loaded before the data wait
-    constexpr int NF = R;  // upper bound of rows per finisher
-    double yreg[NF];
-    int lreg[NF];
-    if (lane == 0) {
-#pragma unroll
-      for (int f = 0; f < NF; ++f) {
-        const int r = wid + f * NW;
-        yreg[f] = 0.0;
-        lreg[f] = 0;
-        if (r < nr) {
-          if (p.loss == 0) yreg[f] = p.y[rowb + r];
-          else lreg[f] = p.labels[rowb + r];
-        }
-      }
-    }
+    const bool act = (lane < NV) && (fr < nr);
+    const double tgt = act ? ysm[rowb - r0 + fr] : 0.0;
     mbar_wait(&bars[st], (uint32_t)((i / STAGES) & 1));
     const Tx* xs = stages + (size_t)st * stage_elems;
     double xr[R][NG][V];
@@ -517,39 +505,51 @@ __global__ void __launch_bounds__(TB, TB <= 128 ? 3 : 1) k1_reg(FgParams p) {
 #pragma unroll
           for (int c = 0; c < CC; ++c) acc[r * CC + c] = fma(xr[r][k][q], wr[k][q][c], acc[r * CC + c]);
     reduce_scatter_n<NV>(acc, lane);
-    if ((lane & ((32 >> LG) - 1)) == 0) red[wid * NV + (lane >> (5 - LG))] = acc[0];
+    double* rb = red + (size_t)(i & 1) * NW * NV;
+    if ((lane & ((32 >> LG) - 1)) == 0) rb[wid * NV + (lane >> (5 - LG))] = acc[0];
     __syncthreads();
     // x of this tile now lives in registers: its stage can be refilled
     if (tid == 0 && i + STAGES < ntile) issue(i + STAGES);
-#pragma unroll
-    for (int f = 0; f < NF; ++f) {
-      const int r = wid + f * NW;
-      if (lane != 0 || r >= nr) continue;
-      double lg[CC];
+
+    // logit of (fr, fc): warps summed in order (same in every warp)
+    double lg = 0.0;
+    if (lane < NV) {
+      lg = rb[lane];
+      for (int w2 = 1; w2 < NW; ++w2) lg = lg + rb[w2 * NV + lane];
+    }
+    double pr, lt = 0.0;
+    if (p.loss == 0) {
+      pr = lg - tgt;
+      lt = __dmul_rn(__dmul_rn(0.5, pr), pr);
+    } else {
+      const int lab = (int)tgt;
+      const int base = (fr * CC) & 31;
+      double mx = 0.0;
 #pragma unroll
       for (int c = 0; c < CC; ++c) {
-        double v = red[r * CC + c];
-        for (int w2 = 1; w2 < NW; ++w2) v = v + red[w2 * NV + r * CC + c];
-        lg[c] = v;
+        const double v = __shfl_sync(0xffffffffu, lg, (base + c) & 31);
+        mx = c == 0 ? v : (v > mx ? v : mx);
       }
-      if (p.loss == 0) {
-        const double e = lg[0] - yreg[f];
-        lterm[r] = __dmul_rn(__dmul_rn(0.5, e), e);
-        dl_s[r * CC] = e;
-      } else {
-        lterm[r] = softmax_loss(lg, CC, lreg[f]);
-        softmax_dl<CC>(lg, CC, lreg[f]);
+      const double e = hexp(lg - mx);
+      double ssum = __shfl_sync(0xffffffffu, e, base);
 #pragma unroll
-        for (int c = 0; c < CC; ++c) dl_s[r * CC + c] = lg[c];
-      }
+      for (int c = 1; c < CC; ++c) ssum = ssum + __shfl_sync(0xffffffffu, e, (base + c) & 31);
+      const double lab_logit = __shfl_sync(0xffffffffu, lg, (base + lab) & 31);
+      pr = e / ssum;
+      if (fc == lab) pr = pr - 1.0;
+      if (wid == 0 && fc == 0) lt = (mx + hlog(ssum)) - lab_logit;
     }
-    __syncthreads();
     double dlr[NV];
 #pragma unroll
-    for (int v = 0; v < NV; ++v) dlr[v] = dl_s[v];
-    if (tid == 0 && p.write_loss)
-      for (int r = 0; r < nr; ++r) la = la + lterm[r];
-    // rows beyond nr hold x = 0 and a stale dl: skip them
+    for (int v = 0; v < NV; ++v) dlr[v] = __shfl_sync(0xffffffffu, pr, v);
+    if (wid == 0 && p.write_loss) {
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const double t = __shfl_sync(0xffffffffu, lt, r * CC);
+        if (r < nr) la = la + t;
+      }
+    }
+    // rows beyond nr: skipped
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       if (r < nr) {
@@ -709,7 +709,8 @@ static cudaError_t launch_fast_cc(const FgLaunch& L, const FgParams& p, cudaStre
 
 template <class Tx, int NG, int CC, int R, int STAGES, int TB>
 static cudaError_t launch_reg_tb(const FgLaunch& L, const FgParams& p, cudaStream_t st) {
-  const size_t smem = fast_smem_bytes(L.ld, (int)sizeof(Tx), L.threads, R, CC, STAGES);
+  const size_t smem = (size_t)STAGES * R * L.ld * sizeof(Tx) + 2 * (size_t)(L.threads / 32) * R * CC * 8 +
+                      STAGES * 8 + 8 * (size_t)((p.n + p.S - 1) / p.S + 1);
   if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
   const bool fullg = ((p.d + VecT<Tx>::V - 1) / VecT<Tx>::V) == NG * L.threads;
   cudaError_t e;
