@@ -207,7 +207,7 @@ int plan_for(int64_t n, int d, int C, int dtype, KernelPlan* kp) {
     kp->fg.rows = R;
     kp->fg.stages = stages;
     kp->fg_passes = 1;
-    // register-tile kernel (512-thread CTAs): plan its own threads / rows
+    // register-tile kernel (default; up to 512-thread CTAs, x converted once per tile)
     if (env_int("HALP_FG_KERNEL", 2) == 2) {
       const int T2 = (int)std::min<int64_t>(512, (ngroups + 31) / 32 * 32);
       const int NG2 = (int)next_pow2((ngroups + T2 - 1) / T2);
@@ -218,13 +218,9 @@ int plan_for(int64_t n, int d, int C, int dtype, KernelPlan* kp) {
       }
       const int64_t S_ = make_shard_plan(n, d, C, dtype, 1, 0).S;
       const int64_t split_rows = (n + S_ - 1) / S_ + 1;  // targets staged in shared memory
-      if (NG2 * V * C <= 32 && NG2 <= 4 && split_rows * 8 <= 64 * 1024 && env_int("HALP_FG_KERNEL", 2) == 2) {
-        kp->fg = FgLaunch{dtype, NG2, CT, T2, ld, 0, 2, R2, 4};
-        if (fast_smem_bytes(ld, es, T2, R2, C, 4) > 220 * 1024) kp->fg.stages = 0;
-      }
+      const size_t smem2 = (size_t)4 * R2 * ld * es + 2 * (size_t)(T2 / 32) * R2 * C * 8 + 32 + 8 * split_rows;
+      if (NG2 * V * C <= 32 && NG2 <= 4 && smem2 <= 200 * 1024) kp->fg = FgLaunch{dtype, NG2, CT, T2, ld, 0, 2, R2, 4};
     }
-    if (fast_smem_bytes(ld, es, T1, R, C, stages) > 220 * 1024)
-      return fail(HALP_UNSUPPORTED, "full_gradient: row tile exceeds shared memory");
   } else {
     const size_t smem = fg_smem_bytes(ld, es, d * C, C, T1, 2, 4);
     if (smem > 220 * 1024) return fail(HALP_UNSUPPORTED, "full_gradient: row tile + iterate exceed shared memory");
@@ -300,7 +296,8 @@ int full_pass(halp_problem* p, double* gn, double* delta, double* loss, double m
   CU(cudaEventRecord(p->ev_fg.a, p->stream));
   for (int pass = 0; pass < p->fg_passes; ++pass) {
     FgParams fp{p->X, p->n, p->d, p->ld, p->C, p->loss, p->y, p->labels, p->w,
-                (int)p->sp.S, (int)p->sp.split_begin, pass * p->fg.ct, pass == 0, p->partials};
+                (int)p->sp.S, (int)p->sp.split_begin, pass * p->fg.ct, pass == 0, p->partials,
+                (int)env_int("HALP_FG_VARIANT", 0)};
     FgLaunch L = p->fg;
     L.nsplit_local = nloc;
     CU(launch_fullgrad(L, fp, p->stream));
@@ -587,7 +584,8 @@ int halp_bench_full_gradient(halp_problem* p, int reps, double* ms_per_pass) {
   for (int r = 0; r < reps; ++r) {
     for (int pass = 0; pass < p->fg_passes; ++pass) {
       FgParams fp{p->X, p->n, p->d, p->ld, p->C, p->loss, p->y, p->labels, p->w,
-                  (int)p->sp.S, (int)p->sp.split_begin, pass * p->fg.ct, pass == 0, p->partials};
+                  (int)p->sp.S, (int)p->sp.split_begin, pass * p->fg.ct, pass == 0, p->partials,
+                (int)env_int("HALP_FG_VARIANT", 0)};
       FgLaunch L = p->fg;
       L.nsplit_local = nloc;
       CU(launch_fullgrad(L, fp, p->stream));

@@ -514,6 +514,7 @@ __global__ void __launch_bounds__(TB, TB <= 128 ? 3 : 1) k1_reg(FgParams p) {
     // logit of (fr, fc): warps summed in order (same in every warp)
     double lg = 0.0;
     if (lane < NV) {
+      // all loads first (independent), then the in-order chain of adds
       lg = rb[lane];
       for (int w2 = 1; w2 < NW; ++w2) lg = lg + rb[w2 * NV + lane];
     }

@@ -18,6 +18,7 @@ struct FgParams {
   const double* w;
   int S, split0, c0, write_loss;
   double* partials;  // [nsplit_local][D+1]
+  int variant;       // experiment switch (HALP_FG_VARIANT), 0 = default
 };
 struct FgLaunch {
   int dtype, ng, ct, threads, ld, nsplit_local;
