@@ -309,9 +309,16 @@ def main():
                               "GB_per_s": gbs, "frac_of_hbm_peak": gbs / world / pk["hbm_gbs"],
                               "algorithmic_bytes_per_gpu": algo, "splits": pl["fg_splits"]}
         c3 = fullgrad["C3"]
-        roofline = {"kernel": "k1_fullgrad (+k1_split_tree), C3 full-gradient pass", "bound": "hbm",
+        traffic = None
+        try:
+            tj = json.load(open(os.path.join(ROOT, "profiles", "k1_traffic.json")))["C3"]
+            traffic = tj["dram_read_bytes_per_launch"] + tj["dram_write_bytes_per_launch"]
+        except Exception:
+            pass
+        roofline = {"kernel": "k1_reg (+k1_tree_pass), C3 full-gradient pass", "bound": "hbm",
                     "achieved": c3["GB_per_s"] / world, "peak": pk["hbm_gbs"], "unit": "GB/s",
-                    "frac": c3["GB_per_s"] / world / pk["hbm_gbs"], "traffic": None,
+                    "frac": c3["GB_per_s"] / world / pk["hbm_gbs"], "traffic": traffic,
+                    "traffic_source": "profiles/k1_traffic.json (ncu dram__bytes_read+write per launch)",
                     "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "_fallback" not in pk else "fallback 6650 GB/s",
                     "algorithmic_bytes_per_launch": c3["algorithmic_bytes_per_gpu"],
                     "bytes_model": "N*d*4 (x, fp32) + N*8 (y, fp64) per pass"}

@@ -1,0 +1,232 @@
+// halp_lpopt.hpp -- header-only C++ mirror of the reference's HALP solver
+// interface over the C ABI (halp.h), for C++ callers of lpopt::run_halp.
+//
+// Same names, fields, defaults and error behaviour as
+//   proj/include/lpopt/objectives.hpp:14,23-33,59-91   (LossFamily, Dataset, Objective)
+//   proj/include/lpopt/optimizers.hpp:13-91            (Algorithm, EpochOption, OptimizerConfig,
+//                                                        MetricRow, RunRecord, DivergenceError,
+//                                                        run_halp, run)
+//   proj/include/lpopt/errors.hpp:8-36                 (Error, InvalidInputError)
+// but Eigen-free: vectors are std::vector<double> (parameter layout d x C
+// column-major, like the reference) and X is row-major n x d.
+#pragma once
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "halp.h"
+
+namespace lpopt_b200 {
+
+struct Error : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct InvalidInputError : Error {
+  using Error::Error;
+};
+struct CudaError : Error {
+  using Error::Error;
+};
+struct UnsupportedError : Error {
+  using Error::Error;
+};
+
+enum class LossFamily { Squared, Softmax };
+enum class Algorithm { Sgd, Svrg, LpSgd, LpSvrg, Halp, LmHalp };
+enum class EpochOption { LastIterate, SampledIterate };
+
+struct Dataset {
+  std::vector<double> X;      // row-major n x d (the reference holds it column-major)
+  long n = 0;
+  int d = 0;
+  std::vector<double> targets;
+  std::vector<int> labels;
+  int num_classes = 0;
+};
+
+struct MetricRow {
+  double pass = 0.0, seconds = 0.0, loss = 0.0, grad_norm = 0.0, delta = 0.0;
+  std::uint64_t iterate_hash = 0;
+  double delta_inner = 0.0, delta_aux = 0.0;
+};
+
+struct RunRecord {
+  std::vector<MetricRow> rows;
+  std::vector<double> final_iterate;
+  std::string status = "ok";
+  std::uint64_t inner_fp_vector_ops = 0;
+  std::uint64_t inner_lp_vector_ops = 0;
+  long steps_taken = 0;
+};
+
+struct DivergenceError : Error {
+  RunRecord partial;
+  DivergenceError(const std::string& msg, RunRecord rec) : Error(msg), partial(std::move(rec)) {}
+};
+
+struct OptimizerConfig {
+  Algorithm algorithm = Algorithm::Svrg;
+  double alpha = 1e-3;
+  int epochs = 1;
+  long inner_steps = 0;
+  int bits = 8;
+  double delta = 0.0;
+  double mu = 0.0;
+  EpochOption option = EpochOption::LastIterate;
+  int full_grad_period = 2;
+  std::uint64_t seed = 0;
+  double metric_every_passes = 0.0;
+  double delta_min = 1e-300;
+  double divergence_limit = 1e12;
+  bool lm_bypass_aux_quant = false;
+  std::vector<double> init;
+};
+
+namespace detail {
+[[noreturn]] inline void raise(int rc) {
+  const std::string m = halp_last_error();
+  if (rc == HALP_INVALID_INPUT) throw InvalidInputError(m);
+  if (rc == HALP_UNSUPPORTED) throw UnsupportedError(m);
+  if (rc == HALP_CUDA_ERROR || rc == HALP_NCCL_ERROR) throw CudaError(m);
+  throw Error(m);
+}
+}  // namespace detail
+
+// lpopt::Objective backed by a device problem (one GPU; see halp.h for NCCL sharding).
+class Objective {
+ public:
+  Objective(Dataset ds, LossFamily loss, double l2, int device = 0) : ds_(std::move(ds)), loss_(loss), l2_(l2) {
+    halp_problem_desc desc{};
+    desc.X = ds_.X.data();
+    desc.dtype = HALP_F64;
+    desc.mem = HALP_MEM_HOST;
+    desc.n = ds_.n;
+    desc.d = ds_.d;
+    desc.loss = loss == LossFamily::Squared ? HALP_SQUARED : HALP_SOFTMAX;
+    desc.num_classes = ds_.num_classes;
+    if (loss == LossFamily::Squared) {
+      if ((long)ds_.targets.size() != ds_.n) throw InvalidInputError("Objective: squared loss needs one target per row");
+      desc.y = ds_.targets.data();
+    } else {
+      if ((long)ds_.labels.size() != ds_.n || ds_.num_classes < 2)
+        throw InvalidInputError("Objective: softmax loss needs labels and classes");
+      labels32_.assign(ds_.labels.begin(), ds_.labels.end());
+      desc.labels = labels32_.data();
+    }
+    desc.l2 = l2;
+    desc.device = device;
+    desc.world_size = 1;
+    const int rc = halp_problem_create(&desc, &h_);
+    if (rc) detail::raise(rc);
+    outputs_ = loss == LossFamily::Squared ? 1 : ds_.num_classes;
+  }
+  Objective(const Objective&) = delete;
+  Objective& operator=(const Objective&) = delete;
+  ~Objective() {
+    if (h_) halp_problem_destroy(h_);
+  }
+
+  long num_components() const { return ds_.n; }
+  int feature_dim() const { return ds_.d; }
+  int num_outputs() const { return outputs_; }
+  int dim() const { return ds_.d * outputs_; }
+  LossFamily loss_family() const { return loss_; }
+  double l2() const { return l2_; }
+  const Dataset& dataset() const { return ds_; }
+  halp_problem* handle() const { return h_; }
+
+  // objectives.cpp:258-311 / :193-223, one fused device pass
+  std::vector<double> full_gradient(const std::vector<double>& w, int num_threads = 1) const {
+    if (num_threads < 1) throw InvalidInputError("full_gradient: num_threads must be >= 1");
+    if ((int)w.size() != dim()) throw InvalidInputError("full_gradient: parameter length mismatch");
+    std::vector<double> g(dim());
+    double l = 0.0;
+    const int rc = halp_full_gradient(h_, w.data(), g.data(), &l);
+    if (rc) detail::raise(rc);
+    return g;
+  }
+  double loss(const std::vector<double>& w) const {
+    if ((int)w.size() != dim()) throw InvalidInputError("loss: parameter length mismatch");
+    std::vector<double> g(dim());
+    double l = 0.0;
+    const int rc = halp_full_gradient(h_, w.data(), g.data(), &l);
+    if (rc) detail::raise(rc);
+    return l;
+  }
+
+ private:
+  Dataset ds_;
+  LossFamily loss_;
+  double l2_;
+  int outputs_ = 1;
+  std::vector<int32_t> labels32_;
+  halp_problem* h_ = nullptr;
+};
+
+// lpopt::run_halp (optimizers.cpp:387-459)
+inline RunRecord run_halp(const Objective& obj, const OptimizerConfig& cfg) {
+  if (!cfg.init.empty() && (int)cfg.init.size() != obj.dim())
+    throw InvalidInputError("optimizer: init length does not match objective");
+  halp_config c{};
+  c.alpha = cfg.alpha;
+  c.epochs = cfg.epochs;
+  c.inner_steps = cfg.inner_steps;
+  c.bits = cfg.bits;
+  c.mu = cfg.mu;
+  c.option = cfg.option == EpochOption::SampledIterate ? 1 : 0;
+  c.full_grad_period = cfg.full_grad_period;
+  c.seed = cfg.seed;
+  c.metric_every_passes = cfg.metric_every_passes;
+  c.delta_min = cfg.delta_min;
+  c.divergence_limit = cfg.divergence_limit;
+  c.init = cfg.init.empty() ? nullptr : cfg.init.data();
+  const int cap = (cfg.epochs > 0 ? cfg.epochs : 0) + 2;
+  std::vector<halp_row> rows(cap);
+  RunRecord out;
+  out.final_iterate.assign(obj.dim(), 0.0);
+  halp_record rec{rows.data(), cap, 0, out.final_iterate.data(), 0, 0, 0, 0};
+  const int rc = halp_run(obj.handle(), &c, &rec);
+  auto fill = [&]() {
+    for (int i = 0; i < rec.rows_n; ++i) {
+      MetricRow r;
+      r.pass = rows[i].pass;
+      r.seconds = rows[i].seconds;
+      r.loss = rows[i].loss;
+      r.grad_norm = rows[i].grad_norm;
+      r.delta = rows[i].delta;
+      r.iterate_hash = rows[i].iterate_hash;
+      out.rows.push_back(r);
+    }
+    out.status = rec.status == HALP_STATUS_CONVERGED ? "converged" : rec.status == HALP_STATUS_DIVERGED ? "diverged" : "ok";
+    out.steps_taken = rec.steps_taken;
+    out.inner_fp_vector_ops = rec.inner_fp_vector_ops;
+    out.inner_lp_vector_ops = rec.inner_lp_vector_ops;
+  };
+  if (rc == HALP_DIVERGED) {
+    fill();
+    throw DivergenceError(halp_last_error(), std::move(out));
+  }
+  if (rc) detail::raise(rc);
+  fill();
+  return out;
+}
+
+// lpopt::run (optimizers.cpp:629-639): the Halp branch
+inline RunRecord run(const Objective& obj, const OptimizerConfig& cfg) {
+  if (cfg.algorithm == Algorithm::Halp) return run_halp(obj, cfg);
+  throw UnsupportedError("only Algorithm::Halp is on the B200 path");
+}
+
+// harness.cpp:296-312
+inline RunRecord run_prepared(const Objective& obj, const OptimizerConfig& cfg) {
+  try {
+    return run(obj, cfg);
+  } catch (const DivergenceError& e) {
+    return e.partial;
+  }
+}
+
+}  // namespace lpopt_b200

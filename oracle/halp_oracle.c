@@ -571,6 +571,63 @@ static void mirror_fullpass(const oq_objective* o, const double* w, const oq_pla
   free(x);
 }
 
+/* Root of the pairwise split tree over splits [s0, s1) in MIRROR order:
+ * out[0..D) gradient column sums, out[D] the loss sum (what one rank's K1 +
+ * k1_tree_pass produce before the NCCL all-gather). */
+int oq_split_subtree(const oq_objective* o, const double* w, const oq_plan* pl, int64_t s0, int64_t s1,
+                     double* out) {
+  const int d = o->d, C = o->C, D = d * C;
+  const int64_t n = o->n;
+  const int S = pl->fg_splits;
+  const int64_t ns = s1 - s0;
+  double* part = (double*)calloc((size_t)ns * (D + 1), sizeof(double));
+  double* x = (double*)malloc(sizeof(double) * (size_t)d);
+  double lg[64];
+  for (int64_t s = s0; s < s1; ++s) {
+    const int64_t r0 = (int64_t)((__int128)n * s / S), r1 = (int64_t)((__int128)n * (s + 1) / S);
+    double* ps = part + (size_t)(s - s0) * (D + 1);
+    double la = 0.0;
+    for (int64_t r = r0; r < r1; ++r) {
+      load_row(o, r, x);
+      for (int c = 0; c < C; ++c) lg[c] = mirror_fg_dot(x, w + (size_t)c * d, d, pl->fg_threads, pl->fg_vec);
+      if (o->loss == OQ_SQUARED) {
+        const double e = lg[0] - o->y[r];
+        la = la + (0.5 * e) * e;
+        for (int j = 0; j < d; ++j) ps[j] = fma(e, x[j], ps[j]);
+      } else {
+        const int y = o->labels[r];
+        la = la + mirror_softmax_loss(lg, C, y);
+        mirror_softmax_dl(lg, C, y);
+        for (int c = 0; c < C; ++c)
+          for (int j = 0; j < d; ++j) ps[(size_t)c * d + j] = fma(lg[c], x[j], ps[(size_t)c * d + j]);
+      }
+    }
+    ps[D] = la;
+  }
+  for (int k = 0; k <= D; ++k) out[k] = tree_sum(part + k, D + 1, ns);
+  free(part);
+  free(x);
+  return OQ_OK;
+}
+
+/* K2 finalize over G gathered rank sums (pairwise tree over ranks) */
+int oq_finalize(const oq_objective* o, const double* w, const double* rank_sums, int G, double* g, double* loss) {
+  const int D = o->d * o->C;
+  for (int k = 0; k < D; ++k) g[k] = tree_sum(rank_sums + k, D + 1, G) / (double)o->n + o->l2 * w[k];
+  double v[256];
+  for (int t = 0; t < 256; ++t) {
+    double a = 0.0;
+    for (int k = t; k < D; k += 256) a = fma(w[k], w[k], a);
+    v[t] = a;
+  }
+  double ws[8];
+  for (int wi = 0; wi < 8; ++wi) ws[wi] = warp_butterfly(v + wi * 32);
+  double sq = ws[0];
+  for (int wi = 1; wi < 8; ++wi) sq = sq + ws[wi];
+  *loss = tree_sum(rank_sums + D, D + 1, G) / (double)o->n + (0.5 * o->l2) * sq;
+  return OQ_OK;
+}
+
 /* finalize kernel order for |g| */
 static double mirror_norm(const double* g, int D) {
   double v[256];

@@ -147,6 +147,12 @@ int64_t  oq_resolve_inner_steps(const oq_config* cfg, int64_t n);
 uint64_t oq_hash_vector(const double* v, int64_t len);
 const char* oq_last_error(void);
 
+/* MIRROR-mode pieces of the multi-GPU full gradient: one rank's split
+ * subtree root [D+1] and the finalize over G gathered rank sums */
+int oq_split_subtree(const oq_objective* o, const double* w, const oq_plan* plan, int64_t s0, int64_t s1,
+                     double* out);
+int oq_finalize(const oq_objective* o, const double* w, const double* rank_sums, int G, double* g, double* loss);
+
 /* mirror-mode exp/log (identical operation sequence to the device code) */
 double oq_mexp(double x);
 /* REF-mode Eigen packet width (1, 2 or 4); default pinned by golden traces */

@@ -104,6 +104,10 @@ def lib():
         L.oq_mexp.argtypes = [C.c_double]
         L.oq_mlog.restype = C.c_double
         L.oq_mlog.argtypes = [C.c_double]
+        L.oq_split_subtree.argtypes = [C.POINTER(_Objective), C.c_void_p, C.POINTER(_Plan), C.c_int64, C.c_int64,
+                                       C.c_void_p]
+        L.oq_finalize.argtypes = [C.POINTER(_Objective), C.c_void_p, C.c_void_p, C.c_int, C.c_void_p,
+                                  C.POINTER(C.c_double)]
         L.oq_resolve_inner_steps.restype = C.c_int64
         L.oq_resolve_inner_steps.argtypes = [C.POINTER(_Config), C.c_int64]
         _lib = L
@@ -227,6 +231,21 @@ class OracleObjective:
         g = np.empty(self.dim, dtype=np.float64)
         _check(lib().oq_full_gradient(C.byref(self._s), w.ctypes.data, num_threads, _plan(plan), g.ctypes.data))
         return g
+
+    def split_subtree(self, w, plan, s0: int, s1: int) -> np.ndarray:
+        w = np.ascontiguousarray(w, dtype=np.float64)
+        out = np.empty(self.dim + 1, dtype=np.float64)
+        _check(lib().oq_split_subtree(C.byref(self._s), w.ctypes.data, _plan(plan), s0, s1, out.ctypes.data))
+        return out
+
+    def finalize(self, w, rank_sums: np.ndarray):
+        w = np.ascontiguousarray(w, dtype=np.float64)
+        rs = np.ascontiguousarray(rank_sums, dtype=np.float64)
+        g = np.empty(self.dim, dtype=np.float64)
+        loss = C.c_double()
+        _check(lib().oq_finalize(C.byref(self._s), w.ctypes.data, rs.ctypes.data, rs.shape[0], g.ctypes.data,
+                                 C.byref(loss)))
+        return g, loss.value
 
     def component_gradient(self, i: int, w) -> np.ndarray:
         w = np.ascontiguousarray(w, dtype=np.float64)
