@@ -43,6 +43,7 @@ sys.path.insert(0, ROOT)
 
 C2 = dict(n=60000, d=784, C=10, density=0.2, l2=1e-4, bits=8, alpha=0.01, mu=2.5)
 C3 = dict(n=4194304, d=4096, dtype="f32")
+C5 = dict(nprob=512, n=4096, d=128, epochs=10, mu=3.0)  # per GPU; T = 2N (reference default)
 C4 = dict(n=16777216, d=1024, dtype="bf16")
 
 
@@ -177,6 +178,34 @@ def fullgrad_sweep(H, cfg, device, reps, world, rank, nccl_id):
     return ms, algo_bytes, pl
 
 
+def c5_batch(H, device, rank, reps=1):
+    """BASELINE C5: 512 independent least-squares HALP problems per GPU (4096 x 128
+    fp32 Gaussian, per-problem seeds, alpha log-uniform [1e-4, 1e-2], b in {8, 16}
+    alternating, T = 2N, K = 10, mu = 3 (unspecified in BASELINE; the golden value)),
+    solved by K5 in one launch.  Returns device ms of the batch run."""
+    import torch
+
+    P, n, d = C5["nprob"], C5["n"], C5["d"]
+    X = torch.empty((P, n, d), dtype=torch.float32, device=f"cuda:{device}")
+    Y = torch.empty((P, n), dtype=torch.float64, device=f"cuda:{device}")
+    for q in range(P):
+        x1, y1 = H.generate("regression", n, d, dtype="f32", noise_sd=0.1, seed=10_000 * (rank + 1) + q, device=device)
+        X[q].copy_(x1)
+        Y[q].copy_(y1)
+    b = H.BatchProblems(X, Y, l2=0.0, device=device)
+    rng = np.random.default_rng(rank)
+    cfgs = [H.OptimizerConfig(algorithm=H.Algorithm.Halp, alpha=float(10 ** rng.uniform(-4, -2)), epochs=C5["epochs"],
+                              inner_steps=0, bits=8 if q % 2 == 0 else 16, mu=C5["mu"], seed=q) for q in range(P)]
+    b.run([H.OptimizerConfig(algorithm=H.Algorithm.Halp, alpha=c.alpha, epochs=1, inner_steps=64, bits=c.bits,
+                             mu=c.mu, seed=c.seed) for c in cfgs])
+    ms = []
+    for _ in range(reps):
+        recs = b.run(cfgs)
+        ms.append(b.device_ms)
+    n_div = sum(r.status == "diverged" for r in recs)
+    return min(ms), n_div, P * C5["epochs"] * 2 * n
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -186,6 +215,7 @@ def main():
     ap.add_argument("--no-fullgrad", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-batch", action="store_true")
     ap.add_argument("--fg-reps", type=int, default=10)
     args = ap.parse_args()
     rank, world, local = dist_env()
@@ -323,6 +353,19 @@ def main():
                     "algorithmic_bytes_per_launch": c3["algorithmic_bytes_per_gpu"],
                     "bytes_model": "N*d*4 (x, fp32) + N*8 (y, fp64) per pass"}
 
+    # ---------------- C5: batched independent problems (K5) ----------------
+    batch = None
+    if not args.no_batch:
+        barrier()
+        bms, ndiv, inner_steps = c5_batch(H, local, rank)
+        bms = max_over_ranks(bms)
+        batch = {"workload": "C5: 512 least-squares problems/GPU, 4096x128 fp32, T=2N=8192, K=10, b 8/16, mu 3",
+                 "problems": C5["nprob"] * world, "ms_per_batch": bms,
+                 "problem_epochs_per_s": C5["nprob"] * world * C5["epochs"] / (bms / 1000.0),
+                 "inner_steps_per_s": inner_steps * world / (bms / 1000.0), "diverged": ndiv,
+                 "scaling": "weak (problems sharded, no collective)"}
+        torch.cuda.empty_cache()
+
     # ---------------- CPU baseline (rank 0, N=1 only) ----------------
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -355,7 +398,7 @@ def main():
                            "share_of_epoch": tim["inner_ms"] / ms_total if world == 1 else None},
             "c2_fullgrad_ms_per_pass": tim["fullgrad_ms"] / c2_fg_passes,
             "loss_first_last": [first_loss, final_loss],
-            "fullgrad": fullgrad, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "fullgrad": fullgrad, "batch": batch, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": gpu_launches, "clocks": clocks,
         }
         print(json.dumps(line), flush=True)

@@ -177,8 +177,12 @@ typedef struct {
 typedef struct halp_batch halp_batch;
 int  halp_batch_create(const halp_batch_desc* desc, halp_batch** out);
 void halp_batch_destroy(halp_batch* b);
-/* cfgs[nprob], recs[nprob]; every problem is an independent lpopt::run_halp */
+/* cfgs[nprob], recs[nprob]; every problem is an independent lpopt::run_halp
+ * (squared loss, d <= 256).  A diverged problem gets status DIVERGED and its
+ * partial record; the call itself returns HALP_OK.  device_ms = kernel time. */
 int  halp_batch_run(halp_batch* b, const halp_config* cfgs, halp_record* recs, double* device_ms);
+/* the batch kernel's reduction plan (for the oracle's MIRROR mode) */
+int  halp_batch_plan(const halp_batch* b, halp_plan* out);
 
 /* ---- synthetic data on the device (configs C2..C5 of BASELINE.json) ---- */
 typedef struct {

@@ -5,7 +5,7 @@ behind the C ABI in include/halp.h); this package is the Python mirror of the
 reference's C++ interface (see halp.py) plus the in-tree build (build.py).
 """
 from .halp import (  # noqa: F401
-    Algorithm, Dataset, DivergenceError, EpochOption, Error, HalpCudaError, InvalidInputError, LossFamily,
+    Algorithm, BatchProblems, Dataset, DivergenceError, EpochOption, Error, HalpCudaError, InvalidInputError, LossFamily,
     MetricRow, Objective, OptimizerConfig, RunRecord, UnsupportedError, generate, halp_scale, hash_vector,
     oracle_plan_for, plan_for, resolve_inner_steps, rng_state_after, run, run_halp, run_prepared, shard_plan,
 )

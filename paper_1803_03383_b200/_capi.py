@@ -83,7 +83,7 @@ SYMBOLS = [
     "halp_last_error", "halp_abi_version", "halp_problem_create", "halp_problem_destroy", "halp_problem_plan",
     "halp_run", "halp_full_gradient", "halp_set_trace", "halp_last_timing", "halp_bench_full_gradient",
     "halp_batch_create", "halp_batch_destroy", "halp_batch_run", "halp_datagen", "halp_shard_plan",
-    "halp_rng_state_after", "halp_plan_for",
+    "halp_rng_state_after", "halp_plan_for", "halp_batch_plan",
 ]
 
 _lib = None
@@ -113,6 +113,7 @@ def lib():
     L.halp_batch_destroy.argtypes = [P]
     L.halp_batch_destroy.restype = None
     L.halp_batch_run.argtypes = [P, C.POINTER(Config), C.POINTER(Record), C.POINTER(C.c_double)]
+    L.halp_batch_plan.argtypes = [P, C.POINTER(Plan)]
     L.halp_datagen.argtypes = [C.POINTER(DatagenDesc), C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p]
     L.halp_shard_plan.argtypes = [C.c_int64, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32] + [
         C.POINTER(C.c_int64)] * 5

@@ -751,13 +751,220 @@ extern "C" int halp_datagen(const halp_datagen_desc* desc, int32_t device, void*
 }
 
 struct halp_batch {
-  int device = 0;
+  int device = 0, dtype = 0, d = 0, ld = 0, nprob = 0, splits = 4;
+  int64_t n = 0;
+  double l2 = 0.0;
+  void* X = nullptr;
+  double* y = nullptr;
+  uint64_t *pow_tab = nullptr, *jump_tab = nullptr;
+  cudaStream_t stream = nullptr;
+  ~halp_batch() {
+    cudaSetDevice(device);
+    for (void* q : {(void*)X, (void*)y, (void*)pow_tab, (void*)jump_tab})
+      if (q) cudaFree(q);
+    if (stream) cudaStreamDestroy(stream);
+  }
 };
-extern "C" int halp_batch_create(const halp_batch_desc*, halp_batch** out) {
-  if (out) *out = nullptr;
-  return fail(HALP_UNSUPPORTED, "halp_batch_create: not built yet");
+
+extern "C" int halp_batch_create(const halp_batch_desc* desc, halp_batch** out) {
+  if (!desc || !out) return fail(HALP_INVALID_INPUT, "halp_batch_create: null argument");
+  *out = nullptr;
+  if (desc->nprob < 1 || desc->n < 1 || desc->d < 1 || !desc->X || !desc->y)
+    return fail(HALP_INVALID_INPUT, "halp_batch_create: empty problems");
+  if (!(std::isfinite(desc->l2) && desc->l2 >= 0.0)) return fail(HALP_INVALID_INPUT, "Objective: l2 must be finite and >= 0");
+  if (desc->d > 256) return fail(HALP_UNSUPPORTED, "halp_batch: d > 256 (use halp_run per problem)");
+  if (desc->dtype < 0 || desc->dtype > 2) return fail(HALP_INVALID_INPUT, "halp_batch_create: bad dtype");
+  int ndev = 0;
+  cudaError_t ce = cudaGetDeviceCount(&ndev);
+  if (ce != cudaSuccess || ndev == 0) return fail(HALP_CUDA_ERROR, "no CUDA device (no CPU fallback)");
+  CU(cudaSetDevice(desc->device));
+  auto* b = new halp_batch();
+  b->device = desc->device;
+  b->dtype = desc->dtype;
+  b->d = desc->d;
+  b->n = desc->n;
+  b->nprob = desc->nprob;
+  b->l2 = desc->l2;
+  auto bail = [&](int rc) {
+    delete b;
+    return rc;
+  };
+  const int es = elem_size(b->dtype);
+  b->ld = (int)(((int64_t)b->d * es + 15) / 16 * 16 / es);
+  b->splits = (int)std::max<int64_t>(4, make_shard_plan(b->n, b->d, 1, b->dtype, 1, 0).S);
+  const bool dev_in = desc->mem == HALP_MEM_DEVICE;
+  const size_t rows_total = (size_t)b->nprob * b->n;
+  if (cudaStreamCreateWithFlags(&b->stream, cudaStreamNonBlocking) != cudaSuccess)
+    return bail(fail(HALP_CUDA_ERROR, "cudaStreamCreate failed"));
+  if (cudaMalloc(&b->X, rows_total * b->ld * es) != cudaSuccess) return bail(fail(HALP_CUDA_ERROR, "cudaMalloc(X)"));
+  if (b->ld != b->d && cudaMemset(b->X, 0, rows_total * b->ld * es) != cudaSuccess)
+    return bail(fail(HALP_CUDA_ERROR, "cudaMemset(X)"));
+  if (cudaMemcpy2D(b->X, (size_t)b->ld * es, desc->X, (size_t)b->d * es, (size_t)b->d * es, rows_total,
+                   dev_in ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice) != cudaSuccess)
+    return bail(fail(HALP_CUDA_ERROR, "copy of X failed"));
+  if (cudaMalloc(&b->y, sizeof(double) * rows_total) != cudaSuccess) return bail(fail(HALP_CUDA_ERROR, "cudaMalloc(y)"));
+  if (cudaMemcpy(b->y, desc->y, sizeof(double) * rows_total, dev_in ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice) !=
+      cudaSuccess)
+    return bail(fail(HALP_CUDA_ERROR, "copy of y failed"));
+  const auto& jt = JumpTables::get();
+  if (cudaMalloc(&b->pow_tab, sizeof(uint64_t) * jt.flat.size()) != cudaSuccess ||
+      cudaMemcpy(b->pow_tab, jt.flat.data(), sizeof(uint64_t) * jt.flat.size(), cudaMemcpyHostToDevice) != cudaSuccess)
+    return bail(fail(HALP_CUDA_ERROR, "RNG tables"));
+  std::vector<uint64_t> tab(2048);
+  mat_tables(jt.power((uint64_t)b->d), tab.data());
+  if (cudaMalloc(&b->jump_tab, sizeof(uint64_t) * 2048) != cudaSuccess ||
+      cudaMemcpy(b->jump_tab, tab.data(), sizeof(uint64_t) * 2048, cudaMemcpyHostToDevice) != cudaSuccess)
+    return bail(fail(HALP_CUDA_ERROR, "RNG tables"));
+  *out = b;
+  return HALP_OK;
 }
+
 extern "C" void halp_batch_destroy(halp_batch* b) { delete b; }
-extern "C" int halp_batch_run(halp_batch*, const halp_config*, halp_record*, double*) {
-  return fail(HALP_UNSUPPORTED, "halp_batch_run: not built yet");
+
+extern "C" int halp_batch_plan(const halp_batch* b, halp_plan* out) {
+  if (!b || !out) return fail(HALP_INVALID_INPUT, "halp_batch_plan: null argument");
+  *out = halp_plan{};
+  out->fg_threads = 32;
+  out->fg_vec = 16 / elem_size(b->dtype);
+  out->fg_splits = b->splits;
+  out->in_ctas = 1;
+  out->in_threads = 32;
+  const int M = (b->d + 31) / 32;
+  out->in_per = M <= 1 ? 1 : M <= 2 ? 2 : M <= 4 ? 4 : 8;
+  out->fg_split_begin = 0;
+  out->fg_split_end = b->splits;
+  return HALP_OK;
+}
+
+extern "C" int halp_batch_run(halp_batch* b, const halp_config* cfgs, halp_record* recs, double* device_ms) {
+  if (!b || !cfgs || !recs) return fail(HALP_INVALID_INPUT, "halp_batch_run: null argument");
+  CU(cudaSetDevice(b->device));
+  const int P = b->nprob, D = b->d;
+  std::vector<double> alpha(P), mu(P), dmin(P), divl(P), mev(P);
+  std::vector<int> bits(P), epochs(P), option(P);
+  std::vector<int64_t> T(P);
+  std::vector<uint64_t> seeds(2 * (size_t)P);
+  std::vector<double> init((size_t)P * D, 0.0);
+  bool any_init = false;
+  int max_rows = 2;
+  for (int q = 0; q < P; ++q) {
+    const halp_config& c = cfgs[q];
+    int rc = validate(nullptr, &c);
+    if (rc) {
+      g_err = "problem " + std::to_string(q) + ": " + g_err;
+      return rc;
+    }
+    T[q] = c.inner_steps > 0 ? c.inner_steps : (int64_t)c.full_grad_period * b->n;
+    alpha[q] = c.alpha;
+    mu[q] = c.mu;
+    dmin[q] = c.delta_min;
+    divl[q] = c.divergence_limit;
+    mev[q] = c.metric_every_passes;
+    bits[q] = c.bits;
+    epochs[q] = c.epochs;
+    option[q] = c.option;
+    seeds[2 * q] = rng_seed_state(c.seed, 0);
+    seeds[2 * q + 1] = rng_seed_state(c.seed, 1);
+    if (c.init) {
+      any_init = true;
+      std::memcpy(&init[(size_t)q * D], c.init, sizeof(double) * D);
+    }
+    max_rows = std::max(max_rows, std::max(c.epochs, 0) + 2);
+  }
+  // one device arena for the parameters and the outputs
+  std::vector<void*> bufs;
+  auto dev = [&](const void* src, size_t bytes) -> void* {
+    void* p = nullptr;
+    if (cudaMalloc(&p, std::max<size_t>(bytes, 8)) != cudaSuccess) return nullptr;
+    bufs.push_back(p);
+    if (src) cudaMemcpyAsync(p, src, bytes, cudaMemcpyHostToDevice, b->stream);
+    return p;
+  };
+  BatchParams bp{};
+  bp.X = b->X;
+  bp.ld = b->ld;
+  bp.d = D;
+  bp.dtype = b->dtype;
+  bp.n = b->n;
+  bp.nprob = P;
+  bp.y = b->y;
+  bp.l2 = b->l2;
+  bp.alpha = (const double*)dev(alpha.data(), 8 * P);
+  bp.mu = (const double*)dev(mu.data(), 8 * P);
+  bp.delta_min = (const double*)dev(dmin.data(), 8 * P);
+  bp.div_limit = (const double*)dev(divl.data(), 8 * P);
+  bp.metric_every = (const double*)dev(mev.data(), 8 * P);
+  bp.bits = (const int*)dev(bits.data(), 4 * P);
+  bp.epochs = (const int*)dev(epochs.data(), 4 * P);
+  bp.option = (const int*)dev(option.data(), 4 * P);
+  bp.T = (const int64_t*)dev(T.data(), 8 * P);
+  bp.seed = (const uint64_t*)dev(seeds.data(), 16 * P);
+  bp.init = any_init ? (const double*)dev(init.data(), 8 * (size_t)P * D) : nullptr;
+  bp.pow_tab = b->pow_tab;
+  bp.jump_tab = b->jump_tab;
+  bp.splits = b->splits;
+  bp.max_rows = max_rows;
+  bp.rows = (double*)dev(nullptr, 8 * 5 * (size_t)P * max_rows);
+  bp.rhash = (uint64_t*)dev(nullptr, 8 * (size_t)P * max_rows);
+  bp.rows_n = (int*)dev(nullptr, 4 * P);
+  bp.status = (int*)dev(nullptr, 4 * P);
+  bp.steps = (int64_t*)dev(nullptr, 8 * P);
+  bp.w_out = (double*)dev(nullptr, 8 * (size_t)P * D);
+  auto cleanup = [&]() {
+    for (void* q : bufs) cudaFree(q);
+  };
+  for (void* q : bufs)
+    if (!q) {
+      cleanup();
+      return fail(HALP_CUDA_ERROR, "halp_batch_run: cudaMalloc failed");
+    }
+  cudaEvent_t e0, e1;
+  CU(cudaEventCreate(&e0));
+  CU(cudaEventCreate(&e1));
+  CU(cudaEventRecord(e0, b->stream));
+  cudaError_t le = launch_batch(bp, 128, b->stream);
+  CU(cudaEventRecord(e1, b->stream));
+  if (le != cudaSuccess) {
+    cleanup();
+    return fail(HALP_CUDA_ERROR, std::string("launch_batch: ") + cudaGetErrorString(le));
+  }
+  std::vector<double> rows(5 * (size_t)P * max_rows), wout((size_t)P * D);
+  std::vector<uint64_t> rh((size_t)P * max_rows);
+  std::vector<int> rn(P), st(P);
+  std::vector<int64_t> stp(P);
+  CU(cudaMemcpyAsync(rows.data(), bp.rows, rows.size() * 8, cudaMemcpyDeviceToHost, b->stream));
+  CU(cudaMemcpyAsync(rh.data(), bp.rhash, rh.size() * 8, cudaMemcpyDeviceToHost, b->stream));
+  CU(cudaMemcpyAsync(rn.data(), bp.rows_n, 4 * P, cudaMemcpyDeviceToHost, b->stream));
+  CU(cudaMemcpyAsync(st.data(), bp.status, 4 * P, cudaMemcpyDeviceToHost, b->stream));
+  CU(cudaMemcpyAsync(stp.data(), bp.steps, 8 * P, cudaMemcpyDeviceToHost, b->stream));
+  CU(cudaMemcpyAsync(wout.data(), bp.w_out, wout.size() * 8, cudaMemcpyDeviceToHost, b->stream));
+  CU(cudaStreamSynchronize(b->stream));
+  float ms = 0;
+  cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cleanup();
+  if (device_ms) *device_ms = ms;
+  int invalid = -1;
+  for (int q = 0; q < P; ++q) {
+    halp_record& r = recs[q];
+    r.rows_n = std::min(rn[q], r.rows_cap);
+    for (int k = 0; k < r.rows_n; ++k) {
+      const double* src = &rows[((size_t)q * max_rows + k) * 5];
+      r.rows[k] = halp_row{src[0], src[1], src[2], src[3], src[4], rh[(size_t)q * max_rows + k]};
+    }
+    r.status = st[q] == 1 ? HALP_STATUS_CONVERGED : st[q] >= 2 ? HALP_STATUS_DIVERGED : HALP_STATUS_OK;
+    r.steps_taken = stp[q];
+    r.inner_fp_vector_ops = 0;
+    r.inner_lp_vector_ops = 0;
+    if (st[q] <= 1) {
+      const int64_t ep = T[q] > 0 ? stp[q] / T[q] : 0;
+      r.inner_fp_vector_ops = (uint64_t)(8 * T[q] * ep);
+    }
+    if (r.final_iterate) std::memcpy(r.final_iterate, &wout[(size_t)q * D], sizeof(double) * D);
+    if (st[q] == 3 && invalid < 0) invalid = q;
+  }
+  if (invalid >= 0)
+    return fail(HALP_INVALID_INPUT, "problem " + std::to_string(invalid) + ": LPRepr: delta must be positive and finite");
+  return HALP_OK;
 }

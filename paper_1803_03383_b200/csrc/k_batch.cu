@@ -1,7 +1,412 @@
-// k_batch.cu -- K5: many independent HALP problems, one persistent CTA each.
+// k_batch.cu -- K5: many independent HALP problems (BASELINE config C5, and the
+// reference's grid / conditioning-sweep workloads, harness.cpp:379-518, which
+// run one lpopt::run_prepared per configuration sequentially).  One CTA of
+// four warps owns one problem and runs the WHOLE lpopt::run_halp
+// (optimizers.cpp:387-459) for it in a single launch: every epoch's full
+// gradient + loss, centering, the T-step inner loop, the Recorder rows
+// (pass, loss, grad norm, delta, FNV-1a iterate hash, optimizers.cpp:104-167,
+// 218-227), divergence / blow-up and convergence.  Problems are independent:
+// no collective, shard them across GPUs.
+//
+// Floating-point order = the single-problem kernels', so the oracle's MIRROR
+// mode (plan of halp_plan_for(n, d, 1)) checks K5 bit for bit:
+//   * full gradient: the K1 split tree -- S splits (power of two), warp w
+//     owns the aligned subtree of splits [w*S/4, (w+1)*S/4) and merges them
+//     in order with a binary-counter stack; the 4 warp roots are combined as
+//     the top of the pairwise tree.  Row dot: lane l owns the 16-byte groups
+//     l, l+32, ... (K1 with fg_threads = 32, which is what the plan picks
+//     for d <= 128 fp32); gradient column = sequential fma over the split's rows.
+//   * finalize: k_finalize's 256-strided order for |g| and |w|.
+//   * inner loop: K3 with one CTA of one warp, M = D/32 coordinates per lane.
+// Squared loss only (the C5 / sweep workloads); d*C <= 256.
 #include "halp_device.cuh"
 #include "kernels.h"
 
 namespace halp {
-cudaError_t launch_batch(const BatchParams&, int, cudaStream_t) { return cudaErrorNotSupported; }
+
+constexpr int kBatchMaxM = 8;     // D <= 256
+constexpr int kBatchMaxLev = 16;  // splits per warp <= 2^15
+
+template <class Tx> struct BVec;
+template <> struct BVec<float> { static constexpr int V = 4; };
+template <> struct BVec<double> { static constexpr int V = 2; };
+template <> struct BVec<__nv_bfloat16> { static constexpr int V = 8; };
+
+template <class Tx>
+__device__ __forceinline__ void load_group_g(const Tx* p, double* out) {
+  const uint4 raw = __ldg(reinterpret_cast<const uint4*>(p));
+  if constexpr (sizeof(Tx) == 4) {
+    out[0] = (double)__uint_as_float(raw.x);
+    out[1] = (double)__uint_as_float(raw.y);
+    out[2] = (double)__uint_as_float(raw.z);
+    out[3] = (double)__uint_as_float(raw.w);
+  } else if constexpr (sizeof(Tx) == 2) {
+    const uint32_t wds[4] = {raw.x, raw.y, raw.z, raw.w};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      out[2 * q] = (double)__uint_as_float(wds[q] << 16);
+      out[2 * q + 1] = (double)__uint_as_float(wds[q] & 0xFFFF0000u);
+    }
+  } else {
+    out[0] = __longlong_as_double(((long long)raw.y << 32) | raw.x);
+    out[1] = __longlong_as_double(((long long)raw.w << 32) | raw.z);
+  }
+}
+
+__device__ __forceinline__ uint64_t fnv1a_doubles(const double* v, int len) {
+  uint64_t h = 1469598103934665603ULL;
+  for (int k = 0; k < len; ++k) {
+    const uint64_t b = (uint64_t)__double_as_longlong(v[k]);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      h ^= (b >> (8 * q)) & 0xFF;
+      h *= 1099511628211ULL;
+    }
+  }
+  return h;
+}
+
+// NG groups of V features per lane (NG*V*32 >= d)
+template <class Tx, int NG, int M>
+__global__ void __launch_bounds__(128) k5_batch(BatchParams p) {
+  constexpr int V = BVec<Tx>::V;
+  const int prob = blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int d = p.d, D = d, ld = p.ld;
+  const int64_t n = p.n;
+  const int S = p.splits;
+  const Tx* X = reinterpret_cast<const Tx*>(p.X) + (size_t)prob * n * ld;
+  const double* y = p.y + (size_t)prob * n;
+
+  __shared__ double w_s[264], g_s[264], wsum[4][257];  // iterate, g~, warp subtree roots (+loss)
+  __shared__ double stats[4];
+  __shared__ int sh_stop, sh_blew;
+
+  const double alpha = p.alpha[prob], mu = p.mu[prob], dmin = p.delta_min[prob], divl = p.div_limit[prob];
+  const int bits = p.bits[prob], epochs = p.epochs[prob], opt2 = p.option[prob];
+  const int64_t T = p.T[prob];
+  const double l2 = p.l2;
+  const double hi = bits == 64 ? 9223372036854775807.0 : (double)((1LL << (bits - 1)) - 1);
+  const double lo = bits == 64 ? -9223372036854775808.0 : (double)(-(1LL << (bits - 1)));
+  const long long maxc = bits == 64 ? 0x7FFFFFFFFFFFFFFFLL : (1LL << (bits - 1)) - 1;
+  const long long minc = bits == 64 ? (long long)0x8000000000000000ULL : -(1LL << (bits - 1));
+  const bool wide = hi > 0x1.0p53;
+  double* rows = p.rows + (size_t)prob * p.max_rows * 5;
+  uint64_t* rhash = p.rhash + (size_t)prob * p.max_rows;
+  const uint64_t t_start = globaltimer_ns();
+
+  for (int k = tid; k < 264; k += 128) w_s[k] = (k < D && p.init) ? p.init[(size_t)prob * D + k] : 0.0;
+  if (tid == 0) {
+    sh_stop = 0;
+    sh_blew = 0;
+  }
+  __syncthreads();
+
+  // RNG states (seeding as rng.hpp:29-32, done on the host: p.seed holds the
+  // stream-0 / stream-1 initial states interleaved)
+  uint64_t s_sample = p.seed[2 * prob];   // stream 0 state (lane-uniform)
+  const uint64_t s_round0 = p.seed[2 * prob + 1];
+  const uint64_t* jtD = p.jump_tab;       // X^D table (global, read-only)
+
+  int nrow = 0;
+  int status = 0;  // 0 ok, 1 converged, 2 diverged
+  int64_t steps = 0;
+  double next_pass = 0.0;
+  const double metric_every = p.metric_every[prob];
+
+  auto boundary = [&](double pass, const double* wv, double loss, double gn, double delta, bool forced) -> bool {
+    // Recorder::boundary (optimizers.cpp:125-152), lane 0 of warp 0; returns "bad"
+    const bool bad = !(isfinite(loss) && isfinite(gn)) || loss > divl || gn > divl;
+    const bool due = forced || metric_every <= 0.0 || pass + 1e-9 >= next_pass;
+    if ((due || bad) && nrow < p.max_rows) {
+      double* r = rows + (size_t)nrow * 5;
+      r[0] = pass;
+      r[1] = (double)(globaltimer_ns() - t_start) * 1e-9;
+      r[2] = loss;
+      r[3] = gn;
+      r[4] = delta;
+      rhash[nrow] = fnv1a_doubles(wv, D);
+      ++nrow;
+      if (metric_every > 0.0) next_pass = pass + metric_every;
+    }
+    return bad;
+  };
+
+  // ---- full gradient + loss in the K1 order; result -> g_s, stats ----
+  auto full_pass = [&]() {
+    // warp w: splits [w*S/4, (w+1)*S/4), binary-counter tree
+    const int sw = S / 4;
+    double stk[kBatchMaxLev][NG * V + 1];
+    int cnt = 0;
+    for (int si = 0; si < sw; ++si) {
+      const int s = wid * sw + si;
+      const int64_t r0 = (int64_t)(((unsigned long long)n * s) / S);
+      const int64_t r1 = (int64_t)(((unsigned long long)n * (s + 1)) / S);
+      double acc[NG * V + 1];
+#pragma unroll
+      for (int q = 0; q < NG * V + 1; ++q) acc[q] = 0.0;
+      for (int64_t r = r0; r < r1; ++r) {
+        double xv[NG][V];
+        double dot = 0.0;
+#pragma unroll
+        for (int k = 0; k < NG; ++k) {
+          const int g = lane + 32 * k;
+          if (g * V < d) {
+            load_group_g<Tx>(X + r * ld + g * V, xv[k]);
+#pragma unroll
+            for (int q = 0; q < V; ++q) dot = fma(xv[k][q], w_s[g * V + q], dot);
+          } else {
+#pragma unroll
+            for (int q = 0; q < V; ++q) xv[k][q] = 0.0;
+          }
+        }
+        dot = warp_allsum(dot);
+        const double e = dot - y[r];
+        acc[NG * V] = acc[NG * V] + __dmul_rn(__dmul_rn(0.5, e), e);
+#pragma unroll
+        for (int k = 0; k < NG; ++k)
+#pragma unroll
+          for (int q = 0; q < V; ++q) acc[k * V + q] = fma(e, xv[k][q], acc[k * V + q]);
+      }
+      // merge split si into the stack (pairwise tree over the warp's splits)
+      int c = si;
+      while (c & 1) {
+        --cnt;
+#pragma unroll
+        for (int q = 0; q < NG * V + 1; ++q) acc[q] = stk[cnt][q] + acc[q];
+        c >>= 1;
+      }
+#pragma unroll
+      for (int q = 0; q < NG * V + 1; ++q) stk[cnt][q] = acc[q];
+      ++cnt;
+    }
+#pragma unroll
+    for (int k = 0; k < NG; ++k)
+#pragma unroll
+      for (int q = 0; q < V; ++q) {
+        const int j = (lane + 32 * k) * V + q;
+        if (j < D) wsum[wid][j] = stk[0][k * V + q];
+      }
+    if (lane == 0) wsum[wid][256] = stk[0][NG * V];
+    __syncthreads();
+    // top of the tree: ((w0 + w1) + (w2 + w3)); g = sum/n + l2 w; norms (k_finalize order)
+    double ag = 0.0, aw = 0.0;
+    for (int k = tid; k < 256; k += 128) {
+      if (k < D) {
+        const double tot = (wsum[0][k] + wsum[1][k]) + (wsum[2][k] + wsum[3][k]);
+        const double g = tot / (double)n + __dmul_rn(l2, w_s[k]);
+        g_s[k] = g;
+      }
+    }
+    __syncthreads();
+    if (wid == 0) {
+      // 256 virtual threads: v[t] = g[t]^2 (t < D), 8 virtual warps of 32 in order
+      double sg = 0.0, sw2 = 0.0;
+      for (int vw = 0; vw < 8; ++vw) {
+        const int t = vw * 32 + lane;
+        ag = t < D ? fma(g_s[t], g_s[t], 0.0) : 0.0;
+        aw = t < D ? fma(w_s[t], w_s[t], 0.0) : 0.0;
+        ag = warp_allsum(ag);
+        aw = warp_allsum(aw);
+        sg = vw == 0 ? ag : sg + ag;
+        sw2 = vw == 0 ? aw : sw2 + aw;
+      }
+      if (lane == 0) {
+        const double ltot = (wsum[0][256] + wsum[1][256]) + (wsum[2][256] + wsum[3][256]);
+        const double gn = sqrt(sg);
+        double delta = 0.0;
+        if (isfinite(gn) && gn > 0.0) {
+          const double span = ldexp(1.0, bits - 1) - 1.0;
+          const double sc = gn / __dmul_rn(mu, span);
+          delta = (sc < dmin) ? dmin : sc;
+        }
+        stats[0] = gn;
+        stats[1] = delta;
+        stats[2] = ltot / (double)n + __dmul_rn(__dmul_rn(0.5, l2), sw2);
+      }
+    }
+    __syncthreads();
+  };
+
+  // inner-loop state (warp 0): lane l owns coordinates [l*M, l*M + M)
+  double wt[M], gtl[M], code[M], snap[M], up[M];
+  bool valid[M];
+  const int k0 = lane * M;
+#pragma unroll
+  for (int i = 0; i < M; ++i) valid[i] = (k0 + i) < D;
+  uint64_t rs = 0;
+  if (wid == 0) rs = jump_count(s_round0, (uint64_t)(D + k0), p.pow_tab);  // after Q(0) of epoch 0
+
+  bool converged = false;
+  for (int k = 0; k < epochs && !converged; ++k) {
+    full_pass();
+    const double gn = stats[0], delta = stats[1], loss = stats[2];
+    if (tid == 0) {
+      const bool bad = boundary((double)steps / (double)n, w_s, loss, gn, delta, k == 0 || gn == 0.0);
+      if (bad) {
+        status = 2;
+        sh_stop = 2;
+      } else if (gn == 0.0) {
+        status = 1;
+        sh_stop = 1;
+      } else if (!(isfinite(delta) && delta > 0.0)) {
+        status = 3;
+        sh_stop = 3;
+      }
+    }
+    __syncthreads();
+    if (sh_stop) {
+      converged = sh_stop == 1;
+      break;
+    }
+    if (wid == 0) {
+      const double rcp = 1.0 / delta;
+      const bool use_rcp = isfinite(rcp) && rcp != 0.0;
+#pragma unroll
+      for (int i = 0; i < M; ++i) {
+        wt[i] = valid[i] ? w_s[k0 + i] : 0.0;
+        gtl[i] = valid[i] ? g_s[k0 + i] : 0.0;
+        code[i] = 0.0;
+        snap[i] = 0.0;
+        up[i] = 0.0;
+      }
+      int64_t t_pick = -1;
+      if (opt2) {
+        s_sample = xs_step(s_sample);
+        t_pick = (int64_t)index_of(s_sample, (uint64_t)T);
+      }
+      int blow = -1;
+      for (int64_t t = 0; t < T; ++t) {
+        if (t == t_pick) {
+#pragma unroll
+          for (int i = 0; i < M; ++i) snap[i] = code[i];
+        }
+        s_sample = xs_step(s_sample);
+        const int64_t row = (int64_t)index_of(s_sample, (uint64_t)n);
+        double xc[M];
+#pragma unroll
+        for (int i = 0; i < M; ++i) xc[i] = valid[i] ? to_d<Tx>(X[row * ld + k0 + i]) : 0.0;
+        double a = 0.0, b = 0.0;
+#pragma unroll
+        for (int i = 0; i < M; ++i) {
+          if (!valid[i]) continue;
+          const double z = __dmul_rn(code[i], delta);
+          a = fma(xc[i], wt[i] + z, a);
+          b = fma(xc[i], wt[i], b);
+        }
+        a = warp_allsum(a);
+        b = warp_allsum(b);
+        const double yi = y[row];
+        const double e1 = a - yi, e2 = b - yi;
+        bool bad = false, slow_any = false;
+        bool slow[M];
+        uint64_t s = rs;
+#pragma unroll
+        for (int i = 0; i < M; ++i) {
+          s = xs_step(s);
+          const double U = uniform_of(s);
+          const double z = __dmul_rn(code[i], delta);
+          const double wz = wt[i] + z;
+          const double g1 = __dmul_rn(e1, xc[i]) + __dmul_rn(l2, wz);
+          const double g2 = __dmul_rn(e2, xc[i]) + __dmul_rn(l2, wt[i]);
+          const double u = z - __dmul_rn(alpha, (g1 - g2) + gtl[i]);
+          up[i] = u;
+          bad |= valid[i] && !isfinite(u);
+          if (use_rcp && !wide) {
+            code[i] = quantize_fast(u, delta, rcp, hi, lo, U, slow[i]);
+            slow_any |= valid[i] && slow[i];
+          } else {
+            code[i] = (double)quantize_code(u, delta, hi, lo, maxc, minc, U);
+          }
+        }
+        if (slow_any) {
+          s = rs;
+#pragma unroll
+          for (int i = 0; i < M; ++i) {
+            s = xs_step(s);
+            if (valid[i] && slow[i]) code[i] = (double)quantize_code(up[i], delta, hi, lo, maxc, minc, uniform_of(s));
+          }
+        }
+        rs = jump_tab(rs, jtD);
+        if (__any_sync(0xffffffffu, bad)) {
+          blow = (int)t;
+          break;
+        }
+      }
+      if (blow >= 0) {
+        // Recorder::blowup: row (inf, inf, delta) hashed over u (optimizers.cpp:156-160)
+#pragma unroll
+        for (int i = 0; i < M; ++i)
+          if (valid[i]) g_s[k0 + i] = up[i];
+        __syncwarp();
+        if (lane == 0) {
+          boundary((double)(steps + blow + 1) / (double)n, g_s, INFINITY, INFINITY, delta, true);
+          status = 2;
+          sh_stop = 2;
+          sh_blew = 1;
+          for (int q = 0; q < D; ++q) p.w_out[(size_t)prob * D + q] = g_s[q];
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < M; ++i)
+          if (valid[i]) w_s[k0 + i] = wt[i] + __dmul_rn(t_pick >= 0 ? snap[i] : code[i], delta);
+        // next epoch: skip its Q(0) draws
+        rs = jump_tab(rs, jtD);
+      }
+    }
+    __syncthreads();
+    if (sh_stop) break;
+    steps += T;
+  }
+  if (!sh_stop && !converged) {
+    full_pass();
+    if (tid == 0) {
+      const bool bad = boundary((double)steps / (double)n, w_s, stats[2], stats[0], stats[1], true);
+      if (bad) status = 2;
+      else if (stats[0] == 0.0) status = 1;
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    p.rows_n[prob] = nrow;
+    p.status[prob] = status;
+    p.steps[prob] = (status >= 2) ? 0 : steps;
+  }
+  if (!sh_blew)
+    for (int q = tid; q < D; q += 128) p.w_out[(size_t)prob * D + q] = w_s[q];
+}
+
+template <class Tx, int NG>
+static cudaError_t launch_b_ng(const BatchParams& p, cudaStream_t st) {
+  const int M = (p.d + 31) / 32;
+  switch (M <= 1 ? 1 : M <= 2 ? 2 : M <= 4 ? 4 : 8) {
+    case 1: k5_batch<Tx, NG, 1><<<p.nprob, 128, 0, st>>>(p); break;
+    case 2: k5_batch<Tx, NG, 2><<<p.nprob, 128, 0, st>>>(p); break;
+    case 4: k5_batch<Tx, NG, 4><<<p.nprob, 128, 0, st>>>(p); break;
+    default: k5_batch<Tx, NG, 8><<<p.nprob, 128, 0, st>>>(p); break;
+  }
+  return cudaGetLastError();
+}
+
+template <class Tx>
+static cudaError_t launch_b_dt(const BatchParams& p, cudaStream_t st) {
+  constexpr int V = BVec<Tx>::V;
+  const int ngroups = (p.d + V - 1) / V;
+  const int NG = (ngroups + 31) / 32;
+  switch (NG) {
+    case 1: return launch_b_ng<Tx, 1>(p, st);
+    case 2: return launch_b_ng<Tx, 2>(p, st);
+    default: return cudaErrorInvalidConfiguration;
+  }
+}
+
+cudaError_t launch_batch(const BatchParams& p, int /*threads*/, cudaStream_t st) {
+  if (p.d > 256 || p.d < 1 || (p.splits & (p.splits - 1)) || p.splits < 4) return cudaErrorInvalidConfiguration;
+  switch (p.dtype) {
+    case 0: return launch_b_dt<double>(p, st);
+    case 1: return launch_b_dt<float>(p, st);
+    default: return launch_b_dt<__nv_bfloat16>(p, st);
+  }
+}
+
 }  // namespace halp

@@ -89,31 +89,32 @@ cudaError_t launch_datagen(const GenParams& p, cudaStream_t st);
 
 // ---- K5 batched independent problems ----
 struct BatchParams {
-  const void* X;       // [nprob][n][ld]
+  const void* X;        // [nprob][n][ld]
   int ld, d, dtype;
   int64_t n;
   int nprob;
-  const double* y;     // [nprob][n]
+  const double* y;      // [nprob][n]
   double l2;
-  const double* alpha; // per problem
+  const double* alpha;  // per problem
   const double* mu;
-  const int* bits;
-  const int* epochs;
-  const int64_t* T;
-  const int* option;
-  const uint64_t* seed;
   const double* delta_min;
   const double* div_limit;
-  const double* init;  // [nprob][d] or null
+  const double* metric_every;
+  const int* bits;
+  const int* epochs;
+  const int* option;
+  const int64_t* T;
+  const uint64_t* seed;  // [nprob][2]: initial states of streams 0 and 1 (rng.hpp:29-32)
+  const double* init;    // [nprob][d] or null
   const uint64_t* pow_tab;
-  int max_rows;
-  double* rows;        // [nprob][max_rows][5] (pass, loss, gn, delta, hash-as-bits)
+  const uint64_t* jump_tab;  // X^d
+  int splits, max_rows;
+  double* rows;          // [nprob][max_rows][5]: pass, seconds, loss, grad_norm, delta
+  uint64_t* rhash;       // [nprob][max_rows]
   int* rows_n;
-  int* status;
+  int* status;           // 0 ok, 1 converged, 2 diverged, 3 invalid delta
   int64_t* steps;
-  double* w_out;       // [nprob][d]
-  double* u_out;       // [nprob][d] blowup vectors
-  uint64_t* rhash;     // [nprob][max_rows]
+  double* w_out;         // [nprob][d] final iterate (the failing update on blow-up)
 };
 cudaError_t launch_batch(const BatchParams& p, int threads, cudaStream_t st);
 

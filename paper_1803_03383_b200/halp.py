@@ -404,6 +404,75 @@ def halp_scale(grad_norm: float, mu: float, bits: int) -> float:
     return grad_norm / (mu * (math.ldexp(1.0, bits - 1) - 1.0))
 
 
+class BatchProblems:
+    """Many independent least-squares problems of one shape (BASELINE C5 and the
+    reference's grid / conditioning sweeps, harness.cpp:379-518) solved by the
+    batched kernel K5: one CTA per problem runs the whole run_halp.
+
+    X: [nprob, n, d] (numpy float64/float32/bf16-as-uint16, or a CUDA tensor),
+    y: [nprob, n].  run(cfgs) returns one RunRecord per problem; a problem that
+    diverges gets status "diverged" and its partial record (run_prepared
+    semantics, harness.cpp:309-311) instead of an exception."""
+
+    def __init__(self, X, y, l2: float = 0.0, device: int = 0):
+        dev = _is_torch_cuda(X)
+        if dev:
+            import torch
+
+            X = X.contiguous()
+            y = torch.as_tensor(y, dtype=torch.float64, device=X.device).contiguous()
+            xptr, yptr = X.data_ptr(), y.data_ptr()
+        else:
+            X = np.ascontiguousarray(X)
+            y = np.ascontiguousarray(y, dtype=np.float64)
+            xptr, yptr = X.ctypes.data, y.ctypes.data
+        self._keep = [X, y]
+        nprob, n, d = (int(v) for v in X.shape)
+        self.nprob, self.n, self.d = nprob, n, d
+        desc = A.BatchDesc(xptr, _x_dtype(X), A.MEM_DEVICE if dev else A.MEM_HOST, n, d, nprob, yptr, float(l2),
+                           device)
+        h = C.c_void_p()
+        rc = A.lib().halp_batch_create(C.byref(desc), C.byref(h))
+        if rc:
+            _raise(rc)
+        self._h = h
+        self.device_ms = 0.0
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            A.lib().halp_batch_destroy(h)
+            self._h = None
+
+    def plan(self) -> dict:
+        pl = A.Plan()
+        rc = A.lib().halp_batch_plan(self._h, C.byref(pl))
+        if rc:
+            _raise(rc)
+        return {k: getattr(pl, k) for k, _ in A.Plan._fields_}
+
+    def oracle_plan(self) -> dict:
+        p = self.plan()
+        return {k: p[k] for k in ("fg_threads", "fg_vec", "fg_splits", "in_ctas", "in_threads", "in_per")}
+
+    def run(self, cfgs) -> list:
+        if len(cfgs) != self.nprob:
+            raise InvalidInputError("halp_batch_run: one config per problem")
+        keep: list = []
+        carr = (A.Config * self.nprob)(*[_to_c_config(c, keep) for c in cfgs])
+        caps = [max(c.epochs, 0) + 2 for c in cfgs]
+        rows = [(A.Row * cap)() for cap in caps]
+        fins = [np.zeros(self.d, dtype=np.float64) for _ in cfgs]
+        recs = (A.Record * self.nprob)(*[A.Record(rows[i], caps[i], 0, fins[i].ctypes.data, 0, 0, 0, 0)
+                                         for i in range(self.nprob)])
+        ms = C.c_double()
+        rc = A.lib().halp_batch_run(self._h, carr, recs, C.byref(ms))
+        if rc:
+            _raise(rc)
+        self.device_ms = ms.value
+        return [_record(recs[i], rows[i], fins[i]) for i in range(self.nprob)]
+
+
 def generate(kind: str, n: int, d: int, *, num_classes: int = 0, dtype: str = "f32", noise_sd: float = 0.0,
              x_scale: float = 1.0, density: float = 1.0, seed: int = 0, device: int = 0):
     """K6 device generator for the BASELINE synthetic configs; returns torch
