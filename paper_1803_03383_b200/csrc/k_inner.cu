@@ -10,22 +10,23 @@
 //
 // Layout: the D = d*C flat coordinates (column-major d x C, objectives.hpp:56-58)
 // are split over the cluster: thread tau = rank*T3 + tid owns the M
-// contiguous coordinates [tau*M, tau*M + M).  w~, g~ and the integer codes
-// of z live in registers for the whole epoch; only the sampled row x_i is
-// read from memory each step, prefetched two steps ahead in raw form.
+// contiguous coordinates [tau*M, tau*M + M).  w~, g~ and the codes of z live
+// in registers for the whole epoch; the sampled row x_i (and, when
+// precomputed, the step's rounding uniforms) are prefetched two steps ahead.
 //
 // Rounding stream: the reference's xorshift64* stream 1, reproduced exactly.
-// Coordinate k of step t uses draw  D*(t+1) + k  of the epoch (after the D
-// draws of Q(0)); a thread steps its M draws sequentially and jumps D draws
-// per step with the GF(2) table of X^D (rng_jump.hpp) held in shared memory.
+// Coordinate k of step t uses draw  D*(t+1) + k  of the epoch.  Either the
+// epoch's uniforms are precomputed by k_uniforms (K4b, fully parallel) and
+// streamed from HBM, or each thread steps its M draws and jumps D draws per
+// step with the GF(2) table of X^D held in shared memory.
 //
-// One cluster barrier per step.  Each warp reduces its partial logits with an
-// xor-butterfly reduce-scatter and stores them into every CTA of the cluster
-// (DSMEM).  After the barrier EVERY warp redundantly combines the warp
-// partials and evaluates the loss derivative (lane-parallel softmax: lane c
-// = class c at wz, lane 16+c = at w~), so nothing is broadcast through a
-// second barrier.  The non-finite flag of step t is published with the
-// partials of step t+1.
+// Per step, ONE exchange: each warp reduces its partial logits with an
+// xor-butterfly reduce-scatter and sends them (with its non-finite flag of the
+// previous step) to every CTA of the cluster with st.async, completing on the
+// receiver's mbarrier (no cluster barrier); a single CTA uses shared memory +
+// __syncthreads.  Then EVERY warp combines the partials and evaluates the loss
+// derivative itself (lane-parallel softmax: lane c = class c at wz, lane 16+c
+// = at w~), so nothing is broadcast through a second barrier.
 //
 // Reduction order (mirrored by oracle MIRROR mode): thread partial =
 // sequential fma over its coordinates; warp = xor butterfly 16..1; across
@@ -39,14 +40,66 @@ namespace halp {
 
 constexpr int kMaxWarpsPerCluster = 128;
 
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "W_%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra W_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ uint32_t mapa_u32(const void* p, uint32_t rank) {
+  uint32_t ra;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(smem_u32(p)), "r"(rank));
+  return ra;
+}
+__device__ __forceinline__ void st_async_f64(uint32_t raddr, double v, uint32_t rbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f64 [%0], %1, [%2];" ::"r"(raddr), "d"(v),
+               "r"(rbar)
+               : "memory");
+}
+__device__ __forceinline__ void st_async_v2f64(uint32_t raddr, double a, double b, uint32_t rbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];" ::"r"(raddr),
+               "d"(a), "d"(b), "r"(rbar)
+               : "memory");
+}
+
+// the M raw elements x[fj[i]] of a row (one vector load when they are
+// contiguous and aligned, else one load per coordinate)
+template <class Tx, int M>
+__device__ __forceinline__ void load_row_m(const Tx* row, const int (&fj)[M], bool vec, Tx (&o)[M]) {
+  constexpr int B = M * (int)sizeof(Tx);
+  if constexpr (B == 16) {
+    if (vec) {
+      const uint4 r = *reinterpret_cast<const uint4*>(row + fj[0]);
+      const Tx* q = reinterpret_cast<const Tx*>(&r);
+#pragma unroll
+      for (int i = 0; i < M; ++i) o[i] = q[i];
+      return;
+    }
+  } else if constexpr (B == 8) {
+    if (vec) {
+      const uint2 r = *reinterpret_cast<const uint2*>(row + fj[0]);
+      const Tx* q = reinterpret_cast<const Tx*>(&r);
+#pragma unroll
+      for (int i = 0; i < M; ++i) o[i] = q[i];
+      return;
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < M; ++i) o[i] = row[fj[i]];
+}
+
 // SPAN2: every warp's 32*M coordinates touch at most two classes (C == 1 or
 // 32*M <= d): 4 slots per warp.  Otherwise: 2*C slots per warp (small d).
 template <class Tx, int M, bool CL, bool SPAN2>
 __global__ void __launch_bounds__(256, 1) k3_inner(InParams p) {
-  constexpr int NSLOT = SPAN2 ? 4 : 32;
+  constexpr int NSLOT = SPAN2 ? 6 : 32;  // record per warp: slots + flag (+pad)
+  constexpr int FLAG = SPAN2 ? 4 : 31;
   __shared__ uint64_t jt[2048];
+  __shared__ __align__(8) uint64_t mbar[2];
   extern __shared__ __align__(16) double xbuf_dyn[];  // [2][NGW][NSLOT]
-  __shared__ int flagbuf[2][kMaxWarpsPerCluster];
 
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, NW = blockDim.x >> 5;
   const uint32_t rank = CL ? cluster_ctarank() : 0u;
@@ -59,11 +112,19 @@ __global__ void __launch_bounds__(256, 1) k3_inner(InParams p) {
   const double delta = p.delta, alpha = p.alpha, l2 = p.l2, rcp = p.rcp;
   const bool squared = (p.loss == 0);
   const int WC = 32 * M;  // coordinates per warp
+  const bool pre = p.U != nullptr;
   auto XB = [&](int par_, int q_, int slot_) -> double& {
     return xbuf_dyn[((size_t)par_ * NGW + q_) * NSLOT + slot_];
   };
+  const uint32_t bytes_step = SPAN2 ? (uint32_t)NGW * 40u : (uint32_t)NGW * (uint32_t)(2 * C + 1) * 8u;
 
-  for (int i = tid; i < 2048; i += blockDim.x) jt[i] = p.jump_tab[i];
+  if (!pre)
+    for (int i = tid; i < 2048; i += blockDim.x) jt[i] = p.jump_tab[i];
+  if (CL && tid == 0) {
+    mbar_init(&mbar[0], 1);
+    mbar_init(&mbar[1], 1);
+    fence_mbar_init();
+  }
 
   // class of this warp's first coordinate (warp-uniform, SPAN2 split point)
   const int64_t wk0 = (int64_t)gw * WC;
@@ -85,7 +146,7 @@ __global__ void __launch_bounds__(256, 1) k3_inner(InParams p) {
     }
   }
 
-  double wt[M], gt[M], up[M], Un[M];
+  double wt[M], gt[M], up[M], Ua[M], Ub[M];
   Tx xa[M], xb[M];
   double code[M], snap[M];  // z codes as exact doubles (|code| <= 2^(bits-1))
   const bool wide = p.hi > 0x1.0p53;
@@ -102,32 +163,40 @@ __global__ void __launch_bounds__(256, 1) k3_inner(InParams p) {
     code[i] = 0.0;
     snap[i] = 0.0;
     up[i] = 0.0;
+    Ua[i] = Ub[i] = 0.0;
   }
   const int cA = cls[0];
   int cB = cA;
 #pragma unroll
   for (int i = 0; i < M; ++i)
     if (valid[i]) cB = cls[i];
-  uint64_t rs = jump_count(p.rstate0, (uint64_t)(k0 < D ? k0 : 0), p.pow_tab);
-  {  // uniforms of step 0
+  // vector row loads when the thread's coordinates are aligned and in one class
+  const bool vecx = (d % M == 0) && (ld % M == 0);
+  const int64_t T = p.T;
+  uint64_t rs = 0;
+  if (!pre) {
+    rs = jump_count(p.rstate0, (uint64_t)(k0 < D ? k0 : 0), p.pow_tab);
     uint64_t s = rs;
 #pragma unroll
     for (int i = 0; i < M; ++i) {
       s = xs_step(s);
-      Un[i] = uniform_of(s);
+      Ua[i] = uniform_of(s);
     }
+  } else {
+    const double* u0 = p.U + k0;
+#pragma unroll
+    for (int i = 0; i < M; ++i) Ua[i] = valid[i] ? u0[i] : 0.0;
+    if (T > 1)
+#pragma unroll
+      for (int i = 0; i < M; ++i) Ub[i] = valid[i] ? u0[D + i] : 0.0;
   }
 
   // rows of steps 0 and 1 in flight (raw), the index of step 2 loaded
-  const int64_t T = p.T;
   int64_t row0 = p.idx[0];
   int64_t row1 = T > 1 ? p.idx[1] : row0;
   int64_t row2 = T > 2 ? p.idx[2] : row1;
-#pragma unroll
-  for (int i = 0; i < M; ++i) {
-    xa[i] = X[row0 * ld + fj[i]];
-    xb[i] = X[row1 * ld + fj[i]];
-  }
+  load_row_m<Tx, M>(X + row0 * ld, fj, vecx, xa);
+  load_row_m<Tx, M>(X + row1 * ld, fj, vecx, xb);
   double yv = squared ? p.y[row0] : 0.0, ynext = squared ? p.y[row1] : 0.0;
   int lab = squared ? 0 : p.labels[row0], labnext = squared ? 0 : p.labels[row1];
 
@@ -138,6 +207,7 @@ __global__ void __launch_bounds__(256, 1) k3_inner(InParams p) {
   for (int64_t t = 0; t <= T; ++t) {
     const bool last = (t == T);
     const int par = (int)(t & 1);
+    if (CL && tid == 0) mbar_expect_tx(&mbar[par], bytes_step);
     double xc[M];
     double a0 = 0.0, b0 = 0.0, a1 = 0.0, b1 = 0.0;
     if (!last) {
@@ -150,10 +220,7 @@ __global__ void __launch_bounds__(256, 1) k3_inner(InParams p) {
         xc[i] = to_d<Tx>(xa[i]);
         xa[i] = xb[i];
       }
-      if (t + 2 < T) {  // raw prefetch of the row of step t+2
-#pragma unroll
-        for (int i = 0; i < M; ++i) xb[i] = X[row2 * ld + fj[i]];
-      }
+      if (t + 2 < T) load_row_m<Tx, M>(X + row2 * ld, fj, vecx, xb);  // raw prefetch, step t+2
       const int cS = SPAN2 ? cw0 : cA;
 #pragma unroll
       for (int i = 0; i < M; ++i) {
@@ -169,7 +236,7 @@ __global__ void __launch_bounds__(256, 1) k3_inner(InParams p) {
         }
       }
     }
-    const int anybad = __any_sync(0xffffffffu, bad_prev);
+    const double flagv = __any_sync(0xffffffffu, bad_prev) ? 1.0 : 0.0;
     if constexpr (SPAN2) {
       // warp reduce-scatter of (a0, b0, a1, b1): lanes 0, 8, 16, 24 end with them
       const bool u16 = (lane & 16) != 0;
@@ -180,13 +247,19 @@ __global__ void __launch_bounds__(256, 1) k3_inner(InParams p) {
       v = v + __shfl_xor_sync(0xffffffffu, v, 4);
       v = v + __shfl_xor_sync(0xffffffffu, v, 2);
       v = v + __shfl_xor_sync(0xffffffffu, v, 1);
-      if ((lane & 7) == 0) {
-        const int slot = ((lane >> 4) << 1) | ((lane >> 3) & 1);
-        if (CL) {
-          for (int r = 0; r < NC; ++r) st_cluster_f64(&XB(par, gw, slot), (uint32_t)r, v);
-        } else {
-          XB(par, gw, slot) = v;
+      if (CL) {
+        const double v0 = __shfl_sync(0xffffffffu, v, 0), v1 = __shfl_sync(0xffffffffu, v, 8);
+        const double v2 = __shfl_sync(0xffffffffu, v, 16), v3 = __shfl_sync(0xffffffffu, v, 24);
+        for (int l0 = lane; l0 < 3 * NC; l0 += 32) {
+          const int r = l0 / 3, kind = l0 - 3 * r;
+          const uint32_t rb = mapa_u32(&mbar[par], (uint32_t)r);
+          if (kind == 0) st_async_v2f64(mapa_u32(&XB(par, gw, 0), (uint32_t)r), v0, v1, rb);
+          else if (kind == 1) st_async_v2f64(mapa_u32(&XB(par, gw, 2), (uint32_t)r), v2, v3, rb);
+          else st_async_f64(mapa_u32(&XB(par, gw, FLAG), (uint32_t)r), flagv, rb);
         }
+      } else {
+        if ((lane & 7) == 0) XB(par, gw, ((lane >> 4) << 1) | ((lane >> 3) & 1)) = v;
+        if (lane == 1) XB(par, gw, FLAG) = flagv;
       }
     } else {
       // 32-slot reduce-scatter (slot 2c = class c at wz, 2c+1 at w~): lane l ends with slot l
@@ -212,33 +285,39 @@ __global__ void __launch_bounds__(256, 1) k3_inner(InParams p) {
           sl[q] = keep + __shfl_xor_sync(0xffffffffu, send, h);
         }
       }
-      if (lane < 2 * C) {
+      const bool sender = lane < 2 * C || lane == FLAG;
+      const double val = lane == FLAG ? flagv : sl[0];
+      if (sender) {
         if (CL) {
-          for (int r = 0; r < NC; ++r) st_cluster_f64(&XB(par, gw, lane), (uint32_t)r, sl[0]);
+          for (int r = 0; r < NC; ++r)
+            st_async_f64(mapa_u32(&XB(par, gw, lane), (uint32_t)r), val, mapa_u32(&mbar[par], (uint32_t)r));
         } else {
-          XB(par, gw, lane) = sl[0];
+          XB(par, gw, lane) = val;
         }
       }
     }
-    if (lane == 1) {
-      if (CL) {
-        for (int r = 0; r < NC; ++r) st_cluster_s32(&flagbuf[par][gw], (uint32_t)r, anybad);
-      } else {
-        flagbuf[par][gw] = anybad;
+    // ---- work independent of the exchange, done while it is in flight ----
+    if (!last && !pre) {
+      uint64_t s = rs;
+#pragma unroll
+      for (int i = 0; i < M; ++i) {
+        s = xs_step(s);
+        Ua[i] = uniform_of(s);
       }
     }
-    if (CL) cluster_sync_all();
+    if (CL) mbar_wait_cluster(&mbar[par], (uint32_t)((t >> 1) & 1));
     else __syncthreads();
 
     // blowup of step t-1?
     {
       int f = 0;
-      for (int q = lane; q < NGW; q += 32) f |= flagbuf[par][q];
+      for (int q = lane; q < NGW; q += 32) f |= XB(par, q, FLAG) != 0.0;
       if (__any_sync(0xffffffffu, f)) {
 #pragma unroll
         for (int i = 0; i < M; ++i)
           if (valid[i]) p.u_out[k0 + i] = up[i];
         if (rank == 0 && tid == 0) *p.blow_step = (int)(t - 1);
+        if (CL) cluster_sync_all();  // nobody leaves while remote stores may target it
         return;
       }
     }
@@ -264,7 +343,6 @@ __global__ void __launch_bounds__(256, 1) k3_inner(InParams p) {
         sb = sb + XB(par, q, 1);
       }
       // lanes >= NGW hold +0.0: butterfly levels that only add zeros are skipped
-      // (the totals then sit in lane 0 and are broadcast)
       for (int o = (NGW >= 32 ? 16 : NGW > 1 ? (1 << (31 - __clz(NGW - 1))) : 0); o >= 1; o >>= 1) {
         sa = sa + __shfl_xor_sync(0xffffffffu, sa, o);
         sb = sb + __shfl_xor_sync(0xffffffffu, sb, o);
@@ -278,8 +356,17 @@ __global__ void __launch_bounds__(256, 1) k3_inner(InParams p) {
     } else {
       double lg = 0.0;
       if (hc < C) {
-        lg = XB(par, q_first, slot_first);
-        for (int q = q_first + 1; q <= q_last; ++q) lg = lg + XB(par, q, slot_rest);
+        // loads first, then the in-order chain
+        constexpr int QH = 16;
+        double pv[QH];
+#pragma unroll
+        for (int j = 0; j < QH; ++j)
+          pv[j] = (q_first + j <= q_last) ? XB(par, q_first + j, j == 0 ? slot_first : slot_rest) : 0.0;
+        lg = pv[0];
+#pragma unroll
+        for (int j = 1; j < QH; ++j)
+          if (q_first + j <= q_last) lg = lg + pv[j];
+        for (int q = q_first + QH; q <= q_last; ++q) lg = lg + XB(par, q, slot_rest);
       }
       const bool act = hc < C;
       double mx = act ? lg : -INFINITY;
@@ -293,8 +380,13 @@ __global__ void __launch_bounds__(256, 1) k3_inner(InParams p) {
       if (hc == li) pr = pr - 1.0;
       p1A = __shfl_sync(0xffffffffu, pr, cA);
       p2A = __shfl_sync(0xffffffffu, pr, 16 + cA);
-      p1B = __shfl_sync(0xffffffffu, pr, cB);
-      p2B = __shfl_sync(0xffffffffu, pr, 16 + cB);
+      if (__all_sync(0xffffffffu, cB == cA)) {
+        p1B = p1A;
+        p2B = p2A;
+      } else {
+        p1B = __shfl_sync(0xffffffffu, pr, cB);
+        p2B = __shfl_sync(0xffffffffu, pr, 16 + cB);
+      }
     }
 
     // ---- element-wise update + stochastic rounding (branch-free) ----
@@ -303,33 +395,35 @@ __global__ void __launch_bounds__(256, 1) k3_inner(InParams p) {
 #pragma unroll
     for (int i = 0; i < M; ++i) {
       const bool inA = cls[i] == cA;
-      const double p1 = inA ? p1A : p1B, p2 = inA ? p2A : p2B;
+      const double pp1 = inA ? p1A : p1B, pp2 = inA ? p2A : p2B;
       const double z = __dmul_rn(code[i], delta);
       const double wz = wt[i] + z;
-      const double g1 = __dmul_rn(p1, xc[i]) + __dmul_rn(l2, wz);
-      const double g2 = __dmul_rn(p2, xc[i]) + __dmul_rn(l2, wt[i]);
+      const double g1 = __dmul_rn(pp1, xc[i]) + __dmul_rn(l2, wz);
+      const double g2 = __dmul_rn(pp2, xc[i]) + __dmul_rn(l2, wt[i]);
       const double u = z - __dmul_rn(alpha, (g1 - g2) + gt[i]);
       up[i] = u;
       bad |= valid[i] && !isfinite(u);
-      code[i] = quantize_fast(u, delta, rcp, p.hi, p.lo, Un[i], slow[i]);
+      code[i] = quantize_fast(u, delta, rcp, p.hi, p.lo, Ua[i], slow[i]);
       slow_any |= valid[i] && slow[i];
     }
     if (slow_any || wide || rcp == 0.0) {  // IEEE-division path for the rare operands
 #pragma unroll
       for (int i = 0; i < M; ++i)
         if (valid[i] && (slow[i] || wide || rcp == 0.0))
-          code[i] = (double)quantize_code(up[i], delta, p.hi, p.lo, p.maxc, p.minc, Un[i]);
-    }
-    rs = jump_tab(rs, jt);
-    {  // uniforms of the next step, off the critical path
-      uint64_t s = rs;
-#pragma unroll
-      for (int i = 0; i < M; ++i) {
-        s = xs_step(s);
-        Un[i] = uniform_of(s);
-      }
+          code[i] = (double)quantize_code(up[i], delta, p.hi, p.lo, p.maxc, p.minc, Ua[i]);
     }
     bad_prev = bad ? 1 : 0;
+    if (pre) {
+#pragma unroll
+      for (int i = 0; i < M; ++i) Ua[i] = Ub[i];
+      if (t + 2 < T) {
+        const double* un = p.U + (t + 2) * D + k0;
+#pragma unroll
+        for (int i = 0; i < M; ++i) Ub[i] = valid[i] ? un[i] : 0.0;
+      }
+    } else {
+      rs = jump_tab(rs, jt);
+    }
     if (t < p.trace_steps) {
 #pragma unroll
       for (int i = 0; i < M; ++i)
@@ -343,12 +437,13 @@ __global__ void __launch_bounds__(256, 1) k3_inner(InParams p) {
     p.w_out[k0 + i] = wt[i] + __dmul_rn(zc, delta);
     p.codes_out[k0 + i] = __double2ll_rn(code[i]);
   }
+  if (CL) cluster_sync_all();  // keep every CTA's shared memory alive until all remote stores landed
 }
 
 template <class Tx, int M, bool SPAN2>
 static cudaError_t launch_in_t(const InLaunch& L, const InParams& p, cudaStream_t st) {
   if (L.ctas * L.threads / 32 > kMaxWarpsPerCluster) return cudaErrorInvalidConfiguration;
-  const size_t smem = sizeof(double) * 2 * (size_t)(L.ctas * L.threads / 32) * (SPAN2 ? 4 : 32);
+  const size_t smem = sizeof(double) * 2 * (size_t)(L.ctas * L.threads / 32) * (SPAN2 ? 6 : 32);
   if (L.ctas == 1) {
     auto kern = k3_inner<Tx, M, false, SPAN2>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
