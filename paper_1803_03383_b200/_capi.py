@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libhalp_b200.so")
+LIB_PATH = os.environ.get("HALP_LIB") or os.path.join(HERE, "libhalp_b200.so")  # HALP_LIB: A/B a variant build
 
 HALP_OK, HALP_INVALID_INPUT, HALP_DIVERGED, HALP_CUDA_ERROR, HALP_NCCL_ERROR, HALP_CAPACITY, HALP_UNSUPPORTED = range(7)
 F64, F32, BF16 = 0, 1, 2

@@ -31,6 +31,8 @@ HEADERS = ["halp_device.cuh", "kernels.h", "rng_jump.hpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-fmad=false", "-std=c++17", "-Xcompiler", "-fPIC",
                      "-Xptxas", "-v", "-I", os.path.join(ROOT, "include")]
+# developer variants only (tools/build_alt.sh), e.g. HALP_NVCC_DEFS="-DHALP_K3_PROF"
+NVCC_FLAGS += os.environ.get("HALP_NVCC_DEFS", "").split()
 CXX_FLAGS = ["-O2", "-std=c++17", "-fPIC", "-Wall", "-Wextra", "-I", os.path.join(CUDA, "include"),
              "-I", os.path.join(ROOT, "include")]
 

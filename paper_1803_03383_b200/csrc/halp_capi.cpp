@@ -145,8 +145,7 @@ struct halp_problem {
   int fg_passes = 1;
   // workspace
   double *w = nullptr, *w2 = nullptr, *g = nullptr, *partials = nullptr, *rank_sum = nullptr, *gathered = nullptr,
-         *stats = nullptr, *u_out = nullptr, *tree_scratch = nullptr, *Ubuf = nullptr;
-  int64_t Ucap = 0;
+         *stats = nullptr, *u_out = nullptr, *tree_scratch = nullptr;
   int64_t* idx = nullptr;
   int64_t idx_cap = 0;
   long long* codes = nullptr;
@@ -164,7 +163,7 @@ struct halp_problem {
     cudaSetDevice(device);
     for (void* ptr : {(void*)w, (void*)w2, (void*)g, (void*)partials, (void*)rank_sum, (void*)gathered, (void*)stats,
                       (void*)u_out, (void*)idx, (void*)codes, (void*)blow, (void*)pow_tab, (void*)jump_tab,
-                      (void*)trace_dev, (void*)y, (void*)labels, (void*)tree_scratch, (void*)Ubuf})
+                      (void*)trace_dev, (void*)y, (void*)labels, (void*)tree_scratch})
       if (ptr) cudaFree(ptr);
     if (own_X && X) cudaFree(X);
     if (comm) Nccl::get().commDestroy(comm);
@@ -228,11 +227,26 @@ int plan_for(int64_t n, int d, int C, int dtype, KernelPlan* kp) {
   }
   // inner loop: M coordinates per thread, up to 16 CTAs per cluster
   const int64_t D = (int64_t)d * C;
-  int M = (int)env_int("HALP_IN_M", 4);
-  while (M > 1 && M > d) M /= 2;
-  int64_t threads = (D + M - 1) / M;
+  // Measured on B200 (tools/sweep_inner.py): one CTA (__syncthreads exchange)
+  // wins while <= 128 threads cover D; beyond, 128-thread CTAs up to a 16-CTA
+  // cluster with the fewest coordinates per thread; 256-thread CTAs last.
+  int M = (int)env_int("HALP_IN_M", 0);
   int NC = (int)env_int("HALP_IN_NC", 0);
-  if (NC <= 0) NC = (int)((threads + 255) / 256);
+  int64_t threads = 0;
+  if (M <= 0) {
+    if (D <= 512) {
+      M = 1;
+      while (M < 4 && (D + M - 1) / M > 128) M *= 2;
+      if (NC <= 0) NC = 1;
+    } else {
+      M = 2;
+      while (M < 8 && (D + M - 1) / M > 16 * 128) M *= 2;
+    }
+  }
+  while (M > 1 && M > d) M /= 2;
+  threads = (D + M - 1) / M;
+  if (NC <= 0) NC = (int)((threads + 127) / 128);
+  if (NC > 16) NC = (int)((threads + 255) / 256);
   while (NC > 16 && M < 8) {
     M *= 2;
     threads = (D + M - 1) / M;
@@ -676,28 +690,11 @@ int halp_run(halp_problem* p, const halp_config* cfg, halp_record* rec) {
     // rounding stream: epoch k starts after k*D*(T+1) draws; Q(0) takes D of them
     const uint64_t r0 = jt.jump(s_round, (uint64_t)k * (uint64_t)D * (uint64_t)(T + 1) + (uint64_t)D);
     CU(cudaMemsetAsync(p->blow, 0xFF, sizeof(int), p->stream));
-    // K4b: this epoch's rounding uniforms, precomputed in parallel when they fit
-    double* Uptr = nullptr;
-    const int64_t nU = T * D;
-    if (nU * 8 <= env_int("HALP_PRE_U_MAX_MB", 32768) * (int64_t)(1 << 20)) {
-      if (p->Ucap < nU) {
-        if (p->Ubuf) cudaFree(p->Ubuf);
-        p->Ubuf = nullptr;
-        p->Ucap = 0;
-        if (cudaMalloc(&p->Ubuf, sizeof(double) * nU) == cudaSuccess) p->Ucap = nU;
-        else cudaGetLastError();
-      }
-      if (p->Ucap >= nU) {
-        CU(launch_uniforms(r0, nU, p->pow_tab, p->Ubuf, p->stream));
-        ++p->timing.kernel_launches;
-        Uptr = p->Ubuf;
-      }
-    }
     const double rcp = 1.0 / delta;
     InParams ip{p->X, p->ld, p->d, p->C, (int)D, p->loss, n, p->y, p->labels, p->l2, cfg->alpha, delta, hi, lo, maxc,
                 minc, std::isfinite(rcp) && rcp != 0.0 && env_int("HALP_IEEE_DIV", 0) == 0 ? rcp : 0.0, p->w, p->w2,
                 p->g, p->idx, T, t_pick, r0, p->pow_tab, p->jump_tab, p->codes, tr_steps > 0 ? p->trace_dev : nullptr,
-                tr_steps, p->blow, p->u_out, Uptr};
+                tr_steps, p->blow, p->u_out};
     CU(cudaEventRecord(p->ev_in.a, p->stream));
     CU(launch_inner(p->in, ip, p->stream));
     ++p->timing.kernel_launches;

@@ -669,21 +669,6 @@ __global__ void k_samples(uint64_t state0, int64_t total, int opt2, uint64_t T, 
   }
 }
 
-// K4b: the rounding-stream uniforms of one epoch's inner loop, U[t*D + k] =
-// uniform of draw D*(t+1) + k of the epoch (rng.hpp:42-44), generated by
-// contiguous segments (one jump per thread, then sequential xorshift steps).
-__global__ void k_uniforms(uint64_t state0, int64_t total, const uint64_t* __restrict__ pow_tab, int64_t per_thread,
-                           double* __restrict__ U) {
-  const int64_t first = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * per_thread;
-  if (first >= total) return;
-  uint64_t s = jump_count(state0, (uint64_t)first, pow_tab);
-  const int64_t last = first + per_thread < total ? first + per_thread : total;
-  for (int64_t j = first; j < last; ++j) {
-    s = xs_step(s);
-    U[j] = uniform_of(s);
-  }
-}
-
 // ---------------------------------------------------------------- dispatch
 size_t fast_smem_bytes(int ld, int elem, int threads, int R, int CC, int stages) {
   size_t b = (size_t)stages * R * ld * elem;
@@ -868,15 +853,6 @@ cudaError_t launch_split_tree(const double* partials, int nsplit, int D1, double
 
 cudaError_t launch_finalize(const FinParams& p, cudaStream_t st) {
   k_finalize<<<1, 256, 0, st>>>(p);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_uniforms(uint64_t state0, int64_t total, const uint64_t* pow_tab, double* U, cudaStream_t st) {
-  const int64_t threads = 148 * 1024;
-  int64_t per = (total + threads - 1) / threads;
-  if (per < 64) per = 64;
-  const int64_t nthr = (total + per - 1) / per;
-  k_uniforms<<<(int)((nthr + 255) / 256), 256, 0, st>>>(state0, total, pow_tab, per, U);
   return cudaGetLastError();
 }
 

@@ -11,14 +11,14 @@
 // Layout: the D = d*C flat coordinates (column-major d x C, objectives.hpp:56-58)
 // are split over the cluster: thread tau = rank*T3 + tid owns the M
 // contiguous coordinates [tau*M, tau*M + M).  w~, g~ and the codes of z live
-// in registers for the whole epoch; the sampled row x_i (and, when
-// precomputed, the step's rounding uniforms) are prefetched two steps ahead.
+// in registers for the whole epoch; the sampled row x_i is prefetched two
+// steps ahead.
 //
 // Rounding stream: the reference's xorshift64* stream 1, reproduced exactly.
-// Coordinate k of step t uses draw  D*(t+1) + k  of the epoch.  Either the
-// epoch's uniforms are precomputed by k_uniforms (K4b, fully parallel) and
-// streamed from HBM, or each thread steps its M draws and jumps D draws per
-// step with the GF(2) table of X^D held in shared memory.
+// Coordinate k of step t uses draw  D*(t+1) + k  of the epoch: each thread
+// steps its M draws and jumps D draws per step with the GF(2) table of X^D
+// held in shared memory -- inside the exchange wait, where it costs nothing
+// (streaming precomputed uniforms from HBM measured ~0.4 us/step slower).
 //
 // Per step, ONE exchange: each warp reduces its partial logits with an
 // xor-butterfly reduce-scatter and sends them (with its non-finite flag of the
@@ -33,6 +33,8 @@
 // warps, squared loss (C == 1): lane l sums warps l, l+32, ... sequentially,
 // then a lane butterfly; softmax (C >= 2): sequential over the warps holding
 // the class, in global warp order.
+#include <cstdio>
+
 #include "halp_device.cuh"
 #include "kernels.h"
 
@@ -40,14 +42,33 @@ namespace halp {
 
 constexpr int kMaxWarpsPerCluster = 128;
 
+// developer build only (-DHALP_K3_PROF): per-phase clock64 split of one warp
+#ifdef HALP_K3_PROF
+#define K3_MARK(i)                         \
+  do {                                     \
+    if (prof_on) {                         \
+      const long long c_ = clock64();      \
+      prof_acc[i] += c_ - prof_last;       \
+      prof_last = c_;                      \
+    }                                      \
+  } while (0)
+#else
+#define K3_MARK(i) \
+  do {             \
+  } while (0)
+#endif
+
 __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "W_%=:\n\t"
-      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
+      "mbarrier.try_wait.parity.relaxed.cluster.shared::cta.b64 p, [%0], %1;\n\t"
       "@!p bra W_%=;\n\t}" ::"r"(smem_u32(bar)),
       "r"(parity)
       : "memory");
+  // the payload arrived by st.async into OUR shared memory: an acquire restricted
+  // to shared::cluster suffices (a plain .acquire.cluster wait also invalidates L1)
+  asm volatile("fence.acquire.sync_restrict::shared::cluster.cluster;" ::: "memory");
 }
 __device__ __forceinline__ uint32_t mapa_u32(const void* p, uint32_t rank) {
   uint32_t ra;
@@ -91,12 +112,37 @@ __device__ __forceinline__ void load_row_m(const Tx* row, const int (&fj)[M], bo
   for (int i = 0; i < M; ++i) o[i] = row[fj[i]];
 }
 
-// SPAN2: every warp's 32*M coordinates touch at most two classes (C == 1 or
-// 32*M <= d): 4 slots per warp.  Otherwise: 2*C slots per warp (small d).
-template <class Tx, int M, bool CL, bool SPAN2>
+
+// store M doubles (vectorised when all are valid; M*8-byte aligned by layout)
+template <int M>
+__device__ __forceinline__ void store_m(double* dst, const double (&v)[M], const bool (&valid)[M], bool allv) {
+  if constexpr (M >= 2) {
+    if (allv) {
+#pragma unroll
+      for (int i = 0; i < M; i += 2) *reinterpret_cast<double2*>(dst + i) = make_double2(v[i], v[i + 1]);
+      return;
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < M; ++i)
+    if (valid[i]) dst[i] = v[i];
+}
+
+// KIND 0: squared loss (C == 1), one (wz, w~) pair per warp.
+// KIND 1: softmax, every warp's 32*M coordinates touch at most two classes
+//         (32*M <= d): two pairs per warp.
+// KIND 2: softmax with small d: 2*C slots per warp.
+template <int KIND>
+struct K3Layout {
+  static constexpr int NSLOT = KIND == 0 ? 4 : KIND == 1 ? 6 : 32;  // doubles per warp record
+  static constexpr int FLAG = KIND == 0 ? 2 : KIND == 1 ? 4 : 31;   // slot of the non-finite flag
+};
+
+template <class Tx, int M, bool CL, int KIND>
 __global__ void __launch_bounds__(256, 1) k3_inner(InParams p) {
-  constexpr int NSLOT = SPAN2 ? 6 : 32;  // record per warp: slots + flag (+pad)
-  constexpr int FLAG = SPAN2 ? 4 : 31;
+  constexpr int NSLOT = K3Layout<KIND>::NSLOT;
+  constexpr int FLAG = K3Layout<KIND>::FLAG;
+  constexpr bool SQ = KIND == 0;
   __shared__ uint64_t jt[2048];
   __shared__ __align__(8) uint64_t mbar[2];
   extern __shared__ __align__(16) double xbuf_dyn[];  // [2][NGW][NSLOT]
@@ -110,52 +156,84 @@ __global__ void __launch_bounds__(256, 1) k3_inner(InParams p) {
   const int64_t k0 = ((int64_t)rank * blockDim.x + tid) * M;
   const Tx* X = reinterpret_cast<const Tx*>(p.X);
   const double delta = p.delta, alpha = p.alpha, l2 = p.l2, rcp = p.rcp;
-  const bool squared = (p.loss == 0);
   const int WC = 32 * M;  // coordinates per warp
-  const bool pre = p.U != nullptr;
-  auto XB = [&](int par_, int q_, int slot_) -> double& {
-    return xbuf_dyn[((size_t)par_ * NGW + q_) * NSLOT + slot_];
-  };
-  const uint32_t bytes_step = SPAN2 ? (uint32_t)NGW * 40u : (uint32_t)NGW * (uint32_t)(2 * C + 1) * 8u;
+  const int PAR_STRIDE = NGW * NSLOT;  // doubles between the two parity buffers
+  auto XB = [&](int par_, int q_, int slot_) -> double& { return xbuf_dyn[par_ * PAR_STRIDE + q_ * NSLOT + slot_]; };
+  const uint32_t bytes_step = KIND == 0 ? (uint32_t)NGW * 24u
+                              : KIND == 1 ? (uint32_t)NGW * 40u
+                                          : (uint32_t)NGW * (uint32_t)(2 * C + 1) * 8u;
 
-  if (!pre)
-    for (int i = tid; i < 2048; i += blockDim.x) jt[i] = p.jump_tab[i];
+  for (int i = tid; i < 2048; i += blockDim.x) jt[i] = p.jump_tab[i];
   if (CL && tid == 0) {
     mbar_init(&mbar[0], 1);
     mbar_init(&mbar[1], 1);
     fence_mbar_init();
   }
 
-  // class of this warp's first coordinate (warp-uniform, SPAN2 split point)
+  // Remote targets of this lane's st.async messages, fixed for the epoch
+  // (parity 1 = parity 0 + a constant offset in every CTA's window).
+  //   KIND 0: lanes 0..15 send the pair to CTA lane, lanes 16..31 the flag to
+  //           CTA lane-16.
+  //   KIND 1: lanes with (lane & 8) == 0 send pair 2*(lane>>4) and lanes 8..15
+  //           the flag, each to CTAs (lane & 7) and (lane & 7) + 8.
+  uint32_t ra0 = 0, ra1 = 0, rb0 = 0, rb1 = 0;
+  bool s0ok = false, s1ok = false;
+  const uint32_t xb_par_off = (uint32_t)(PAR_STRIDE * 8), mb_par_off = 8u;
+  if (CL && KIND == 0) {
+    const int slot = lane < 16 ? 0 : FLAG;
+    const int r0 = lane & 15;
+    s0ok = r0 < NC;
+    ra0 = mapa_u32(&XB(0, gw, slot), (uint32_t)(s0ok ? r0 : 0));
+    rb0 = mapa_u32(&mbar[0], (uint32_t)(s0ok ? r0 : 0));
+  } else if (CL && KIND == 1) {
+    const int slot = (lane & 8) ? FLAG : 2 * (lane >> 4);
+    const bool sender = !(lane & 8) || !(lane & 16);
+    const int r0 = lane & 7, r1 = (lane & 7) + 8;
+    s0ok = sender && r0 < NC;
+    s1ok = sender && r1 < NC;
+    ra0 = mapa_u32(&XB(0, gw, slot), (uint32_t)(s0ok ? r0 : 0));
+    ra1 = mapa_u32(&XB(0, gw, slot), (uint32_t)(s1ok ? r1 : 0));
+    rb0 = mapa_u32(&mbar[0], (uint32_t)(s0ok ? r0 : 0));
+    rb1 = mapa_u32(&mbar[0], (uint32_t)(s1ok ? r1 : 0));
+  }
+
+  // class of this warp's first coordinate (warp-uniform, KIND 1 split point)
   const int64_t wk0 = (int64_t)gw * WC;
   const int cw0 = (int)(wk0 < D ? wk0 / d : 0);
 
   // per-lane plan of the cross-warp logit sum (softmax): lane hc (+16 for w~)
+  // reads the records of warps q_first..q_last, as offsets from its parity base
   const int hc = lane & 15;
   const int isw = (lane >> 4) & 1;
-  int q_first = 0, q_last = -1, slot_first = 0, slot_rest = 0;
-  if (!squared && hc < C) {
-    q_first = (int)(((int64_t)hc * d) / WC);
-    q_last = (int)((((int64_t)hc + 1) * d - 1) / WC);
-    if (SPAN2) {
+  int nq = 0, off_first = 0, off_rest = 0;
+  if (!SQ && hc < C) {
+    const int q_first = (int)(((int64_t)hc * d) / WC);
+    const int q_last = (int)((((int64_t)hc + 1) * d - 1) / WC);
+    int slot_first, slot_rest;
+    if (KIND == 1) {
       const int c_of_first = (int)(((int64_t)q_first * WC) / d);
       slot_first = (c_of_first == hc ? 0 : 2) + isw;
       slot_rest = isw;
     } else {
       slot_first = slot_rest = 2 * hc + isw;
     }
+    nq = q_last - q_first + 1;
+    off_first = q_first * NSLOT + slot_first;
+    off_rest = q_first * NSLOT + slot_rest;
   }
 
-  double wt[M], gt[M], up[M], Ua[M], Ub[M];
+  double wt[M], gt[M], up[M], Ua[M];
   Tx xa[M], xb[M];
   double code[M], snap[M];  // z codes as exact doubles (|code| <= 2^(bits-1))
   const bool wide = p.hi > 0x1.0p53;
   int cls[M], fj[M];
   bool valid[M];
+  bool allv = true;
 #pragma unroll
   for (int i = 0; i < M; ++i) {
     const int64_t k = k0 + i;
     valid[i] = k < D;
+    allv = allv && valid[i];
     cls[i] = valid[i] ? (int)(k / d) : 0;
     fj[i] = valid[i] ? (int)(k % d) : 0;
     wt[i] = valid[i] ? p.w[k] : 0.0;
@@ -163,33 +241,18 @@ __global__ void __launch_bounds__(256, 1) k3_inner(InParams p) {
     code[i] = 0.0;
     snap[i] = 0.0;
     up[i] = 0.0;
-    Ua[i] = Ub[i] = 0.0;
+    Ua[i] = 0.0;
   }
   const int cA = cls[0];
   int cB = cA;
 #pragma unroll
   for (int i = 0; i < M; ++i)
     if (valid[i]) cB = cls[i];
+  const bool oneclass = __all_sync(0xffffffffu, cB == cA);
   // vector row loads when the thread's coordinates are aligned and in one class
   const bool vecx = (d % M == 0) && (ld % M == 0);
   const int64_t T = p.T;
-  uint64_t rs = 0;
-  if (!pre) {
-    rs = jump_count(p.rstate0, (uint64_t)(k0 < D ? k0 : 0), p.pow_tab);
-    uint64_t s = rs;
-#pragma unroll
-    for (int i = 0; i < M; ++i) {
-      s = xs_step(s);
-      Ua[i] = uniform_of(s);
-    }
-  } else {
-    const double* u0 = p.U + k0;
-#pragma unroll
-    for (int i = 0; i < M; ++i) Ua[i] = valid[i] ? u0[i] : 0.0;
-    if (T > 1)
-#pragma unroll
-      for (int i = 0; i < M; ++i) Ub[i] = valid[i] ? u0[D + i] : 0.0;
-  }
+  uint64_t rs = jump_count(p.rstate0, (uint64_t)(k0 < D ? k0 : 0), p.pow_tab);
 
   // rows of steps 0 and 1 in flight (raw), the index of step 2 loaded
   int64_t row0 = p.idx[0];
@@ -197,14 +260,19 @@ __global__ void __launch_bounds__(256, 1) k3_inner(InParams p) {
   int64_t row2 = T > 2 ? p.idx[2] : row1;
   load_row_m<Tx, M>(X + row0 * ld, fj, vecx, xa);
   load_row_m<Tx, M>(X + row1 * ld, fj, vecx, xb);
-  double yv = squared ? p.y[row0] : 0.0, ynext = squared ? p.y[row1] : 0.0;
-  int lab = squared ? 0 : p.labels[row0], labnext = squared ? 0 : p.labels[row1];
+  double yv = SQ ? p.y[row0] : 0.0, ynext = SQ ? p.y[row1] : 0.0;
+  int lab = SQ ? 0 : p.labels[row0], labnext = SQ ? 0 : p.labels[row1];
 
   __syncthreads();
   if (CL) cluster_sync_all();
 
   int bad_prev = 0;
+#ifdef HALP_K3_PROF
+  const bool prof_on = rank == 0 && tid == 0;
+  long long prof_acc[16] = {}, prof_last = clock64();
+#endif
   for (int64_t t = 0; t <= T; ++t) {
+    K3_MARK(7);
     const bool last = (t == T);
     const int par = (int)(t & 1);
     if (CL && tid == 0) mbar_expect_tx(&mbar[par], bytes_step);
@@ -221,13 +289,13 @@ __global__ void __launch_bounds__(256, 1) k3_inner(InParams p) {
         xa[i] = xb[i];
       }
       if (t + 2 < T) load_row_m<Tx, M>(X + row2 * ld, fj, vecx, xb);  // raw prefetch, step t+2
-      const int cS = SPAN2 ? cw0 : cA;
+      const int cS = KIND == 1 ? cw0 : cA;
 #pragma unroll
       for (int i = 0; i < M; ++i) {
         if (!valid[i]) continue;
         const double z = __dmul_rn(code[i], delta);
         const double wz = wt[i] + z;
-        if (cls[i] == cS) {
+        if (SQ || cls[i] == cS) {
           a0 = fma(xc[i], wz, a0);
           b0 = fma(xc[i], wt[i], b0);
         } else {
@@ -236,9 +304,29 @@ __global__ void __launch_bounds__(256, 1) k3_inner(InParams p) {
         }
       }
     }
+    K3_MARK(0);
     const double flagv = __any_sync(0xffffffffu, bad_prev) ? 1.0 : 0.0;
-    if constexpr (SPAN2) {
-      // warp reduce-scatter of (a0, b0, a1, b1): lanes 0, 8, 16, 24 end with them
+    if constexpr (KIND == 0) {
+      // all-reduce butterfly of a0 on lanes 0..15 and of b0 on lanes 16..31
+      const bool u16 = (lane & 16) != 0;
+      double v = (u16 ? b0 : a0) + __shfl_xor_sync(0xffffffffu, u16 ? a0 : b0, 16);
+      v = v + __shfl_xor_sync(0xffffffffu, v, 8);
+      v = v + __shfl_xor_sync(0xffffffffu, v, 4);
+      v = v + __shfl_xor_sync(0xffffffffu, v, 2);
+      v = v + __shfl_xor_sync(0xffffffffu, v, 1);
+      const double vp = __shfl_xor_sync(0xffffffffu, v, 16);
+      if (CL) {
+        const uint32_t xo = par ? xb_par_off : 0u, mo = par ? mb_par_off : 0u;
+        if (s0ok) {
+          if (!u16) st_async_v2f64(ra0 + xo, v, vp, rb0 + mo);
+          else st_async_f64(ra0 + xo, flagv, rb0 + mo);
+        }
+      } else {
+        if (lane == 0) *reinterpret_cast<double2*>(&XB(par, gw, 0)) = make_double2(v, vp);
+        if (lane == 16) XB(par, gw, FLAG) = flagv;
+      }
+    } else if constexpr (KIND == 1) {
+      // warp reduce-scatter of (a0, b0, a1, b1): 8-lane group g ends with slot g
       const bool u16 = (lane & 16) != 0;
       const double s0 = (u16 ? a1 : a0) + __shfl_xor_sync(0xffffffffu, u16 ? a0 : a1, 16);
       const double s1 = (u16 ? b1 : b0) + __shfl_xor_sync(0xffffffffu, u16 ? b0 : b1, 16);
@@ -247,19 +335,19 @@ __global__ void __launch_bounds__(256, 1) k3_inner(InParams p) {
       v = v + __shfl_xor_sync(0xffffffffu, v, 4);
       v = v + __shfl_xor_sync(0xffffffffu, v, 2);
       v = v + __shfl_xor_sync(0xffffffffu, v, 1);
+      const double vp = __shfl_xor_sync(0xffffffffu, v, 8);  // pair g with g^1
       if (CL) {
-        const double v0 = __shfl_sync(0xffffffffu, v, 0), v1 = __shfl_sync(0xffffffffu, v, 8);
-        const double v2 = __shfl_sync(0xffffffffu, v, 16), v3 = __shfl_sync(0xffffffffu, v, 24);
-        for (int l0 = lane; l0 < 3 * NC; l0 += 32) {
-          const int r = l0 / 3, kind = l0 - 3 * r;
-          const uint32_t rb = mapa_u32(&mbar[par], (uint32_t)r);
-          if (kind == 0) st_async_v2f64(mapa_u32(&XB(par, gw, 0), (uint32_t)r), v0, v1, rb);
-          else if (kind == 1) st_async_v2f64(mapa_u32(&XB(par, gw, 2), (uint32_t)r), v2, v3, rb);
-          else st_async_f64(mapa_u32(&XB(par, gw, FLAG), (uint32_t)r), flagv, rb);
+        const uint32_t xo = par ? xb_par_off : 0u, mo = par ? mb_par_off : 0u;
+        if (!u8) {
+          if (s0ok) st_async_v2f64(ra0 + xo, v, vp, rb0 + mo);
+          if (s1ok) st_async_v2f64(ra1 + xo, v, vp, rb1 + mo);
+        } else {
+          if (s0ok) st_async_f64(ra0 + xo, flagv, rb0 + mo);
+          if (s1ok) st_async_f64(ra1 + xo, flagv, rb1 + mo);
         }
       } else {
-        if ((lane & 7) == 0) XB(par, gw, ((lane >> 4) << 1) | ((lane >> 3) & 1)) = v;
-        if (lane == 1) XB(par, gw, FLAG) = flagv;
+        if ((lane & 15) == 0) *reinterpret_cast<double2*>(&XB(par, gw, (lane >> 4) << 1)) = make_double2(v, vp);
+        if (lane == 8) XB(par, gw, FLAG) = flagv;
       }
     } else {
       // 32-slot reduce-scatter (slot 2c = class c at wz, 2c+1 at w~): lane l ends with slot l
@@ -296,32 +384,40 @@ __global__ void __launch_bounds__(256, 1) k3_inner(InParams p) {
         }
       }
     }
+    K3_MARK(1);
     // ---- work independent of the exchange, done while it is in flight ----
-    if (!last && !pre) {
+    if (!last) {
       uint64_t s = rs;
 #pragma unroll
       for (int i = 0; i < M; ++i) {
         s = xs_step(s);
         Ua[i] = uniform_of(s);
       }
+      rs = jump_tab(rs, jt);
     }
+    K3_MARK(2);
     if (CL) mbar_wait_cluster(&mbar[par], (uint32_t)((t >> 1) & 1));
     else __syncthreads();
+    K3_MARK(3);
 
-    // blowup of step t-1?
-    {
-      int f = 0;
-      for (int q = lane; q < NGW; q += 32) f |= XB(par, q, FLAG) != 0.0;
-      if (__any_sync(0xffffffffu, f)) {
+    const double* xbp = xbuf_dyn + par * PAR_STRIDE;
+    // blowup of step t-1?  (flags loaded now, tested after this step's update:
+    // a blowup leaves code[] dead, and u of step t-1 is already in u_out)
+    int fl = 0;
 #pragma unroll
-        for (int i = 0; i < M; ++i)
-          if (valid[i]) p.u_out[k0 + i] = up[i];
+    for (int j = 0; j < kMaxWarpsPerCluster / 32; ++j) {
+      const int q = lane + 32 * j;
+      if (q < NGW) fl |= xbp[q * NSLOT + FLAG] != 0.0;
+    }
+    if (last) {
+      if (__any_sync(0xffffffffu, fl)) {
         if (rank == 0 && tid == 0) *p.blow_step = (int)(t - 1);
         if (CL) cluster_sync_all();  // nobody leaves while remote stores may target it
         return;
       }
+      break;
     }
-    if (last) break;
+    K3_MARK(4);
     const double yi = yv;
     const int li = lab;
     row0 = row1;
@@ -330,18 +426,24 @@ __global__ void __launch_bounds__(256, 1) k3_inner(InParams p) {
     lab = labnext;
     if (t + 3 < T) row2 = p.idx[t + 3];
     if (t + 2 < T) {
-      if (squared) ynext = p.y[row1];
+      if (SQ) ynext = p.y[row1];
       else labnext = p.labels[row1];
     }
 
     // loss derivative at wz (p1) and at w~ (p2) for this thread's classes
     double p1A, p2A, p1B, p2B;
-    if (squared) {
+    if constexpr (SQ) {
       double sa = 0.0, sb = 0.0;
-      for (int q = lane; q < NGW; q += 32) {
-        sa = sa + XB(par, q, 0);
-        sb = sb + XB(par, q, 1);
+#pragma unroll
+      for (int j = 0; j < kMaxWarpsPerCluster / 32; ++j) {
+        const int q = lane + 32 * j;
+        if (q < NGW) {
+          const double2 v = *reinterpret_cast<const double2*>(xbp + q * NSLOT);
+          sa = sa + v.x;
+          sb = sb + v.y;
+        }
       }
+      K3_MARK(8);
       // lanes >= NGW hold +0.0: butterfly levels that only add zeros are skipped
       for (int o = (NGW >= 32 ? 16 : NGW > 1 ? (1 << (31 - __clz(NGW - 1))) : 0); o >= 1; o >>= 1) {
         sa = sa + __shfl_xor_sync(0xffffffffu, sa, o);
@@ -354,33 +456,40 @@ __global__ void __launch_bounds__(256, 1) k3_inner(InParams p) {
       p1A = p1B = sa - yi;
       p2A = p2B = sb - yi;
     } else {
-      double lg = 0.0;
-      if (hc < C) {
-        // loads first, then the in-order chain
-        constexpr int QH = 16;
-        double pv[QH];
+      // loads first, then the in-order chain
+      constexpr int QH = 8;
+      double pv[QH];
+      pv[0] = nq > 0 ? xbp[off_first] : 0.0;
 #pragma unroll
-        for (int j = 0; j < QH; ++j)
-          pv[j] = (q_first + j <= q_last) ? XB(par, q_first + j, j == 0 ? slot_first : slot_rest) : 0.0;
-        lg = pv[0];
+      for (int j = 1; j < QH; ++j) pv[j] = j < nq ? xbp[off_rest + j * NSLOT] : 0.0;
+      double lg = pv[0];
 #pragma unroll
-        for (int j = 1; j < QH; ++j)
-          if (q_first + j <= q_last) lg = lg + pv[j];
-        for (int q = q_first + QH; q <= q_last; ++q) lg = lg + XB(par, q, slot_rest);
-      }
+      for (int j = 1; j < QH; ++j)
+        if (j < nq) lg = lg + pv[j];
+      for (int j = QH; j < nq; ++j) lg = lg + xbp[off_rest + j * NSLOT];
+      K3_MARK(8);
       const bool act = hc < C;
       double mx = act ? lg : -INFINITY;
 #pragma unroll
       for (int o = 8; o >= 1; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      K3_MARK(9);
       const double e = act ? hexp(lg - mx) : 0.0;
+      K3_MARK(10);
       const int base = lane & 16;
-      double s = __shfl_sync(0xffffffffu, e, base);  // sequential sum (mirror order)
-      for (int c = 1; c < C; ++c) s = s + __shfl_sync(0xffffffffu, e, base + c);
+      double ev[16];
+#pragma unroll
+      for (int c = 0; c < 16; ++c) ev[c] = __shfl_sync(0xffffffffu, e, base + c);
+      double s = ev[0];  // sequential sum (mirror order)
+#pragma unroll
+      for (int c = 1; c < 16; ++c)
+        if (c < C) s = s + ev[c];
+      K3_MARK(11);
       double pr = e / s;
+      K3_MARK(12);
       if (hc == li) pr = pr - 1.0;
       p1A = __shfl_sync(0xffffffffu, pr, cA);
       p2A = __shfl_sync(0xffffffffu, pr, 16 + cA);
-      if (__all_sync(0xffffffffu, cB == cA)) {
+      if (oneclass) {
         p1B = p1A;
         p2B = p2A;
       } else {
@@ -388,6 +497,7 @@ __global__ void __launch_bounds__(256, 1) k3_inner(InParams p) {
         p2B = __shfl_sync(0xffffffffu, pr, 16 + cB);
       }
     }
+    K3_MARK(5);
 
     // ---- element-wise update + stochastic rounding (branch-free) ----
     bool bad = false, slow_any = false;
@@ -412,18 +522,15 @@ __global__ void __launch_bounds__(256, 1) k3_inner(InParams p) {
         if (valid[i] && (slow[i] || wide || rcp == 0.0))
           code[i] = (double)quantize_code(up[i], delta, p.hi, p.lo, p.maxc, p.minc, Ua[i]);
     }
-    bad_prev = bad ? 1 : 0;
-    if (pre) {
-#pragma unroll
-      for (int i = 0; i < M; ++i) Ua[i] = Ub[i];
-      if (t + 2 < T) {
-        const double* un = p.U + (t + 2) * D + k0;
-#pragma unroll
-        for (int i = 0; i < M; ++i) Ub[i] = valid[i] ? un[i] : 0.0;
-      }
-    } else {
-      rs = jump_tab(rs, jt);
+    if (__any_sync(0xffffffffu, fl)) {
+      if (rank == 0 && tid == 0) *p.blow_step = (int)(t - 1);
+      if (CL) cluster_sync_all();  // nobody leaves while remote stores may target it
+      return;
     }
+    // u of this step, kept for a blowup report at step t+1
+    store_m<M>(p.u_out + k0, up, valid, allv);
+    bad_prev = bad ? 1 : 0;
+    K3_MARK(6);
     if (t < p.trace_steps) {
 #pragma unroll
       for (int i = 0; i < M; ++i)
@@ -437,21 +544,33 @@ __global__ void __launch_bounds__(256, 1) k3_inner(InParams p) {
     p.w_out[k0 + i] = wt[i] + __dmul_rn(zc, delta);
     p.codes_out[k0 + i] = __double2ll_rn(code[i]);
   }
+#ifdef HALP_K3_PROF
+  if (prof_on)
+    printf("K3PROF T=%lld dot %.0f | send %.0f | rng %.0f | wait %.0f | flag %.0f | deriv %.0f | update %.0f | tail %.0f\n",
+           (long long)T, prof_acc[0] / (double)T, prof_acc[1] / (double)T, prof_acc[2] / (double)T,
+           prof_acc[3] / (double)T, prof_acc[4] / (double)T, prof_acc[5] / (double)T, prof_acc[6] / (double)T,
+           prof_acc[7] / (double)T);
+  if (prof_on)
+    printf("K3PROF deriv split: sum %.0f | max %.0f | exp %.0f | csum %.0f | div %.0f | rest %.0f\n", prof_acc[8] / (double)T,
+           prof_acc[9] / (double)T, prof_acc[10] / (double)T, prof_acc[11] / (double)T, prof_acc[12] / (double)T,
+           prof_acc[5] / (double)T);
+#endif
   if (CL) cluster_sync_all();  // keep every CTA's shared memory alive until all remote stores landed
 }
 
-template <class Tx, int M, bool SPAN2>
+template <class Tx, int M, int KIND>
 static cudaError_t launch_in_t(const InLaunch& L, const InParams& p, cudaStream_t st) {
   if (L.ctas * L.threads / 32 > kMaxWarpsPerCluster) return cudaErrorInvalidConfiguration;
-  const size_t smem = sizeof(double) * 2 * (size_t)(L.ctas * L.threads / 32) * (SPAN2 ? 6 : 32);
+  const size_t smem = sizeof(double) * 2 * (size_t)(L.ctas * L.threads / 32) * K3Layout<KIND>::NSLOT;
   if (L.ctas == 1) {
-    auto kern = k3_inner<Tx, M, false, SPAN2>;
+    auto kern = k3_inner<Tx, M, false, KIND>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     kern<<<1, L.threads, smem, st>>>(p);
     return cudaGetLastError();
   }
-  auto kern = k3_inner<Tx, M, true, SPAN2>;
+  if (L.ctas > 16) return cudaErrorInvalidConfiguration;
+  auto kern = k3_inner<Tx, M, true, KIND>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   if (e != cudaSuccess) return e;
   e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -472,18 +591,19 @@ static cudaError_t launch_in_t(const InLaunch& L, const InParams& p, cudaStream_
 }
 
 template <class Tx, int M>
-static cudaError_t launch_in_span(const InLaunch& L, const InParams& p, cudaStream_t st) {
-  if (p.C == 1 || 32 * M <= p.d) return launch_in_t<Tx, M, true>(L, p, st);
-  return launch_in_t<Tx, M, false>(L, p, st);
+static cudaError_t launch_in_kind(const InLaunch& L, const InParams& p, cudaStream_t st) {
+  if (p.loss == 0) return launch_in_t<Tx, M, 0>(L, p, st);
+  if (32 * M <= p.d) return launch_in_t<Tx, M, 1>(L, p, st);
+  return launch_in_t<Tx, M, 2>(L, p, st);
 }
 
 template <class Tx>
 static cudaError_t launch_in_dt(const InLaunch& L, const InParams& p, cudaStream_t st) {
   switch (L.per) {
-    case 1: return launch_in_span<Tx, 1>(L, p, st);
-    case 2: return launch_in_span<Tx, 2>(L, p, st);
-    case 4: return launch_in_span<Tx, 4>(L, p, st);
-    default: return launch_in_span<Tx, 8>(L, p, st);
+    case 1: return launch_in_kind<Tx, 1>(L, p, st);
+    case 2: return launch_in_kind<Tx, 2>(L, p, st);
+    case 4: return launch_in_kind<Tx, 4>(L, p, st);
+    default: return launch_in_kind<Tx, 8>(L, p, st);
   }
 }
 

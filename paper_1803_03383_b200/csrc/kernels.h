@@ -42,7 +42,6 @@ struct FinParams {
 };
 cudaError_t launch_finalize(const FinParams& p, cudaStream_t st);
 
-cudaError_t launch_uniforms(uint64_t state0, int64_t total, const uint64_t* pow_tab, double* U, cudaStream_t st);
 cudaError_t launch_samples(uint64_t state0, int64_t total, int opt2, uint64_t T, uint64_t n, const uint64_t* pow_tab,
                            int64_t* idx, int64_t* tpick, cudaStream_t st);
 
@@ -69,7 +68,6 @@ struct InParams {
   int64_t trace_steps;
   int* blow_step;            // -1 or failing step index
   double* u_out;             // [D] update vector of the failing step
-  const double* U;           // [T][D] precomputed rounding uniforms of the epoch, or null
 };
 struct InLaunch {
   int dtype, ctas, threads, per, nslot_pow2;

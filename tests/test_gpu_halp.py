@@ -135,13 +135,10 @@ def test_codes_match_reference_order(H, oracle):
     assert np.count_nonzero(tr.reshape(steps, 100) != orec.trace) == 0
 
 
-@pytest.mark.parametrize("pre", [0, 1])
-@pytest.mark.parametrize("nc,m", [(1, 1), (2, 2), (4, 1), (3, 4), (16, 1), (8, 4)])
-def test_cluster_plans_bitexact(H, oracle, nc, m, pre, monkeypatch):
-    """pre=1: rounding uniforms precomputed by k_uniforms; pre=0: in-kernel jumps."""
+@pytest.mark.parametrize("nc,m", [(1, 1), (2, 2), (4, 1), (3, 4), (16, 1), (8, 4), (1, 8), (16, 2)])
+def test_cluster_plans_bitexact(H, oracle, nc, m, monkeypatch):
     monkeypatch.setenv("HALP_IN_NC", str(nc))
     monkeypatch.setenv("HALP_IN_M", str(m))
-    monkeypatch.setenv("HALP_PRE_U_MAX_MB", "32768" if pre else "0")
     X, y = oracle.make_regression(600, 150, 0.1, 5)
     Xf = X.astype(np.float32)
     g, o = objs(H, oracle, Xf, y, l2=1e-3)
@@ -154,10 +151,8 @@ def test_cluster_plans_bitexact(H, oracle, nc, m, pre, monkeypatch):
     assert np.array_equal(rec.final_iterate, orec.final_iterate)
 
 
-@pytest.mark.parametrize("pre", [0, 1])
-@pytest.mark.parametrize("C,nc", [(2, 1), (10, 0), (3, 2), (10, 8)])
-def test_softmax_run_bitexact(H, oracle, C, nc, pre, monkeypatch):
-    monkeypatch.setenv("HALP_PRE_U_MAX_MB", "32768" if pre else "0")
+@pytest.mark.parametrize("C,nc", [(2, 1), (10, 0), (3, 2), (10, 8), (10, 16), (15, 4)])
+def test_softmax_run_bitexact(H, oracle, C, nc, monkeypatch):
     if nc:
         monkeypatch.setenv("HALP_IN_NC", str(nc))
     rng = np.random.default_rng(7 + C)

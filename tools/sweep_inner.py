@@ -1,6 +1,6 @@
 """Inner-loop (K3) plan sweep: us/step for cluster size NC and coords/thread M.
 
-    python tools/sweep_inner.py c2|c3|c1 [T]
+    python tools/sweep_inner.py c2|c3|c1 [T] [NC:M,NC:M,...] [VAR=VALUE ...]
 """
 import itertools
 import os
@@ -22,6 +22,10 @@ elif which == "c3":
     X, y = H.generate("regression", 65536, 4096, dtype="f32", noise_sd=0.1, seed=3)
     obj = H.Objective(H.Dataset(X, targets=y), H.LossFamily.Squared, 0.0)
     cfg = dict(alpha=5e-5, mu=1.0, bits=16)
+elif which.startswith("r"):
+    X, y = H.generate("regression", 8192, int(which[1:]), dtype="f32", noise_sd=0.01, seed=0)
+    obj = H.Objective(H.Dataset(X, targets=y), H.LossFamily.Squared, 0.0)
+    cfg = dict(alpha=1e-4, mu=1e3, bits=8)
 else:
     X, y = H.generate("regression", 8192, 256, dtype="f32", noise_sd=0.01, seed=0)
     obj = H.Objective(H.Dataset(X, targets=y), H.LossFamily.Squared, 0.0)
@@ -36,15 +40,27 @@ print("RESULT", p["in_ctas"], p["in_threads"], p["in_per"], "%.3f" % (1000 * t["
 def main():
     which = sys.argv[1]
     T = int(sys.argv[2]) if len(sys.argv) > 2 else 5000
+    rgrid = [(0, 0)] + [(1, m) for m in (1, 2, 4, 8)] + [(nc, m) for nc in (2, 4, 8, 16) for m in (1, 2, 4)]
     grids = {"c2": [(nc, m) for nc in (4, 8, 16) for m in (1, 2, 4, 8)],
              "c3": [(nc, m) for nc in (1, 2, 4, 8, 16) for m in (1, 2, 4, 8)],
-             "c1": [(nc, m) for nc in (1, 2, 4) for m in (1, 2, 4, 8)]}[which]
+             "c1": [(nc, m) for nc in (1, 2, 4) for m in (1, 2, 4, 8)]}.get(which, rgrid)
     env = dict(os.environ, ROOT=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    tag = ""
+    for a in sys.argv[3:]:
+        if "=" in a:
+            k, v = a.split("=", 1)
+            env[k] = v
+            tag += " " + a
+        else:
+            grids = [tuple(int(x) for x in g.split(":")) for g in a.split(",")]
     for nc, m in grids:
-        env["HALP_IN_NC"], env["HALP_IN_M"] = str(nc), str(m)
+        env["HALP_IN_NC"], env["HALP_IN_M"] = str(nc), str(m)  # 0 = the library's own plan
         r = subprocess.run([sys.executable, "-c", CHILD, which, str(T)], env=env, capture_output=True, text=True)
         line = [l for l in r.stdout.splitlines() if l.startswith("RESULT")]
-        print(which, "NC", nc, "M", m, line[0] if line else ("ERR " + r.stderr.strip().splitlines()[-1][:150] if r.stderr.strip() else "ERR"), flush=True)
+        profs = [l for l in r.stdout.splitlines() if l.startswith("K3PROF")]  # -DHALP_K3_PROF builds
+        for l in profs[-2:]:
+            print("   ", l)
+        print(which + tag, "NC", nc, "M", m, line[0] if line else ("ERR " + r.stderr.strip().splitlines()[-1][:150] if r.stderr.strip() else "ERR"), flush=True)
 
 
 if __name__ == "__main__":
