@@ -158,7 +158,7 @@ static int check_objective(const oq_objective* o) {
  * ====================================================================== */
 
 /* Deterministic exp/log built only from IEEE +,-,*,/,fma, rint and
- * exponent manipulation; the device code (csrc/halp_math.cuh) performs the
+ * exponent manipulation; the device code (csrc/halp_device.cuh hexp/hlog) performs the
  * identical sequence, so results agree bit for bit. */
 double oq_mexp(double x) {
   if (!(x == x)) return x;
@@ -167,20 +167,19 @@ double oq_mexp(double x) {
   const double kf = rint(x * 1.4426950408889634);
   const double r1 = fma(-kf, 6.93147180369123816490e-01, x);
   const double r = fma(-kf, 1.90821492927058770002e-10, r1);
-  double p = 1.60590438368216145994e-10;             /* 1/13! */
-  p = fma(p, r, 2.08767569878680989792e-09);         /* 1/12! */
-  p = fma(p, r, 2.50521083854417187751e-08);         /* 1/11! */
-  p = fma(p, r, 2.75573192239858906526e-07);
-  p = fma(p, r, 2.75573192239858906526e-06);
-  p = fma(p, r, 2.48015873015873015873e-05);
-  p = fma(p, r, 1.98412698412698412698e-04);
-  p = fma(p, r, 1.38888888888888888889e-03);
-  p = fma(p, r, 8.33333333333333333333e-03);
-  p = fma(p, r, 4.16666666666666666667e-02);
-  p = fma(p, r, 1.66666666666666666667e-01);
-  p = fma(p, r, 0.5);
-  p = fma(p, r, 1.0);
-  p = fma(p, r, 1.0);
+  /* Taylor polynomial of degree 13 evaluated by Estrin's scheme (depth 5
+   * instead of 13 dependent fma; k_inner.cu/k_fullgrad.cu use the same) */
+  const double r2 = r * r, r4 = r2 * r2, r8 = r4 * r4;
+  const double q0 = fma(1.0, r, 1.0);
+  const double q1 = fma(1.66666666666666666667e-01, r, 0.5);
+  const double q2 = fma(8.33333333333333333333e-03, r, 4.16666666666666666667e-02);
+  const double q3 = fma(1.98412698412698412698e-04, r, 1.38888888888888888889e-03);
+  const double q4 = fma(2.75573192239858906526e-06, r, 2.48015873015873015873e-05);
+  const double q5 = fma(2.50521083854417187751e-08, r, 2.75573192239858906526e-07);
+  const double q6 = fma(1.60590438368216145994e-10, r, 2.08767569878680989792e-09);
+  const double e0 = fma(q1, r2, q0), e1 = fma(q3, r2, q2), e2 = fma(q5, r2, q4);
+  const double u0 = fma(e1, r4, e0), u1 = fma(q6, r4, e2);
+  const double p = fma(u1, r8, u0);
   const int k = (int)kf;
   /* scale by 2^k in two steps so subnormal results round once */
   if (k > -1000) {
@@ -504,6 +503,22 @@ static double mirror_softmax_loss(const double* l, int C, int label) {
   double s = 0.0;
   for (int c = 0; c < C; ++c) s = s + oq_mexp(l[c] - mx);
   return (mx + oq_mlog(s)) - l[label];
+}
+
+/* K3's softmax derivative: exact max, deterministic exp, denominator summed
+ * by a pairwise tree over 16 class slots padded with zeros (k_inner.cu) */
+static void mirror_softmax_dl_k3(double* l, int C, int label) {
+  double mx = l[0];
+  for (int c = 1; c < C; ++c) if (l[c] > mx) mx = l[c];
+  double e[64];
+  int P = 16;
+  while (P < C) P *= 2; /* the device supports C <= 15 */
+  for (int c = 0; c < P; ++c) e[c] = c < C ? oq_mexp(l[c] - mx) : 0.0;
+  for (int h = 1; h < P; h <<= 1)
+    for (int c = 0; c < P; c += 2 * h) e[c] = e[c] + e[c + h];
+  const double s = e[0];
+  for (int c = 0; c < C; ++c) l[c] = oq_mexp(l[c] - mx) / s;
+  l[label] = l[label] - 1.0;
 }
 
 /* pairwise tree over n items (split at the largest power of two < n) */
@@ -943,8 +958,8 @@ int oq_run_halp(const oq_objective* o, const oq_config* cfg, const oq_plan* plan
           }
         } else {
           const int y = o->labels[i];
-          mirror_softmax_dl(la, C, y);
-          mirror_softmax_dl(lb, C, y);
+          mirror_softmax_dl_k3(la, C, y);
+          mirror_softmax_dl_k3(lb, C, y);
           for (int c = 0; c < C; ++c)
             for (int j = 0; j < d; ++j) {
               const size_t q = (size_t)c * d + j;

@@ -132,20 +132,18 @@ __device__ __forceinline__ double hexp(double x) {
   const double kf = rint(__dmul_rn(x, 1.4426950408889634));
   const double r1 = fma(-kf, 6.93147180369123816490e-01, x);
   const double r = fma(-kf, 1.90821492927058770002e-10, r1);
-  double p = 1.60590438368216145994e-10;
-  p = fma(p, r, 2.08767569878680989792e-09);
-  p = fma(p, r, 2.50521083854417187751e-08);
-  p = fma(p, r, 2.75573192239858906526e-07);
-  p = fma(p, r, 2.75573192239858906526e-06);
-  p = fma(p, r, 2.48015873015873015873e-05);
-  p = fma(p, r, 1.98412698412698412698e-04);
-  p = fma(p, r, 1.38888888888888888889e-03);
-  p = fma(p, r, 8.33333333333333333333e-03);
-  p = fma(p, r, 4.16666666666666666667e-02);
-  p = fma(p, r, 1.66666666666666666667e-01);
-  p = fma(p, r, 0.5);
-  p = fma(p, r, 1.0);
-  p = fma(p, r, 1.0);
+  // degree-13 Taylor polynomial by Estrin's scheme (oq_mexp, same order)
+  const double r2 = __dmul_rn(r, r), r4 = __dmul_rn(r2, r2), r8 = __dmul_rn(r4, r4);
+  const double q0 = fma(1.0, r, 1.0);
+  const double q1 = fma(1.66666666666666666667e-01, r, 0.5);
+  const double q2 = fma(8.33333333333333333333e-03, r, 4.16666666666666666667e-02);
+  const double q3 = fma(1.98412698412698412698e-04, r, 1.38888888888888888889e-03);
+  const double q4 = fma(2.75573192239858906526e-06, r, 2.48015873015873015873e-05);
+  const double q5 = fma(2.50521083854417187751e-08, r, 2.75573192239858906526e-07);
+  const double q6 = fma(1.60590438368216145994e-10, r, 2.08767569878680989792e-09);
+  const double e0 = fma(q1, r2, q0), e1 = fma(q3, r2, q2), e2 = fma(q5, r2, q4);
+  const double u0 = fma(e1, r4, e0), u1 = fma(q6, r4, e2);
+  const double p = fma(u1, r8, u0);
   const int k = (int)kf;
   if (k > -1000) {
     const int k1 = k / 2, k2 = k - k1;

@@ -32,7 +32,8 @@
 // sequential fma over its coordinates; warp = xor butterfly 16..1; across
 // warps, squared loss (C == 1): lane l sums warps l, l+32, ... sequentially,
 // then a lane butterfly; softmax (C >= 2): sequential over the warps holding
-// the class, in global warp order.
+// the class, in global warp order; the softmax denominator is a pairwise tree
+// over 16 class slots (zero padded).
 #include <cstdio>
 
 #include "halp_device.cuh"
@@ -145,6 +146,7 @@ __global__ void __launch_bounds__(256, 1) k3_inner(InParams p) {
   constexpr bool SQ = KIND == 0;
   __shared__ uint64_t jt[2048];
   __shared__ __align__(8) uint64_t mbar[2];
+  __shared__ __align__(16) double gsc[2][8][32];  // softmax gathers: [parity][warp][lane]
   extern __shared__ __align__(16) double xbuf_dyn[];  // [2][NGW][NSLOT]
 
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, NW = blockDim.x >> 5;
@@ -222,7 +224,7 @@ __global__ void __launch_bounds__(256, 1) k3_inner(InParams p) {
     off_rest = q_first * NSLOT + slot_rest;
   }
 
-  double wt[M], gt[M], up[M], Ua[M];
+  double wt[M], gt[M], l2w[M], up[M], Ua[M];
   Tx xa[M], xb[M];
   double code[M], snap[M];  // z codes as exact doubles (|code| <= 2^(bits-1))
   const bool wide = p.hi > 0x1.0p53;
@@ -238,6 +240,7 @@ __global__ void __launch_bounds__(256, 1) k3_inner(InParams p) {
     fj[i] = valid[i] ? (int)(k % d) : 0;
     wt[i] = valid[i] ? p.w[k] : 0.0;
     gt[i] = valid[i] ? p.g[k] : 0.0;
+    l2w[i] = __dmul_rn(l2, wt[i]);
     code[i] = 0.0;
     snap[i] = 0.0;
     up[i] = 0.0;
@@ -249,6 +252,8 @@ __global__ void __launch_bounds__(256, 1) k3_inner(InParams p) {
   for (int i = 0; i < M; ++i)
     if (valid[i]) cB = cls[i];
   const bool oneclass = __all_sync(0xffffffffu, cB == cA);
+  // KIND 1: does this warp straddle two classes? (else a1 = b1 = 0 always)
+  const bool wsplit = KIND == 1 && !__all_sync(0xffffffffu, !valid[0] || (cA == cw0 && cB == cw0));
   // vector row loads when the thread's coordinates are aligned and in one class
   const bool vecx = (d % M == 0) && (ld % M == 0);
   const int64_t T = p.T;
@@ -290,17 +295,26 @@ __global__ void __launch_bounds__(256, 1) k3_inner(InParams p) {
       }
       if (t + 2 < T) load_row_m<Tx, M>(X + row2 * ld, fj, vecx, xb);  // raw prefetch, step t+2
       const int cS = KIND == 1 ? cw0 : cA;
+      if (SQ || (KIND == 1 && !wsplit)) {  // single-class warp: one pair
 #pragma unroll
-      for (int i = 0; i < M; ++i) {
-        if (!valid[i]) continue;
-        const double z = __dmul_rn(code[i], delta);
-        const double wz = wt[i] + z;
-        if (SQ || cls[i] == cS) {
+        for (int i = 0; i < M; ++i) {
+          if (!valid[i]) continue;
+          const double wz = wt[i] + __dmul_rn(code[i], delta);
           a0 = fma(xc[i], wz, a0);
           b0 = fma(xc[i], wt[i], b0);
-        } else {
-          a1 = fma(xc[i], wz, a1);
-          b1 = fma(xc[i], wt[i], b1);
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < M; ++i) {
+          if (!valid[i]) continue;
+          const double wz = wt[i] + __dmul_rn(code[i], delta);
+          if (cls[i] == cS) {
+            a0 = fma(xc[i], wz, a0);
+            b0 = fma(xc[i], wt[i], b0);
+          } else {
+            a1 = fma(xc[i], wz, a1);
+            b1 = fma(xc[i], wt[i], b1);
+          }
         }
       }
     }
@@ -456,7 +470,7 @@ __global__ void __launch_bounds__(256, 1) k3_inner(InParams p) {
       p1A = p1B = sa - yi;
       p2A = p2B = sb - yi;
     } else {
-      // loads first, then the in-order chain
+      // loads first, then the in-order chain (absent warps add +0.0: exact)
       constexpr int QH = 8;
       double pv[QH];
       pv[0] = nq > 0 ? xbp[off_first] : 0.0;
@@ -464,25 +478,48 @@ __global__ void __launch_bounds__(256, 1) k3_inner(InParams p) {
       for (int j = 1; j < QH; ++j) pv[j] = j < nq ? xbp[off_rest + j * NSLOT] : 0.0;
       double lg = pv[0];
 #pragma unroll
-      for (int j = 1; j < QH; ++j)
-        if (j < nq) lg = lg + pv[j];
+      for (int j = 1; j < QH; ++j) lg = lg + pv[j];
       for (int j = QH; j < nq; ++j) lg = lg + xbp[off_rest + j * NSLOT];
       K3_MARK(8);
+      // every lane gathers its half's 16 logits (one shuffle round) and takes
+      // the max in registers; softmax sum = pairwise tree over 16 (zeros pad)
       const bool act = hc < C;
-      double mx = act ? lg : -INFINITY;
+      // gathers through a per-warp shared scratch (parity double-buffered):
+      // one store + 8 broadcast 16-byte loads instead of 32 shuffles
+      double* gs = &gsc[par][wid][0];
+      const double2* gh = reinterpret_cast<const double2*>(gs + (lane & 16));
+      double mv[16];
+      gs[lane] = act ? lg : -INFINITY;
+      __syncwarp();
 #pragma unroll
-      for (int o = 8; o >= 1; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      for (int c = 0; c < 8; ++c) {
+        const double2 v2 = gh[c];
+        mv[2 * c] = v2.x;
+        mv[2 * c + 1] = v2.y;
+      }
+#pragma unroll
+      for (int h = 8; h >= 1; h >>= 1)
+#pragma unroll
+        for (int c = 0; c < h; ++c) mv[c] = fmax(mv[c], mv[c + h]);
+      const double mx = mv[0];
       K3_MARK(9);
       const double e = act ? hexp(lg - mx) : 0.0;
       K3_MARK(10);
-      const int base = lane & 16;
+      __syncwarp();
       double ev[16];
+      gs[lane] = e;
+      __syncwarp();
 #pragma unroll
-      for (int c = 0; c < 16; ++c) ev[c] = __shfl_sync(0xffffffffu, e, base + c);
-      double s = ev[0];  // sequential sum (mirror order)
+      for (int c = 0; c < 8; ++c) {
+        const double2 v2 = gh[c];
+        ev[2 * c] = v2.x;
+        ev[2 * c + 1] = v2.y;
+      }
 #pragma unroll
-      for (int c = 1; c < 16; ++c)
-        if (c < C) s = s + ev[c];
+      for (int h = 1; h < 16; h <<= 1)
+#pragma unroll
+        for (int c = 0; c < 16; c += 2 * h) ev[c] = ev[c] + ev[c + h];
+      const double s = ev[0];
       K3_MARK(11);
       double pr = e / s;
       K3_MARK(12);
@@ -509,7 +546,7 @@ __global__ void __launch_bounds__(256, 1) k3_inner(InParams p) {
       const double z = __dmul_rn(code[i], delta);
       const double wz = wt[i] + z;
       const double g1 = __dmul_rn(pp1, xc[i]) + __dmul_rn(l2, wz);
-      const double g2 = __dmul_rn(pp2, xc[i]) + __dmul_rn(l2, wt[i]);
+      const double g2 = __dmul_rn(pp2, xc[i]) + l2w[i];
       const double u = z - __dmul_rn(alpha, (g1 - g2) + gt[i]);
       up[i] = u;
       bad |= valid[i] && !isfinite(u);
