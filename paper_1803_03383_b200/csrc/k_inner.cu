@@ -135,9 +135,13 @@ __device__ __forceinline__ void store_m(double* dst, const double (&v)[M], const
 // KIND 2: softmax with small d: 2*C slots per warp.
 template <int KIND>
 struct K3Layout {
-  static constexpr int NSLOT = KIND == 0 ? 4 : KIND == 1 ? 6 : 32;  // doubles per warp record
-  static constexpr int FLAG = KIND == 0 ? 2 : KIND == 1 ? 4 : 31;   // slot of the non-finite flag
+  static constexpr int NSLOT = KIND == 0 ? 2 : KIND == 1 ? 4 : 32;  // doubles per warp record
+  static constexpr int FLAG = KIND == 2 ? 31 : -1;                  // explicit flag slot (KIND 2)
 };
+// KIND 0/1 carry the blowup flag in-band: a warp whose previous update was
+// non-finite sends this signalling-NaN pattern in place of all its partials
+// (arithmetic never produces it; NaN logits make receivers rescan for it).
+constexpr long long kFlagBits = 0x7FF4A1B2C3D4E5F6LL;
 
 template <class Tx, int M, bool CL, int KIND>
 __global__ void __launch_bounds__(256, 1) k3_inner(InParams p) {
@@ -161,8 +165,8 @@ __global__ void __launch_bounds__(256, 1) k3_inner(InParams p) {
   const int WC = 32 * M;  // coordinates per warp
   const int PAR_STRIDE = NGW * NSLOT;  // doubles between the two parity buffers
   auto XB = [&](int par_, int q_, int slot_) -> double& { return xbuf_dyn[par_ * PAR_STRIDE + q_ * NSLOT + slot_]; };
-  const uint32_t bytes_step = KIND == 0 ? (uint32_t)NGW * 24u
-                              : KIND == 1 ? (uint32_t)NGW * 40u
+  const uint32_t bytes_step = KIND == 0 ? (uint32_t)NGW * 16u
+                              : KIND == 1 ? (uint32_t)NGW * 32u
                                           : (uint32_t)NGW * (uint32_t)(2 * C + 1) * 8u;
 
   for (int i = tid; i < 2048; i += blockDim.x) jt[i] = p.jump_tab[i];
@@ -174,22 +178,20 @@ __global__ void __launch_bounds__(256, 1) k3_inner(InParams p) {
 
   // Remote targets of this lane's st.async messages, fixed for the epoch
   // (parity 1 = parity 0 + a constant offset in every CTA's window).
-  //   KIND 0: lanes 0..15 send the pair to CTA lane, lanes 16..31 the flag to
-  //           CTA lane-16.
-  //   KIND 1: lanes with (lane & 8) == 0 send pair 2*(lane>>4) and lanes 8..15
-  //           the flag, each to CTAs (lane & 7) and (lane & 7) + 8.
+  //   KIND 0: lanes 0..15 send the pair to CTA lane.
+  //   KIND 1: lanes with (lane & 8) == 0 send pair 2*(lane>>4) to CTAs
+  //           (lane & 7) and (lane & 7) + 8.
   uint32_t ra0 = 0, ra1 = 0, rb0 = 0, rb1 = 0;
   bool s0ok = false, s1ok = false;
   const uint32_t xb_par_off = (uint32_t)(PAR_STRIDE * 8), mb_par_off = 8u;
   if (CL && KIND == 0) {
-    const int slot = lane < 16 ? 0 : FLAG;
     const int r0 = lane & 15;
-    s0ok = r0 < NC;
-    ra0 = mapa_u32(&XB(0, gw, slot), (uint32_t)(s0ok ? r0 : 0));
+    s0ok = lane < 16 && r0 < NC;
+    ra0 = mapa_u32(&XB(0, gw, 0), (uint32_t)(s0ok ? r0 : 0));
     rb0 = mapa_u32(&mbar[0], (uint32_t)(s0ok ? r0 : 0));
   } else if (CL && KIND == 1) {
-    const int slot = (lane & 8) ? FLAG : 2 * (lane >> 4);
-    const bool sender = !(lane & 8) || !(lane & 16);
+    const int slot = 2 * (lane >> 4);
+    const bool sender = !(lane & 8);
     const int r0 = lane & 7, r1 = (lane & 7) + 8;
     s0ok = sender && r0 < NC;
     s1ok = sender && r1 < NC;
@@ -319,7 +321,9 @@ __global__ void __launch_bounds__(256, 1) k3_inner(InParams p) {
       }
     }
     K3_MARK(0);
-    const double flagv = __any_sync(0xffffffffu, bad_prev) ? 1.0 : 0.0;
+    const bool flag = __any_sync(0xffffffffu, bad_prev);
+    const double flagv = flag ? 1.0 : 0.0;
+    const double fnan = __longlong_as_double(kFlagBits);
     if constexpr (KIND == 0) {
       // all-reduce butterfly of a0 on lanes 0..15 and of b0 on lanes 16..31
       const bool u16 = (lane & 16) != 0;
@@ -328,16 +332,13 @@ __global__ void __launch_bounds__(256, 1) k3_inner(InParams p) {
       v = v + __shfl_xor_sync(0xffffffffu, v, 4);
       v = v + __shfl_xor_sync(0xffffffffu, v, 2);
       v = v + __shfl_xor_sync(0xffffffffu, v, 1);
-      const double vp = __shfl_xor_sync(0xffffffffu, v, 16);
+      double vp = __shfl_xor_sync(0xffffffffu, v, 16);
+      if (flag) v = vp = fnan;
       if (CL) {
         const uint32_t xo = par ? xb_par_off : 0u, mo = par ? mb_par_off : 0u;
-        if (s0ok) {
-          if (!u16) st_async_v2f64(ra0 + xo, v, vp, rb0 + mo);
-          else st_async_f64(ra0 + xo, flagv, rb0 + mo);
-        }
+        if (s0ok) st_async_v2f64(ra0 + xo, v, vp, rb0 + mo);
       } else {
         if (lane == 0) *reinterpret_cast<double2*>(&XB(par, gw, 0)) = make_double2(v, vp);
-        if (lane == 16) XB(par, gw, FLAG) = flagv;
       }
     } else if constexpr (KIND == 1) {
       // warp reduce-scatter of (a0, b0, a1, b1): 8-lane group g ends with slot g
@@ -349,19 +350,14 @@ __global__ void __launch_bounds__(256, 1) k3_inner(InParams p) {
       v = v + __shfl_xor_sync(0xffffffffu, v, 4);
       v = v + __shfl_xor_sync(0xffffffffu, v, 2);
       v = v + __shfl_xor_sync(0xffffffffu, v, 1);
-      const double vp = __shfl_xor_sync(0xffffffffu, v, 8);  // pair g with g^1
+      double vp = __shfl_xor_sync(0xffffffffu, v, 8);  // pair g with g^1
+      if (flag) v = vp = fnan;
       if (CL) {
         const uint32_t xo = par ? xb_par_off : 0u, mo = par ? mb_par_off : 0u;
-        if (!u8) {
-          if (s0ok) st_async_v2f64(ra0 + xo, v, vp, rb0 + mo);
-          if (s1ok) st_async_v2f64(ra1 + xo, v, vp, rb1 + mo);
-        } else {
-          if (s0ok) st_async_f64(ra0 + xo, flagv, rb0 + mo);
-          if (s1ok) st_async_f64(ra1 + xo, flagv, rb1 + mo);
-        }
+        if (s0ok) st_async_v2f64(ra0 + xo, v, vp, rb0 + mo);
+        if (s1ok) st_async_v2f64(ra1 + xo, v, vp, rb1 + mo);
       } else {
         if ((lane & 15) == 0) *reinterpret_cast<double2*>(&XB(par, gw, (lane >> 4) << 1)) = make_double2(v, vp);
-        if (lane == 8) XB(par, gw, FLAG) = flagv;
       }
     } else {
       // 32-slot reduce-scatter (slot 2c = class c at wz, 2c+1 at w~): lane l ends with slot l
@@ -415,16 +411,32 @@ __global__ void __launch_bounds__(256, 1) k3_inner(InParams p) {
     K3_MARK(3);
 
     const double* xbp = xbuf_dyn + par * PAR_STRIDE;
-    // blowup of step t-1?  (flags loaded now, tested after this step's update:
-    // a blowup leaves code[] dead, and u of step t-1 is already in u_out)
-    int fl = 0;
+    // blowup of step t-1?  Tested after this step's update (a blowup leaves
+    // code[] dead, and u of step t-1 is already in u_out).  KIND 0/1: a lane
+    // whose partial sums came out NaN raises `cand`, and the records are then
+    // scanned for the flag pattern (a NaN of this step's own is not a flag).
+    auto flagged = [&]() -> bool {
+      int f = 0;
 #pragma unroll
-    for (int j = 0; j < kMaxWarpsPerCluster / 32; ++j) {
-      const int q = lane + 32 * j;
-      if (q < NGW) fl |= xbp[q * NSLOT + FLAG] != 0.0;
+      for (int j = 0; j < kMaxWarpsPerCluster / 32; ++j) {
+        const int q = lane + 32 * j;
+        if (q < NGW) {
+          if constexpr (KIND == 2) f |= xbp[q * NSLOT + FLAG] != 0.0;
+          else f |= __double_as_longlong(xbp[q * NSLOT]) == kFlagBits;
+        }
+      }
+      return __any_sync(0xffffffffu, f);
+    };
+    int fl = 0;
+    if constexpr (KIND == 2) {
+#pragma unroll
+      for (int j = 0; j < kMaxWarpsPerCluster / 32; ++j) {
+        const int q = lane + 32 * j;
+        if (q < NGW) fl |= xbp[q * NSLOT + FLAG] != 0.0;
+      }
     }
     if (last) {
-      if (__any_sync(0xffffffffu, fl)) {
+      if (flagged()) {
         if (rank == 0 && tid == 0) *p.blow_step = (int)(t - 1);
         if (CL) cluster_sync_all();  // nobody leaves while remote stores may target it
         return;
@@ -457,6 +469,7 @@ __global__ void __launch_bounds__(256, 1) k3_inner(InParams p) {
           sb = sb + v.y;
         }
       }
+      fl = isnan(sa) || isnan(sb);
       K3_MARK(8);
       // lanes >= NGW hold +0.0: butterfly levels that only add zeros are skipped
       for (int o = (NGW >= 32 ? 16 : NGW > 1 ? (1 << (31 - __clz(NGW - 1))) : 0); o >= 1; o >>= 1) {
@@ -480,6 +493,7 @@ __global__ void __launch_bounds__(256, 1) k3_inner(InParams p) {
 #pragma unroll
       for (int j = 1; j < QH; ++j) lg = lg + pv[j];
       for (int j = QH; j < nq; ++j) lg = lg + xbp[off_rest + j * NSLOT];
+      if (KIND == 1) fl = isnan(lg);
       K3_MARK(8);
       // every lane gathers its half's 16 logits (one shuffle round) and takes
       // the max in registers; softmax sum = pairwise tree over 16 (zeros pad)
@@ -559,7 +573,7 @@ __global__ void __launch_bounds__(256, 1) k3_inner(InParams p) {
         if (valid[i] && (slow[i] || wide || rcp == 0.0))
           code[i] = (double)quantize_code(up[i], delta, p.hi, p.lo, p.maxc, p.minc, Ua[i]);
     }
-    if (__any_sync(0xffffffffu, fl)) {
+    if (__any_sync(0xffffffffu, fl) && (KIND == 2 || flagged())) {
       if (rank == 0 && tid == 0) *p.blow_step = (int)(t - 1);
       if (CL) cluster_sync_all();  // nobody leaves while remote stores may target it
       return;

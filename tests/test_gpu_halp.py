@@ -262,3 +262,34 @@ def test_device_resident_inputs_and_datagen(H, oracle):
     assert 0.15 < float((Xs != 0).float().mean()) < 0.25
     Xb, lb = H.generate("logistic", 4096, 1024, dtype="bf16", x_scale=1 / 32, seed=2)
     assert Xb.dtype == torch.bfloat16 and set(np.unique(lb.cpu().numpy())) <= {0, 1}
+
+
+@pytest.mark.parametrize("kind,nc,m", [("sq", 1, 2), ("sq", 4, 1), ("sq", 16, 2), ("sm1", 4, 2), ("sm1", 1, 4),
+                                       ("sm2", 0, 0), ("sm2", 2, 1)])
+def test_blowup_mid_epoch_bitexact(H, oracle, kind, nc, m, monkeypatch):
+    """Blowups after a few inner steps, on single-CTA and cluster plans of all
+    three inner-loop kinds: same step, same partial record, same iterate."""
+    if nc:
+        monkeypatch.setenv("HALP_IN_NC", str(nc))
+        monkeypatch.setenv("HALP_IN_M", str(m))
+    rng = np.random.default_rng(5)
+    if kind == "sq":
+        X, y = oracle.make_regression(300, 150, 0.5, 3)
+        g, o = objs(H, oracle, X.astype(np.float32), y, l2=1e-3)
+        alpha = 3e305
+    else:
+        d, C = (300, 3) if kind == "sm1" else (20, 10)
+        X = (rng.random((400, d)) * 4.0).astype(np.float32)
+        lab = rng.integers(0, C, 400).astype(np.int32)
+        g, o = objs(H, oracle, X, labels=lab, C=C, l2=1e-4)
+        alpha = 1.5e308 if kind == "sm1" else 5e307
+    cfg = dict(alpha=alpha, epochs=3, inner_steps=50, bits=8, mu=2.0, seed=4)
+    oc = oracle.OracleConfig(**cfg)
+    orec = oracle.run_halp(o, oc, plan=g.oracle_plan())
+    assert orec.status == "diverged"
+    with pytest.raises(H.DivergenceError) as ei:
+        H.run_halp(g, H.OptimizerConfig(algorithm=H.Algorithm.Halp, **cfg))
+    part = ei.value.partial
+    rows_equal(part.rows, orec.rows)
+    assert np.array_equal(part.final_iterate, orec.final_iterate)
+    assert part.steps_taken == orec.steps_taken
