@@ -223,7 +223,16 @@ int plan_for(int64_t n, int d, int C, int dtype, KernelPlan* kp) {
     }
   } else {
     const size_t smem = fg_smem_bytes(ld, es, d * C, C, T1, 2, 4);
-    if (smem > 220 * 1024) return fail(HALP_UNSUPPORTED, "full_gradient: row tile + iterate exceed shared memory");
+    // softmax with 3..15 classes: one-pass kernel with a 32-slot reduce-scatter
+    const int64_t S_ = make_shard_plan(n, d, C, dtype, 1, 0).S;
+    const int Ts = (int)((ngroups + 31) / 32 * 32);
+    if (C >= 3 && ngroups <= 256 && V * C <= 64 && !(es == 2 && C < 8) && env_int("HALP_FG_GENERIC", 0) == 0 &&
+        smx_smem_bytes(ld, es, d, C, Ts, (n + S_ - 1) / S_ + 1) <= 220 * 1024) {
+      kp->fg = FgLaunch{dtype, 1, C, Ts, ld, 0, 3, 32 / C, 4};
+      kp->fg_passes = 1;
+    } else if (smem > 220 * 1024) {
+      return fail(HALP_UNSUPPORTED, "full_gradient: row tile + iterate exceed shared memory");
+    }
   }
   // inner loop: M coordinates per thread, up to 16 CTAs per cluster
   const int64_t D = (int64_t)d * C;
