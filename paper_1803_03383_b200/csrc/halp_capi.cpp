@@ -179,6 +179,48 @@ struct KernelPlan {
   int fg_passes = 1;
 };
 
+// K1 streaming-kernel plan for C <= 2 (k_fullgrad_stream.cu): thread count
+// covering the 16-byte feature groups, rows per tile by the register budget,
+// only shapes instantiated in HALP_STREAM_SHAPES.  Returns false if none fits.
+bool stream_shape_ok(int nw, int ng, int r, int st) {
+#define HALP_STREAM_OK(NW, NG, R, ST) \
+  if (nw == NW && ng == NG && r == R && st == ST) return true;
+  HALP_STREAM_SHAPES(HALP_STREAM_OK)
+#undef HALP_STREAM_OK
+  return false;
+}
+
+bool plan_stream(int d, int C, int dtype, FgLaunch* out) {
+  const int es = elem_size(dtype);
+  const int V = 16 / es;
+  const int ld = (int)(((int64_t)d * es + 15) / 16 * 16 / es);
+  const int ngroups = (d + V - 1) / V;
+  int NG = (int)env_int("HALP_FG_NG", 0);
+  if (NG <= 0) {
+    NG = 1;  // measured on B200 (tools/fg_sweep.py): 256-thread CTAs beat 512 at C3
+    while (ngroups > 256 * NG) NG *= 2;
+  }
+  if (NG > 4) return false;
+  int T1 = 32;
+  while (T1 < 512 && T1 * NG < ngroups) T1 *= 2;
+  if (T1 * NG < ngroups) return false;
+  const int row_bytes = ld * es;
+  int stages = (int)env_int("HALP_FG_STAGES", 4);
+  int R = (int)env_int("HALP_FG_ROWS", 0);
+  if (R <= 0) {
+    R = 8;
+    const int reg_cap = std::min(255, 65536 / T1);
+    auto regs = [&](int r) { return 2 * (r * NG * V + 2 * NG * V * C + r * C) + 48; };
+    while (R > 1 && (R * C > 16 || R * NG * V > 32 || regs(R) > reg_cap || (int64_t)R * row_bytes > 32 * 1024 ||
+                     !stream_shape_ok(T1 / 32, NG, R, stages)))
+      R /= 2;
+  }
+  if (!stream_shape_ok(T1 / 32, NG, R, stages)) return false;
+  if (stream_smem_bytes(ld, es, T1 / 32, R, C, stages) > 220 * 1024) return false;
+  *out = FgLaunch{dtype, NG, C, T1, ld, 0, 4, R, stages};
+  return true;
+}
+
 // kernel plan as a pure function of the problem shape (CPU-callable)
 int plan_for(int64_t n, int d, int C, int dtype, KernelPlan* kp) {
   (void)n;
@@ -220,6 +262,14 @@ int plan_for(int64_t n, int d, int C, int dtype, KernelPlan* kp) {
       const int64_t split_rows = (n + S_ - 1) / S_ + 1;  // targets staged in shared memory
       const size_t smem2 = (size_t)4 * R2 * ld * es + 2 * (size_t)(T2 / 32) * R2 * C * 8 + 32 + 8 * split_rows;
       if (NG2 * V * C <= 32 && NG2 <= 4 && smem2 <= 200 * 1024) kp->fg = FgLaunch{dtype, NG2, CT, T2, ld, 0, 2, R2, 4};
+    }
+  }
+  // persistent streaming kernel (default for C <= 2)
+  if (C <= 2 && env_int("HALP_FG_GENERIC", 0) == 0 && env_int("HALP_FG_KERNEL", 4) == 4) {
+    FgLaunch fl;
+    if (plan_stream(d, C, dtype, &fl)) {
+      kp->fg = fl;
+      kp->fg_passes = 1;
     }
   } else {
     const size_t smem = fg_smem_bytes(ld, es, d * C, C, T1, 2, 4);

@@ -794,6 +794,7 @@ size_t fg_smem_bytes(int ld, int elem, int D, int C, int threads, int R, int sta
 
 cudaError_t launch_fullgrad(const FgLaunch& L, const FgParams& p, cudaStream_t st) {
   if (L.fast == 3) return launch_fullgrad_smx(L, p, st);
+  if (L.fast == 4) return launch_fullgrad_stream(L, p, st);
   if (L.fast == 2) {
     switch (L.dtype * 10 + p.C) {
       case 1: return launch_reg_cc<double, 1>(L, p, st);

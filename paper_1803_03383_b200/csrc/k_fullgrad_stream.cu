@@ -1,0 +1,365 @@
+// k_fullgrad_stream.cu -- K1 for the HBM-bound shapes (C <= 2 outputs per
+// feature, i.e. least squares and 2-class softmax; BASELINE C1/C3/C4): a
+// persistent streaming kernel.
+//
+// Reference: Objective::full_gradient + Objective::loss in one HBM pass
+// (proj/src/objectives.cpp:258-311 and :193-223; squared rows :274-276,
+// softmax rows :277-283).
+//
+// Structure (everything that decides the instruction count is compile-time):
+//   * one CTA per SM (or two), each walking its splits s = blockIdx.x,
+//     blockIdx.x + gridDim.x, ... with ONE continuous cp.async.bulk ring of
+//     STAGES tiles of R rows -- the ring runs across split boundaries, so the
+//     copy engine never drains between splits;
+//   * thread t owns the 16-byte feature groups t, t + T1, ... (NG of them):
+//     its slice of w~ and of the split's gradient columns live in registers,
+//     the tile's x slice is converted to fp64 once and reused by the dot and
+//     the gradient phase;
+//   * per tile ONE __syncthreads: warp reduce-scatter of the R x C partial
+//     logits -> shared (parity double-buffered) -> every warp sums the NW
+//     warp partials of its lane's slot (fully unrolled) and evaluates the
+//     loss derivative itself (squared: e = x.w - y; softmax: lane-parallel),
+//     so no second barrier broadcasts it.
+//
+// Floating-point order = k1_reg / k1_fullgrad = oracle MIRROR mode (DESIGN.md
+// "Reduction orders"): row dot = sequential fma over the thread's groups,
+// warp xor butterfly 16..1, warps summed in order; gradient column =
+// sequential fma over the split's rows; loss = sequential over the rows.
+#include "halp_device.cuh"
+#include "kernels.h"
+
+namespace halp {
+
+namespace {
+
+template <class Tx> struct VecK;
+template <> struct VecK<float> { static constexpr int V = 4; };
+template <> struct VecK<__nv_bfloat16> { static constexpr int V = 8; };
+template <> struct VecK<double> { static constexpr int V = 2; };
+
+// one 16-byte group from shared memory, upcast exactly
+template <class Tx>
+__device__ __forceinline__ void load_group_k(const Tx* p, double* out) {
+  const uint4 raw = *reinterpret_cast<const uint4*>(p);
+  if constexpr (sizeof(Tx) == 4) {
+    out[0] = (double)__uint_as_float(raw.x);
+    out[1] = (double)__uint_as_float(raw.y);
+    out[2] = (double)__uint_as_float(raw.z);
+    out[3] = (double)__uint_as_float(raw.w);
+  } else if constexpr (sizeof(Tx) == 2) {
+    const uint32_t wds[4] = {raw.x, raw.y, raw.z, raw.w};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      out[2 * q] = (double)__uint_as_float(wds[q] << 16);
+      out[2 * q + 1] = (double)__uint_as_float(wds[q] & 0xFFFF0000u);
+    }
+  } else {
+    out[0] = __longlong_as_double(((long long)raw.y << 32) | raw.x);
+    out[1] = __longlong_as_double(((long long)raw.w << 32) | raw.z);
+  }
+}
+
+// xor-butterfly reduce-scatter of NV slots (NV a power of two <= 32): lane l
+// ends with the full warp sum of slot l >> (5 - log2 NV).  The pairs added at
+// every level are the butterfly's, so each slot's value equals a plain
+// xor-butterfly all-reduce (addition is commutative).
+template <int NV>
+__device__ __forceinline__ void reduce_scatter_k(double (&v)[NV], int lane) {
+#pragma unroll
+  for (int st = 0; st < 5; ++st) {
+    const int off = 16 >> st;
+    const int cur = NV >> st;
+    if (cur > 1) {
+      const int h = cur >> 1;
+      const bool up = (lane & off) != 0;
+#pragma unroll
+      for (int i = 0; i < h; ++i) {
+        const double send = up ? v[i] : v[i + h];
+        const double keep = up ? v[i + h] : v[i];
+        v[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+      }
+    } else {
+      v[0] = v[0] + __shfl_xor_sync(0xffffffffu, v[0], off);
+    }
+  }
+}
+
+template <int N> struct Log2 { static constexpr int v = 1 + Log2<N / 2>::v; };
+template <> struct Log2<1> { static constexpr int v = 0; };
+
+template <bool B> struct BoolTag { static constexpr bool value = B; };
+
+}  // namespace
+
+template <class Tx, int CC, int NW, int NG, int R, int STAGES, bool FULLG>
+__global__ void __launch_bounds__(NW * 32, 1) k1_stream(FgParams p, int nloc) {
+  constexpr int V = VecK<Tx>::V;
+  constexpr int T1 = NW * 32;
+  constexpr int NV = R * CC;
+  constexpr int LG = Log2<NV>::v;
+  static_assert((NV & (NV - 1)) == 0 && NV <= 32, "R*C must be a power of two <= 32");
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int d = p.d, D = d * CC, ld = p.ld;
+  const int ngroups = (d + V - 1) / V;
+  const int64_t stage_elems = (int64_t)R * ld;
+  Tx* stages = reinterpret_cast<Tx*>(smem);
+  double* red = reinterpret_cast<double*>(smem + (size_t)STAGES * stage_elems * sizeof(Tx));  // [2][NW][NV]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(red + 2 * NW * NV);
+  const Tx* X = reinterpret_cast<const Tx*>(p.X);
+  const unsigned long long nn = (unsigned long long)p.n, SS = (unsigned long long)p.S;
+
+  double wr[NG][V][CC];
+  bool gval[NG];
+#pragma unroll
+  for (int k = 0; k < NG; ++k) {
+    gval[k] = FULLG || (tid + k * T1 < ngroups);
+#pragma unroll
+    for (int q = 0; q < V; ++q)
+#pragma unroll
+      for (int c = 0; c < CC; ++c) {
+        const int j = (tid + k * T1) * V + q;
+        wr[k][q][c] = j < d ? p.w[c * d + j] : 0.0;
+      }
+  }
+  if (tid == 0) {
+#pragma unroll
+    for (int st = 0; st < STAGES; ++st) mbar_init(&bars[st], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  // ---- producer (thread 0): the CTA's tile sequence across its splits ----
+  int ls_p = blockIdx.x;
+  int64_t pt = 0, pr0 = 0, pr1 = 0;
+  if (tid == 0 && ls_p < nloc) {
+    pr0 = (int64_t)(nn * (unsigned long long)(p.split0 + ls_p) / SS);
+    pr1 = (int64_t)(nn * (unsigned long long)(p.split0 + ls_p + 1) / SS);
+  }
+  auto issue = [&](int64_t j) {
+    if (ls_p >= nloc) return;
+    const int st = (int)(j % STAGES);
+    const int64_t row = pr0 + pt * R;
+    const int64_t rows = (pr1 - row) < R ? (pr1 - row) : R;
+    const uint32_t bytes = (uint32_t)(rows * ld * (int64_t)sizeof(Tx));
+    mbar_expect_tx(&bars[st], bytes);
+    bulk_g2s(stages + st * stage_elems, X + row * ld, bytes, &bars[st]);
+    if (row + R >= pr1) {
+      ls_p += gridDim.x;
+      pt = 0;
+      if (ls_p < nloc) {
+        pr0 = (int64_t)(nn * (unsigned long long)(p.split0 + ls_p) / SS);
+        pr1 = (int64_t)(nn * (unsigned long long)(p.split0 + ls_p + 1) / SS);
+      }
+    } else {
+      ++pt;
+    }
+  };
+  if (tid == 0)
+#pragma unroll 1
+    for (int j = 0; j < STAGES; ++j) issue(j);
+
+  // lane (fr, fc) = (row, class) of the loss-derivative slot it evaluates
+  const int fr = lane / CC, fc = lane % CC;
+  int64_t jseq = 0;  // consumer position in the CTA's tile sequence
+
+#pragma unroll 1
+  for (int ls = blockIdx.x; ls < nloc; ls += gridDim.x) {
+    const int64_t r0 = (int64_t)(nn * (unsigned long long)(p.split0 + ls) / SS);
+    const int64_t r1 = (int64_t)(nn * (unsigned long long)(p.split0 + ls + 1) / SS);
+    const int64_t ntile = (r1 - r0 + R - 1) / R;
+    double gacc[NG][V][CC];
+#pragma unroll
+    for (int k = 0; k < NG; ++k)
+#pragma unroll
+      for (int q = 0; q < V; ++q)
+#pragma unroll
+        for (int c = 0; c < CC; ++c) gacc[k][q][c] = 0.0;
+    double la = 0.0;
+    // targets of the slot rows, one tile ahead
+    double tgt = 0.0;
+    if (lane < NV && r0 + fr < r1) tgt = CC == 1 ? p.y[r0 + fr] : (double)p.labels[r0 + fr];
+
+#pragma unroll 1
+    for (int64_t i = 0; i < ntile; ++i, ++jseq) {
+      const int64_t rowb = r0 + i * R;
+      const int nr = (int)((r1 - rowb) < R ? (r1 - rowb) : R);
+      const double tcur = tgt;
+      if (lane < NV && rowb + R + fr < r1)
+        tgt = CC == 1 ? p.y[rowb + R + fr] : (double)p.labels[rowb + R + fr];
+      const int st = (int)(jseq % STAGES);
+      mbar_wait(&bars[st], (uint32_t)((jseq / STAGES) & 1));
+      const Tx* xs = stages + st * stage_elems;
+      double* rb = red + (jseq & 1) * (NW * NV);
+
+      auto body = [&](auto full_tag) {
+        constexpr bool FULL = decltype(full_tag)::value;
+        double xr[R][NG][V];
+        double acc[NV];
+#pragma unroll
+        for (int v = 0; v < NV; ++v) acc[v] = 0.0;
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+#pragma unroll
+          for (int k = 0; k < NG; ++k) {
+            if ((FULL || r < nr) && gval[k]) {
+              load_group_k<Tx>(xs + (int64_t)r * ld + (tid + k * T1) * V, xr[r][k]);
+            } else {
+#pragma unroll
+              for (int q = 0; q < V; ++q) xr[r][k][q] = 0.0;
+            }
+          }
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+#pragma unroll
+          for (int k = 0; k < NG; ++k)
+#pragma unroll
+            for (int q = 0; q < V; ++q)
+#pragma unroll
+              for (int c = 0; c < CC; ++c) acc[r * CC + c] = fma(xr[r][k][q], wr[k][q][c], acc[r * CC + c]);
+        reduce_scatter_k<NV>(acc, lane);
+        if ((lane & ((32 >> LG) - 1)) == 0) rb[wid * NV + (lane >> (5 - LG))] = acc[0];
+        __syncthreads();
+        // every thread's x slice is in registers: the stage can be refilled
+        if (tid == 0) issue(jseq + STAGES);
+
+        // logit of slot (fr, fc): the NW warp partials summed in warp order
+        double lg = 0.0;
+        if (lane < NV) {
+          double pv[NW];
+#pragma unroll
+          for (int w2 = 0; w2 < NW; ++w2) pv[w2] = rb[w2 * NV + lane];
+          lg = pv[0];
+#pragma unroll
+          for (int w2 = 1; w2 < NW; ++w2) lg = lg + pv[w2];
+        }
+        double pr, lt = 0.0;
+        if constexpr (CC == 1) {
+          pr = lg - tcur;
+          lt = __dmul_rn(__dmul_rn(0.5, pr), pr);
+        } else {
+          const int lab = (int)tcur;
+          const int base = (fr * CC) & 31;
+          double mx = 0.0;
+#pragma unroll
+          for (int c = 0; c < CC; ++c) {
+            const double v = __shfl_sync(0xffffffffu, lg, (base + c) & 31);
+            mx = c == 0 ? v : (v > mx ? v : mx);
+          }
+          const double e = hexp(lg - mx);
+          double ssum = __shfl_sync(0xffffffffu, e, base);
+#pragma unroll
+          for (int c = 1; c < CC; ++c) ssum = ssum + __shfl_sync(0xffffffffu, e, (base + c) & 31);
+          const double lab_logit = __shfl_sync(0xffffffffu, lg, (base + lab) & 31);
+          pr = e / ssum;
+          if (fc == lab) pr = pr - 1.0;
+          if (wid == 0 && fc == 0 && lane < NV) lt = (mx + hlog(ssum)) - lab_logit;
+        }
+        double dlr[NV];
+#pragma unroll
+        for (int v = 0; v < NV; ++v) dlr[v] = __shfl_sync(0xffffffffu, pr, v);
+        if (wid == 0) {
+#pragma unroll
+          for (int r = 0; r < R; ++r) {
+            const double t = __shfl_sync(0xffffffffu, lt, r * CC);
+            if (FULL || r < nr) la = la + t;
+          }
+        }
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          if (FULL || r < nr) {
+#pragma unroll
+            for (int k = 0; k < NG; ++k)
+#pragma unroll
+              for (int q = 0; q < V; ++q)
+#pragma unroll
+                for (int c = 0; c < CC; ++c) gacc[k][q][c] = fma(dlr[r * CC + c], xr[r][k][q], gacc[k][q][c]);
+          }
+        }
+      };
+      if (nr == R) body(BoolTag<true>{});
+      else body(BoolTag<false>{});
+    }
+
+    double* out = p.partials + (size_t)ls * (D + 1);
+#pragma unroll
+    for (int k = 0; k < NG; ++k) {
+      const int g = tid + k * T1;
+      if (gval[k]) {
+#pragma unroll
+        for (int q = 0; q < V; ++q) {
+          const int j = g * V + q;
+          if (j < d)
+#pragma unroll
+            for (int c = 0; c < CC; ++c) out[(size_t)c * d + j] = gacc[k][q][c];
+        }
+      }
+    }
+    if (tid == 0) out[D] = la;
+  }
+}
+
+// ------------------------------------------------------------------ dispatch
+size_t stream_smem_bytes(int ld, int elem, int warps, int R, int CC, int stages) {
+  size_t b = (size_t)stages * R * ld * elem;
+  b = (b + 15) / 16 * 16;
+  b += (size_t)2 * warps * R * CC * 8 + (size_t)stages * 8;
+  return b;
+}
+
+namespace {
+
+template <class Tx, int CC, int NW, int NG, int R, int STAGES, bool FULLG>
+cudaError_t launch_stream_k(const FgLaunch& L, const FgParams& p, cudaStream_t st) {
+  auto kern = k1_stream<Tx, CC, NW, NG, R, STAGES, FULLG>;
+  const size_t smem = stream_smem_bytes(L.ld, (int)sizeof(Tx), NW, R, CC, STAGES);
+  if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  int dev = 0, sms = 0, per_sm = 0;
+  if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
+  if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
+  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NW * 32, smem)) != cudaSuccess) return e;
+  if (per_sm < 1) return cudaErrorInvalidConfiguration;
+  int grid = sms * per_sm;
+  if (grid > L.nsplit_local) grid = L.nsplit_local;
+  kern<<<grid, NW * 32, smem, st>>>(p, L.nsplit_local);
+  return cudaGetLastError();
+}
+
+template <class Tx, int CC, int NW, int NG, int R, int STAGES>
+cudaError_t launch_stream_f(const FgLaunch& L, const FgParams& p, cudaStream_t st) {
+  constexpr int V = VecK<Tx>::V;
+  const bool fullg = ((p.d + V - 1) / V) == NG * NW * 32;
+  if (fullg) return launch_stream_k<Tx, CC, NW, NG, R, STAGES, true>(L, p, st);
+  return launch_stream_k<Tx, CC, NW, NG, R, STAGES, false>(L, p, st);
+}
+
+// planned shapes (plan_for): key = NW*10000 + NG*1000 + R*10 + STAGES
+template <class Tx, int CC>
+cudaError_t launch_stream_cc(const FgLaunch& L, const FgParams& p, cudaStream_t st) {
+  const int nw = L.threads / 32;
+  switch (nw * 10000 + L.ng * 1000 + L.rows * 10 + L.stages) {
+#define HALP_STREAM_CASE(NW, NG, R, ST) \
+  case NW * 10000 + NG * 1000 + R * 10 + ST: return launch_stream_f<Tx, CC, NW, NG, R, ST>(L, p, st);
+    HALP_STREAM_SHAPES(HALP_STREAM_CASE)
+#undef HALP_STREAM_CASE
+    default: return cudaErrorInvalidConfiguration;
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_fullgrad_stream(const FgLaunch& L, const FgParams& p, cudaStream_t st) {
+  switch (L.dtype * 10 + p.C) {
+    case 1: return launch_stream_cc<double, 1>(L, p, st);
+    case 2: return launch_stream_cc<double, 2>(L, p, st);
+    case 11: return launch_stream_cc<float, 1>(L, p, st);
+    case 12: return launch_stream_cc<float, 2>(L, p, st);
+    case 21: return launch_stream_cc<__nv_bfloat16, 1>(L, p, st);
+    case 22: return launch_stream_cc<__nv_bfloat16, 2>(L, p, st);
+    default: return cudaErrorInvalidConfiguration;
+  }
+}
+
+}  // namespace halp

@@ -22,7 +22,7 @@ struct FgParams {
 };
 struct FgLaunch {
   int dtype, ng, ct, threads, ld, nsplit_local;
-  int fast, rows, stages;  // fast: 1/2 register-resident paths for C <= 2, 3 softmax C >= 3; rows per tile, ring depth
+  int fast, rows, stages;  // fast: 1/2 register-resident paths for C <= 2, 3 softmax C >= 3, 4 streaming C <= 2; rows per tile, ring depth
 };
 size_t fg_smem_bytes(int ld, int elem, int D, int C, int threads, int R, int stages);
 size_t fast_smem_bytes(int ld, int elem, int threads, int R, int CC, int stages);
@@ -30,6 +30,15 @@ cudaError_t launch_fullgrad(const FgLaunch& L, const FgParams& p, cudaStream_t s
 // softmax with 3..15 classes (FgLaunch.fast == 3), k_fullgrad_smx.cu
 size_t smx_smem_bytes(int ld, int elem, int d, int C, int threads, int64_t split_rows);
 cudaError_t launch_fullgrad_smx(const FgLaunch& L, const FgParams& p, cudaStream_t st);
+// streaming kernel for C <= 2 (FgLaunch.fast == 4), k_fullgrad_stream.cu.
+// Instantiated shapes (NW warps, NG groups/thread, R rows/tile, ring depth);
+// plan_for only picks shapes from this list.
+#define HALP_STREAM_SHAPES(X) \
+  X(1, 1, 4, 4) X(1, 1, 8, 4) X(2, 1, 4, 4) X(2, 1, 8, 4) X(4, 1, 4, 4) X(4, 1, 8, 4) X(8, 1, 2, 4) \
+  X(8, 1, 4, 4) X(16, 1, 2, 4) X(16, 1, 4, 4) X(8, 2, 2, 4) X(16, 2, 1, 4) X(16, 2, 2, 4) X(8, 4, 1, 4) \
+  X(8, 4, 2, 4) X(16, 4, 1, 4) X(16, 2, 2, 6) X(8, 2, 2, 6) X(8, 4, 2, 6) X(4, 1, 4, 6)
+size_t stream_smem_bytes(int ld, int elem, int warps, int R, int CC, int stages);
+cudaError_t launch_fullgrad_stream(const FgLaunch& L, const FgParams& p, cudaStream_t st);
 cudaError_t launch_split_tree(const double* partials, int nsplit, int D1, double* out, double* scratch,
                               cudaStream_t st);
 
