@@ -345,7 +345,7 @@ def main():
             traffic = tj["dram_read_bytes_per_launch"] + tj["dram_write_bytes_per_launch"]
         except Exception:
             pass
-        roofline = {"kernel": "k1_reg (+k1_tree_pass), C3 full-gradient pass", "bound": "hbm",
+        roofline = {"kernel": "k1_stream (+k1_tree_pass), C3 full-gradient pass", "bound": "hbm",
                     "achieved": c3["GB_per_s"] / world, "peak": pk["hbm_gbs"], "unit": "GB/s",
                     "frac": c3["GB_per_s"] / world / pk["hbm_gbs"], "traffic": traffic,
                     "traffic_source": "profiles/k1_traffic.json (ncu dram__bytes_read+write per launch)",

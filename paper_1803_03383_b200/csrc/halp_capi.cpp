@@ -123,6 +123,59 @@ uint64_t fnv1a(const double* v, int64_t len) {  // optimizers.cpp:218-227
   return h;
 }
 
+// ---- device memory: the device's stream-ordered pool, never trimmed ----
+// Problems are created and destroyed per solve (run_prepared, sweeps, the e2e
+// path); keeping freed blocks in the pool makes that O(1) instead of a
+// cudaMalloc/cudaFree (and page-table work) per solve.
+int pool_setup(int device) {
+  static bool done[64] = {};
+  if (device < 0 || device >= 64) return HALP_INVALID_INPUT;
+  if (done[device]) return HALP_OK;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) != cudaSuccess) return HALP_CUDA_ERROR;
+  uint64_t keep = UINT64_MAX;
+  if (cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep) != cudaSuccess) return HALP_CUDA_ERROR;
+  done[device] = true;
+  return HALP_OK;
+}
+template <class T>
+cudaError_t dalloc(T** ptr, size_t bytes, cudaStream_t st) {
+  return cudaMallocAsync(reinterpret_cast<void**>(ptr), std::max<size_t>(bytes, 16), st);
+}
+
+// RNG jump tables, uploaded once per device and kept resident: the 64
+// power tables X^(2^b) (1 MiB) and, per epoch length D, the X^D table (16 KiB)
+struct RngTables {
+  const uint64_t* pow_tab = nullptr;
+  std::vector<std::pair<int64_t, const uint64_t*>> jump;  // (D, table)
+};
+int rng_tables(int device, int64_t D, const uint64_t** pow_tab, const uint64_t** jump_tab) {
+  static RngTables per_dev[64];
+  if (device < 0 || device >= 64) return fail(HALP_INVALID_INPUT, "device index out of range");
+  RngTables& t = per_dev[device];
+  const auto& jt = JumpTables::get();
+  if (!t.pow_tab) {
+    uint64_t* d = nullptr;
+    CU(cudaMalloc(&d, sizeof(uint64_t) * jt.flat.size()));
+    CU(cudaMemcpy(d, jt.flat.data(), sizeof(uint64_t) * jt.flat.size(), cudaMemcpyHostToDevice));
+    t.pow_tab = d;
+  }
+  *pow_tab = t.pow_tab;
+  for (const auto& e : t.jump)
+    if (e.first == D) {
+      *jump_tab = e.second;
+      return HALP_OK;
+    }
+  std::vector<uint64_t> tab(2048);
+  mat_tables(jt.power((uint64_t)D), tab.data());
+  uint64_t* d = nullptr;
+  CU(cudaMalloc(&d, sizeof(uint64_t) * 2048));
+  CU(cudaMemcpy(d, tab.data(), sizeof(uint64_t) * 2048, cudaMemcpyHostToDevice));
+  t.jump.emplace_back(D, d);
+  *jump_tab = d;
+  return HALP_OK;
+}
+
 }  // namespace
 
 struct halp_problem {
@@ -150,7 +203,7 @@ struct halp_problem {
   int64_t idx_cap = 0;
   long long* codes = nullptr;
   int* blow = nullptr;
-  uint64_t *pow_tab = nullptr, *jump_tab = nullptr;
+  const uint64_t *pow_tab = nullptr, *jump_tab = nullptr;  // resident per device (rng_tables)
   long long* trace_dev = nullptr;
   int64_t trace_dev_steps = 0;
   int64_t* trace_host = nullptr;
@@ -161,11 +214,12 @@ struct halp_problem {
 
   ~halp_problem() {
     cudaSetDevice(device);
+    // stream-ordered frees back into the device pool (no device-wide sync)
     for (void* ptr : {(void*)w, (void*)w2, (void*)g, (void*)partials, (void*)rank_sum, (void*)gathered, (void*)stats,
-                      (void*)u_out, (void*)idx, (void*)codes, (void*)blow, (void*)pow_tab, (void*)jump_tab,
-                      (void*)trace_dev, (void*)y, (void*)labels, (void*)tree_scratch})
-      if (ptr) cudaFree(ptr);
-    if (own_X && X) cudaFree(X);
+                      (void*)u_out, (void*)idx, (void*)codes, (void*)blow, (void*)trace_dev, (void*)y,
+                      (void*)labels, (void*)tree_scratch})
+      if (ptr) cudaFreeAsync(ptr, stream);
+    if (own_X && X) cudaFreeAsync(X, stream);
     if (comm) Nccl::get().commDestroy(comm);
     if (stream) cudaStreamDestroy(stream);
   }
@@ -333,24 +387,20 @@ int ensure_workspace(halp_problem* p) {
   const int64_t D1 = p->D + 1;
   const int64_t nloc = p->sp.split_end - p->sp.split_begin;
   if (!p->w) {
-    CU(cudaMalloc(&p->w, sizeof(double) * p->D));
-    CU(cudaMalloc(&p->w2, sizeof(double) * p->D));
-    CU(cudaMalloc(&p->g, sizeof(double) * p->D));
-    CU(cudaMalloc(&p->u_out, sizeof(double) * p->D));
-    CU(cudaMalloc(&p->partials, sizeof(double) * D1 * nloc));
-    CU(cudaMalloc(&p->tree_scratch, sizeof(double) * D1 * std::max<int64_t>(1, nloc / 64)));
-    CU(cudaMalloc(&p->rank_sum, sizeof(double) * D1));
-    CU(cudaMalloc(&p->gathered, sizeof(double) * D1 * p->world));
-    CU(cudaMalloc(&p->stats, sizeof(double) * 4));
-    CU(cudaMalloc(&p->codes, sizeof(long long) * p->D));
-    CU(cudaMalloc(&p->blow, sizeof(int)));
-    const auto& jt = JumpTables::get();
-    CU(cudaMalloc(&p->pow_tab, sizeof(uint64_t) * jt.flat.size()));
-    CU(cudaMemcpy(p->pow_tab, jt.flat.data(), sizeof(uint64_t) * jt.flat.size(), cudaMemcpyHostToDevice));
-    std::vector<uint64_t> tab(2048);
-    mat_tables(jt.power((uint64_t)p->D), tab.data());
-    CU(cudaMalloc(&p->jump_tab, sizeof(uint64_t) * 2048));
-    CU(cudaMemcpy(p->jump_tab, tab.data(), sizeof(uint64_t) * 2048, cudaMemcpyHostToDevice));
+    cudaStream_t st = p->stream;
+    CU(dalloc(&p->w, sizeof(double) * p->D, st));
+    CU(dalloc(&p->w2, sizeof(double) * p->D, st));
+    CU(dalloc(&p->g, sizeof(double) * p->D, st));
+    CU(dalloc(&p->u_out, sizeof(double) * p->D, st));
+    CU(dalloc(&p->partials, sizeof(double) * D1 * nloc, st));
+    CU(dalloc(&p->tree_scratch, sizeof(double) * D1 * std::max<int64_t>(1, nloc / 64), st));
+    CU(dalloc(&p->rank_sum, sizeof(double) * D1, st));
+    CU(dalloc(&p->gathered, sizeof(double) * D1 * p->world, st));
+    CU(dalloc(&p->stats, sizeof(double) * 4, st));
+    CU(dalloc(&p->codes, sizeof(long long) * p->D, st));
+    CU(dalloc(&p->blow, sizeof(int), st));
+    int rc = rng_tables(p->device, p->D, &p->pow_tab, &p->jump_tab);
+    if (rc) return rc;
     CU(cudaEventCreate(&p->ev_fg.a));
     CU(cudaEventCreate(&p->ev_fg.b));
     CU(cudaEventCreate(&p->ev_fin.a));
@@ -525,10 +575,12 @@ int halp_problem_create(const halp_problem_desc* desc, halp_problem** out) {
   cudaError_t ce = cudaGetDeviceCount(&ndev);
   if (ce != cudaSuccess || ndev == 0)
     return fail(HALP_CUDA_ERROR, std::string("no CUDA device (no CPU fallback): ") + cudaGetErrorString(ce));
+  if (desc->device < 0 || desc->device >= ndev) return fail(HALP_INVALID_INPUT, "device index out of range");
   CU(cudaSetDevice(desc->device));
-  cudaDeviceProp prop;
-  CU(cudaGetDeviceProperties(&prop, desc->device));
-  if (prop.major != 10) return fail(HALP_CUDA_ERROR, "libhalp_b200 is built for sm_100a (B200) only");
+  int major = 0;
+  CU(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, desc->device));
+  if (major != 10) return fail(HALP_CUDA_ERROR, "libhalp_b200 is built for sm_100a (B200) only");
+  if (pool_setup(desc->device)) return fail(HALP_CUDA_ERROR, "cannot configure the device memory pool");
 
   auto* p = new halp_problem();
   p->device = desc->device;
@@ -557,33 +609,41 @@ int halp_problem_create(const halp_problem_desc* desc, halp_problem** out) {
     p->own_X = false;
   } else {
     const size_t bytes = (size_t)p->n * p->ld * es;
-    if (cudaMalloc(&p->X, bytes) != cudaSuccess) return bail(fail(HALP_CUDA_ERROR, "cudaMalloc(X) failed"));
+    if (dalloc(&p->X, bytes, p->stream) != cudaSuccess) return bail(fail(HALP_CUDA_ERROR, "cudaMallocAsync(X) failed"));
     p->own_X = true;
     // padding columns must be zero: kernels process whole 16-byte groups
-    if (p->ld != p->d && cudaMemset(p->X, 0, bytes) != cudaSuccess)
+    if (p->ld != p->d && cudaMemsetAsync(p->X, 0, bytes, p->stream) != cudaSuccess)
       return bail(fail(HALP_CUDA_ERROR, "cudaMemset(X) failed"));
-    if (cudaMemcpy2D(p->X, (size_t)p->ld * es, desc->X, (size_t)p->d * es, (size_t)p->d * es, (size_t)p->n,
-                     dev_in ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice) != cudaSuccess)
+    // async on the problem's stream (a DMA straight from pinned host memory)
+    if (cudaMemcpy2DAsync(p->X, (size_t)p->ld * es, desc->X, (size_t)p->d * es, (size_t)p->d * es, (size_t)p->n,
+                          dev_in ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, p->stream) != cudaSuccess)
       return bail(fail(HALP_CUDA_ERROR, "copy of X to the device failed"));
     if (!dev_in) p->create_h2d += (int64_t)p->n * p->d * es;
   }
   if (p->loss == HALP_SQUARED) {
-    if (cudaMalloc(&p->y, sizeof(double) * p->n) != cudaSuccess) return bail(fail(HALP_CUDA_ERROR, "cudaMalloc(y)"));
-    if (cudaMemcpy(p->y, desc->y, sizeof(double) * p->n, dev_in ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice) !=
-        cudaSuccess)
+    if (dalloc(&p->y, sizeof(double) * p->n, p->stream) != cudaSuccess) return bail(fail(HALP_CUDA_ERROR, "cudaMallocAsync(y)"));
+    if (cudaMemcpyAsync(p->y, desc->y, sizeof(double) * p->n, dev_in ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                        p->stream) != cudaSuccess)
       return bail(fail(HALP_CUDA_ERROR, "copy of y failed"));
     if (!dev_in) p->create_h2d += (int64_t)p->n * 8;
   } else {
-    std::vector<int32_t> lab(p->n);
-    if (cudaMemcpy(lab.data(), desc->labels, sizeof(int32_t) * p->n,
-                   dev_in ? cudaMemcpyDeviceToHost : cudaMemcpyHostToHost) != cudaSuccess)
+    // Objective ctor: every label in [0, C) (objectives.cpp:150-153); host labels are checked in place
+    std::vector<int32_t> lab;
+    const int32_t* lh = static_cast<const int32_t*>(desc->labels);
+    if (dev_in) {
+      lab.resize(p->n);
+      if (cudaMemcpy(lab.data(), desc->labels, sizeof(int32_t) * p->n, cudaMemcpyDeviceToHost) != cudaSuccess)
+        return bail(fail(HALP_CUDA_ERROR, "copy of labels failed"));
+      lh = lab.data();
+    }
+    for (int64_t i = 0; i < p->n; ++i)
+      if (lh[i] < 0 || lh[i] >= C) return bail(fail(HALP_INVALID_INPUT, "Objective: label outside [0, num_classes)"));
+    if (dalloc(&p->labels, sizeof(int32_t) * p->n, p->stream) != cudaSuccess)
+      return bail(fail(HALP_CUDA_ERROR, "cudaMallocAsync(labels)"));
+    if (cudaMemcpyAsync(p->labels, desc->labels, sizeof(int32_t) * p->n,
+                        dev_in ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, p->stream) != cudaSuccess)
       return bail(fail(HALP_CUDA_ERROR, "copy of labels failed"));
-    for (int32_t v : lab)
-      if (v < 0 || v >= C) return bail(fail(HALP_INVALID_INPUT, "Objective: label outside [0, num_classes)"));
-    if (cudaMalloc(&p->labels, sizeof(int32_t) * p->n) != cudaSuccess) return bail(fail(HALP_CUDA_ERROR, "cudaMalloc(labels)"));
-    if (cudaMemcpy(p->labels, lab.data(), sizeof(int32_t) * p->n, cudaMemcpyHostToDevice) != cudaSuccess)
-      return bail(fail(HALP_CUDA_ERROR, "copy of labels failed"));
-    p->create_h2d += (int64_t)p->n * 4;
+    if (!dev_in) p->create_h2d += (int64_t)p->n * 4;
   }
   p->sp = make_shard_plan(p->n, p->d, C, p->dtype, world, p->rank);
   int rc = choose_plans(p);
@@ -598,6 +658,8 @@ int halp_problem_create(const halp_problem_desc* desc, halp_problem** out) {
   }
   rc = ensure_workspace(p);
   if (rc) return bail(rc);
+  // the caller may release its host buffers when create returns
+  if (cudaStreamSynchronize(p->stream) != cudaSuccess) return bail(fail(HALP_CUDA_ERROR, "upload of the dataset failed"));
   p->timing.h2d_bytes = p->create_h2d;
   *out = p;
   return HALP_OK;
@@ -687,8 +749,8 @@ int halp_run(halp_problem* p, const halp_config* cfg, halp_record* rec) {
   const int opt2 = cfg->option == 1;
   p->timing = halp_timing{};
   if (p->idx_cap < T) {
-    if (p->idx) cudaFree(p->idx);
-    CU(cudaMalloc(&p->idx, sizeof(int64_t) * T));
+    if (p->idx) cudaFreeAsync(p->idx, p->stream);
+    CU(dalloc(&p->idx, sizeof(int64_t) * T, p->stream));
     p->idx_cap = T;
   }
   std::vector<double> wh(D, 0.0);
@@ -700,8 +762,8 @@ int halp_run(halp_problem* p, const halp_config* cfg, halp_record* rec) {
   int64_t traced = 0;
   int64_t tr_steps = p->trace_cap > 0 ? std::min<int64_t>(T, p->trace_cap / D) : 0;
   if (tr_steps > p->trace_dev_steps) {
-    if (p->trace_dev) cudaFree(p->trace_dev);
-    CU(cudaMalloc(&p->trace_dev, sizeof(long long) * tr_steps * D));
+    if (p->trace_dev) cudaFreeAsync(p->trace_dev, p->stream);
+    CU(dalloc(&p->trace_dev, sizeof(long long) * tr_steps * D, p->stream));
     p->trace_dev_steps = tr_steps;
   }
 
