@@ -521,6 +521,24 @@ static void mirror_softmax_dl_k3(double* l, int C, int label) {
   l[label] = l[label] - 1.0;
 }
 
+/* Two-class softmax in K1 (k_fullgrad_stream.cu): the logits enter only
+ * through s = x.(w1 - w0), so K1 makes ONE dot per row with v = w1 - w0
+ * (IEEE differences) and evaluates
+ *   q = exp(-|s|), den = 1 + q, p0 = (s > 0 ? q : 1) / den,
+ *   dl0 = p0 - [y == 0], dl1 = -dl0,
+ *   loss = max(a, 0) + log(den),  a = s (y == 0) or -s (y == 1),
+ * the reference's softmax rows (objectives.cpp:206-217, :277-283) for C = 2
+ * up to rounding (tests: MIRROR vs REF within 1e-12).  The class-1 gradient
+ * column is the exact negation of class 0's.  Returns the loss term. */
+static double mirror_logistic_row(double s, int label, double* dl0) {
+  const double q = oq_mexp(-fabs(s));
+  const double den = 1.0 + q;
+  const double p0 = (s > 0.0 ? q : 1.0) / den;
+  *dl0 = label == 0 ? p0 - 1.0 : p0;
+  const double a = label == 0 ? s : -s;
+  return (a > 0.0 ? a : 0.0) + oq_mlog(den);
+}
+
 /* pairwise tree over n items (split at the largest power of two < n) */
 static double tree_sum(const double* v, int64_t stride, int64_t n) {
   if (n == 1) return v[0];
@@ -541,6 +559,9 @@ static void mirror_fullpass(const oq_objective* o, const double* w, const oq_pla
   double* part = (double*)calloc((size_t)S * D, sizeof(double));
   double* lpart = (double*)calloc((size_t)S, sizeof(double));
   double* x = (double*)malloc(sizeof(double) * (size_t)d);
+  double* vdiff = (double*)malloc(sizeof(double) * (size_t)d);
+  if (C == 2)
+    for (int j = 0; j < d; ++j) vdiff[j] = w[d + j] - w[j];
   double lg[64];
   for (int s = 0; s < S; ++s) {
     const int64_t r0 = (int64_t)((__int128)n * s / S), r1 = (int64_t)((__int128)n * (s + 1) / S);
@@ -548,6 +569,13 @@ static void mirror_fullpass(const oq_objective* o, const double* w, const oq_pla
     double la = 0.0;
     for (int64_t r = r0; r < r1; ++r) {
       load_row(o, r, x);
+      if (C == 2) { /* two classes: the logistic form of K1 */
+        const double sd = mirror_fg_dot(x, vdiff, d, pl->fg_threads, pl->fg_vec);
+        double dl0;
+        la = la + mirror_logistic_row(sd, o->labels[r], &dl0);
+        for (int j = 0; j < d; ++j) ps[j] = fma(dl0, x[j], ps[j]);
+        continue;
+      }
       for (int c = 0; c < C; ++c) lg[c] = mirror_fg_dot(x, w + (size_t)c * d, d, pl->fg_threads, pl->fg_vec);
       if (o->loss == OQ_SQUARED) {
         const double e = lg[0] - o->y[r];
@@ -561,6 +589,8 @@ static void mirror_fullpass(const oq_objective* o, const double* w, const oq_pla
           for (int j = 0; j < d; ++j) ps[(size_t)c * d + j] = fma(lg[c], x[j], ps[(size_t)c * d + j]);
       }
     }
+    if (C == 2)
+      for (int j = 0; j < d; ++j) ps[d + j] = -ps[j];
     lpart[s] = la;
   }
   for (int k = 0; k < D; ++k) {
@@ -584,6 +614,7 @@ static void mirror_fullpass(const oq_objective* o, const double* w, const oq_pla
   free(part);
   free(lpart);
   free(x);
+  free(vdiff);
 }
 
 /* Root of the pairwise split tree over splits [s0, s1) in MIRROR order:
@@ -597,6 +628,9 @@ int oq_split_subtree(const oq_objective* o, const double* w, const oq_plan* pl, 
   const int64_t ns = s1 - s0;
   double* part = (double*)calloc((size_t)ns * (D + 1), sizeof(double));
   double* x = (double*)malloc(sizeof(double) * (size_t)d);
+  double* vdiff = (double*)malloc(sizeof(double) * (size_t)d);
+  if (C == 2)
+    for (int j = 0; j < d; ++j) vdiff[j] = w[d + j] - w[j];
   double lg[64];
   for (int64_t s = s0; s < s1; ++s) {
     const int64_t r0 = (int64_t)((__int128)n * s / S), r1 = (int64_t)((__int128)n * (s + 1) / S);
@@ -604,6 +638,13 @@ int oq_split_subtree(const oq_objective* o, const double* w, const oq_plan* pl, 
     double la = 0.0;
     for (int64_t r = r0; r < r1; ++r) {
       load_row(o, r, x);
+      if (C == 2) { /* two classes: the logistic form of K1 */
+        const double sd = mirror_fg_dot(x, vdiff, d, pl->fg_threads, pl->fg_vec);
+        double dl0;
+        la = la + mirror_logistic_row(sd, o->labels[r], &dl0);
+        for (int j = 0; j < d; ++j) ps[j] = fma(dl0, x[j], ps[j]);
+        continue;
+      }
       for (int c = 0; c < C; ++c) lg[c] = mirror_fg_dot(x, w + (size_t)c * d, d, pl->fg_threads, pl->fg_vec);
       if (o->loss == OQ_SQUARED) {
         const double e = lg[0] - o->y[r];
@@ -617,11 +658,14 @@ int oq_split_subtree(const oq_objective* o, const double* w, const oq_plan* pl, 
           for (int j = 0; j < d; ++j) ps[(size_t)c * d + j] = fma(lg[c], x[j], ps[(size_t)c * d + j]);
       }
     }
+    if (C == 2)
+      for (int j = 0; j < d; ++j) ps[d + j] = -ps[j];
     ps[D] = la;
   }
   for (int k = 0; k <= D; ++k) out[k] = tree_sum(part + k, D + 1, ns);
   free(part);
   free(x);
+  free(vdiff);
   return OQ_OK;
 }
 

@@ -264,8 +264,9 @@ bool plan_stream(int d, int C, int dtype, FgLaunch* out) {
   if (R <= 0) {
     R = 8;
     const int reg_cap = std::min(255, 65536 / T1);
-    auto regs = [&](int r) { return 2 * (r * NG * V + 2 * NG * V * C + r * C) + 48; };
-    while (R > 1 && (R * C > 16 || R * NG * V > 32 || regs(R) > reg_cap || (int64_t)R * row_bytes > 32 * 1024 ||
+    // one effective column for both losses (two classes: the logistic form)
+    auto regs = [&](int r) { return 2 * (r * NG * V + 2 * NG * V + r) + 48; };
+    while (R > 1 && (R * NG * V > 64 || regs(R) > reg_cap || (int64_t)R * row_bytes > 32 * 1024 ||
                      !stream_shape_ok(T1 / 32, NG, R, stages)))
       R /= 2;
   }
@@ -290,41 +291,18 @@ int plan_for(int64_t n, int d, int C, int dtype, KernelPlan* kp) {
   if (CT > C) CT = (int)next_pow2(C);
   kp->fg = FgLaunch{dtype, NG, CT, T1, ld, 0, 0, 2, 4};
   kp->fg_passes = (C + CT - 1) / CT;
-  // fast register-resident path: C <= 2 and the iterate slice fits in registers
-  if (C <= 2 && NG * V * C <= 32 && env_int("HALP_FG_GENERIC", 0) == 0) {
-    const int row_bytes = ld * es;
-    int R = 1;  // rows per tile: tiles of <= 16 KB, at most 8 rows, <= 32 reduction slots
-    while (R < 8 && R * 2 * row_bytes <= 16 * 1024 && R * 2 * C <= 32 && NG * R * 2 <= 8) R *= 2;
-    if (env_int("HALP_FG_ROWS", 0) > 0) R = (int)env_int("HALP_FG_ROWS", 0);
-    int stages = 6;
-    if (fast_smem_bytes(ld, es, T1, R, C, stages) > 110 * 1024) stages = 3;
-    if (env_int("HALP_FG_STAGES", 0) > 0) stages = (int)env_int("HALP_FG_STAGES", 0);
-    kp->fg.fast = 1;
-    kp->fg.rows = R;
-    kp->fg.stages = stages;
-    kp->fg_passes = 1;
-    // register-tile kernel (default; up to 512-thread CTAs, x converted once per tile)
-    if (env_int("HALP_FG_KERNEL", 2) == 2) {
-      const int T2 = (int)std::min<int64_t>(512, (ngroups + 31) / 32 * 32);
-      const int NG2 = (int)next_pow2((ngroups + T2 - 1) / T2);
-      int R2 = (int)env_int("HALP_FG_ROWS", 0);
-      if (R2 <= 0) {
-        R2 = 1;
-        while (R2 < 8 && R2 * 2 * row_bytes <= 32 * 1024 && R2 * 2 * C <= 32 && NG2 * V * R2 * 2 <= 32) R2 *= 2;
-      }
-      const int64_t S_ = make_shard_plan(n, d, C, dtype, 1, 0).S;
-      const int64_t split_rows = (n + S_ - 1) / S_ + 1;  // targets staged in shared memory
-      const size_t smem2 = (size_t)4 * R2 * ld * es + 2 * (size_t)(T2 / 32) * R2 * C * 8 + 32 + 8 * split_rows;
-      if (NG2 * V * C <= 32 && NG2 <= 4 && smem2 <= 200 * 1024) kp->fg = FgLaunch{dtype, NG2, CT, T2, ld, 0, 2, R2, 4};
-    }
-  }
-  // persistent streaming kernel (default for C <= 2)
-  if (C <= 2 && env_int("HALP_FG_GENERIC", 0) == 0 && env_int("HALP_FG_KERNEL", 4) == 4) {
+  // persistent streaming kernel (C <= 2; HALP_FG_GENERIC=1 forces the generic kernel for least squares)
+  if (C <= 2 && env_int("HALP_FG_GENERIC", 0) == 0) {
     FgLaunch fl;
     if (plan_stream(d, C, dtype, &fl)) {
       kp->fg = fl;
       kp->fg_passes = 1;
+    } else if (C == 2) {
+      // the two-class logistic form (MIRROR order) exists only in the streaming kernel
+      return fail(HALP_UNSUPPORTED, "full_gradient: two-class rows wider than the streaming kernel's register tiles");
     }
+  } else if (C == 2) {
+    return fail(HALP_UNSUPPORTED, "full_gradient: two-class objectives need the streaming kernel");
   } else {
     const size_t smem = fg_smem_bytes(ld, es, d * C, C, T1, 2, 4);
     // softmax with 3..15 classes: one-pass kernel with a 32-slot reduce-scatter

@@ -193,392 +193,6 @@ __global__ void __launch_bounds__(256) k1_fullgrad(FgParams p) {
   if (tid == 0 && p.write_loss) out[D] = la;
 }
 
-// Fast path for C <= 2 classes: the iterate lives in registers, rows are
-// zero-padded to whole 16-byte groups (so only the group index is tested),
-// R rows are reduced at once with a warp reduce-scatter, and the
-// per-row finishing work runs on different warps.  Same floating-point order
-// as k1_fullgrad (and as the oracle's MIRROR mode).
-template <int NV>
-__device__ __forceinline__ void reduce_scatter_n(double (&v)[NV], int lane) {
-#pragma unroll
-  for (int st = 0; st < 5; ++st) {
-    const int off = 16 >> st;
-    constexpr int dummy = 0;
-    (void)dummy;
-    const int cur = NV >> st;
-    if (cur > 1) {
-      const int h = cur >> 1;
-      const bool up = (lane & off) != 0;
-#pragma unroll
-      for (int i = 0; i < h; ++i) {
-        const double send = up ? v[i] : v[i + h];
-        const double keep = up ? v[i + h] : v[i];
-        v[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
-      }
-    } else {
-      v[0] = v[0] + __shfl_xor_sync(0xffffffffu, v[0], off);
-    }
-  }
-}
-
-template <class Tx, int NG, int CC, int R, int STAGES>
-__global__ void __launch_bounds__(256, 2) k1_fast(FgParams p) {
-  constexpr int V = VecT<Tx>::V;
-  constexpr int NV = R * CC;  // slots per warp (power of two <= 32)
-  constexpr int LG = NV <= 1 ? 0 : NV <= 2 ? 1 : NV <= 4 ? 2 : NV <= 8 ? 3 : NV <= 16 ? 4 : 5;
-  extern __shared__ __align__(128) unsigned char smem[];
-  const int T1 = blockDim.x, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, NW = T1 >> 5;
-  const int d = p.d, D = d * CC, ld = p.ld;
-  const int ngroups = (d + V - 1) / V;
-  const size_t stage_elems = (size_t)R * ld;
-  Tx* stages = reinterpret_cast<Tx*>(smem);
-  double* red = reinterpret_cast<double*>(smem + STAGES * stage_elems * sizeof(Tx));  // [2][NW][NV]
-  double* dl_s = red + 2 * NW * NV;                                                    // [2][R][CC]
-  double* lterm = dl_s + 2 * NV;                                                       // [2][R]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(lterm + 2 * R);
-
-  const int s = p.split0 + blockIdx.x;
-  const int64_t r0 = (int64_t)(((unsigned long long)p.n * (unsigned long long)s) / (unsigned long long)p.S);
-  const int64_t r1 = (int64_t)(((unsigned long long)p.n * (unsigned long long)(s + 1)) / (unsigned long long)p.S);
-  const int64_t ntile = (r1 - r0 + R - 1) / R;
-  const Tx* X = reinterpret_cast<const Tx*>(p.X);
-
-  double wr[NG][V][CC];
-#pragma unroll
-  for (int k = 0; k < NG; ++k)
-#pragma unroll
-    for (int q = 0; q < V; ++q)
-#pragma unroll
-      for (int c = 0; c < CC; ++c) {
-        const int j = (tid + k * T1) * V + q;
-        wr[k][q][c] = j < d ? p.w[c * d + j] : 0.0;
-      }
-  if (tid == 0) {
-    for (int st = 0; st < STAGES; ++st) mbar_init(&bars[st], 1);
-    fence_mbar_init();
-  }
-  __syncthreads();
-  auto issue = [&](int64_t tile) {
-    const int st = (int)(tile % STAGES);
-    const int64_t row = r0 + tile * R;
-    const int64_t rows = (r1 - row) < R ? (r1 - row) : R;
-    const uint32_t bytes = (uint32_t)(rows * ld * sizeof(Tx));
-    mbar_expect_tx(&bars[st], bytes);
-    bulk_g2s(stages + (size_t)st * stage_elems, X + row * ld, bytes, &bars[st]);
-  };
-  if (tid == 0)
-    for (int64_t t = 0; t < ntile && t < STAGES; ++t) issue(t);
-
-  // dot phase of tile i: per-warp slot sums into red[i & 1]
-  auto dot_tile = [&](int64_t i) {
-    const int st = (int)(i % STAGES);
-    mbar_wait(&bars[st], (uint32_t)((i / STAGES) & 1));
-    const Tx* xs = stages + (size_t)st * stage_elems;
-    const int nr = (int)((r1 - (r0 + i * R)) < R ? (r1 - (r0 + i * R)) : R);
-    double acc[NV];
-#pragma unroll
-    for (int v = 0; v < NV; ++v) acc[v] = 0.0;
-#pragma unroll
-    for (int k = 0; k < NG; ++k) {
-      const int g = tid + k * T1;
-      if (g < ngroups) {
-#pragma unroll
-        for (int r = 0; r < R; ++r) {
-          if (r < nr) {
-            double xv[V];
-            load_group<Tx>(xs + (size_t)r * ld + g * V, xv);
-#pragma unroll
-            for (int q = 0; q < V; ++q)
-#pragma unroll
-              for (int c = 0; c < CC; ++c) acc[r * CC + c] = fma(xv[q], wr[k][q][c], acc[r * CC + c]);
-          }
-        }
-      }
-    }
-    reduce_scatter_n<NV>(acc, lane);
-    if ((lane & ((32 >> LG) - 1)) == 0) red[(i & 1) * NW * NV + wid * NV + (lane >> (5 - LG))] = acc[0];
-  };
-
-  double gacc[NG][V][CC];
-#pragma unroll
-  for (int k = 0; k < NG; ++k)
-#pragma unroll
-    for (int q = 0; q < V; ++q)
-#pragma unroll
-      for (int c = 0; c < CC; ++c) gacc[k][q][c] = 0.0;
-  double la = 0.0;
-
-  // finisher targets (lane 0 of warp r % NW owns row r of a tile): prefetched y / label
-  double ypre[(R + 7) / 8 + 1];
-  int lpre[(R + 7) / 8 + 1];
-  auto prefetch_targets = [&](int64_t i) {
-    if (lane == 0 && i < ntile) {
-      int slot = 0;
-      for (int r = wid; r < R; r += NW, ++slot) {
-        const int64_t row = r0 + i * R + r;
-        if (row < r1) {
-          if (p.loss == 0) ypre[slot] = p.y[row];
-          else lpre[slot] = p.labels[row];
-        }
-      }
-    }
-  };
-
-  prefetch_targets(0);
-  dot_tile(0);
-  for (int64_t i = 0; i < ntile; ++i) {
-    __syncthreads();  // red[i&1] complete; grad(i-1) done everywhere; dl[i&1] free
-    // stage of tile i-1 is free: refill it
-    if (tid == 0 && i >= 1 && i - 1 + STAGES < ntile) issue(i - 1 + STAGES);
-    const int64_t rowb = r0 + i * R;
-    const int nr = (int)((r1 - rowb) < R ? (r1 - rowb) : R);
-    // finishers: logits -> loss term and loss derivative of tile i
-    if (lane == 0) {
-      int slot = 0;
-      for (int r = wid; r < nr; r += NW, ++slot) {
-        double lg[CC];
-#pragma unroll
-        for (int c = 0; c < CC; ++c) {
-          const double* rb = red + (i & 1) * NW * NV;
-          double v = rb[r * CC + c];
-          for (int w2 = 1; w2 < NW; ++w2) v = v + rb[w2 * NV + r * CC + c];
-          lg[c] = v;
-        }
-        double* dls = dl_s + (i & 1) * NV;
-        if (p.loss == 0) {
-          const double e = lg[0] - ypre[slot];
-          lterm[(i & 1) * R + r] = __dmul_rn(__dmul_rn(0.5, e), e);
-          dls[r * CC] = e;
-        } else {
-          const int lab = lpre[slot];
-          lterm[(i & 1) * R + r] = softmax_loss(lg, CC, lab);
-          softmax_dl<CC>(lg, CC, lab);
-#pragma unroll
-          for (int c = 0; c < CC; ++c) dls[r * CC + c] = lg[c];
-        }
-      }
-    }
-    prefetch_targets(i + 1);
-    // dot phase of the next tile overlaps the finishers
-    if (i + 1 < ntile) dot_tile(i + 1);
-    __syncthreads();  // dl[i&1] ready
-    // gradient phase of tile i, sequential over its rows
-    const Tx* xs = stages + (size_t)(i % STAGES) * stage_elems;
-    const double* dls = dl_s + (i & 1) * NV;
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-      if (r < nr) {
-        double dlr[CC];
-#pragma unroll
-        for (int c = 0; c < CC; ++c) dlr[c] = dls[r * CC + c];
-#pragma unroll
-        for (int k = 0; k < NG; ++k) {
-          const int g = tid + k * T1;
-          if (g < ngroups) {
-            double xv[V];
-            load_group<Tx>(xs + (size_t)r * ld + g * V, xv);
-#pragma unroll
-            for (int q = 0; q < V; ++q)
-#pragma unroll
-              for (int c = 0; c < CC; ++c) gacc[k][q][c] = fma(dlr[c], xv[q], gacc[k][q][c]);
-          }
-        }
-      }
-    }
-    if (tid == 0 && p.write_loss)
-      for (int r = 0; r < nr; ++r) la = la + lterm[(i & 1) * R + r];
-  }
-
-  double* out = p.partials + (size_t)blockIdx.x * (D + 1);
-#pragma unroll
-  for (int k = 0; k < NG; ++k) {
-    const int g = tid + k * T1;
-#pragma unroll
-    for (int q = 0; q < V; ++q) {
-      const int j = g * V + q;
-      if (g < ngroups && j < d)
-#pragma unroll
-        for (int c = 0; c < CC; ++c) out[(size_t)c * d + j] = gacc[k][q][c];
-    }
-  }
-  if (tid == 0 && p.write_loss) out[D] = la;
-}
-
-// Register-tile variant: each thread converts its R x (NG*V) slice of a tile
-// ONCE into fp64 registers and uses it for both the dot and the gradient
-// phase; full tiles run without per-row / per-group predicates.  Same
-// floating-point order as k1_fullgrad / k1_fast (oracle MIRROR mode).
-template <class Tx, int NG, int CC, int R, int STAGES, bool FULLG, int TB>
-__global__ void __launch_bounds__(TB, TB <= 128 ? 3 : 1) k1_reg(FgParams p) {
-  constexpr int V = VecT<Tx>::V;
-  constexpr int NV = R * CC;
-  constexpr int LG = NV <= 1 ? 0 : NV <= 2 ? 1 : NV <= 4 ? 2 : NV <= 8 ? 3 : NV <= 16 ? 4 : 5;
-  extern __shared__ __align__(128) unsigned char smem[];
-  const int T1 = blockDim.x, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, NW = T1 >> 5;
-  const int d = p.d, D = d * CC, ld = p.ld;
-  const int ngroups = (d + V - 1) / V;
-  const size_t stage_elems = (size_t)R * ld;
-  Tx* stages = reinterpret_cast<Tx*>(smem);
-  double* red = reinterpret_cast<double*>(smem + STAGES * stage_elems * sizeof(Tx));  // [2][NW][NV]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(red + 2 * NW * NV);
-  double* ysm = reinterpret_cast<double*>(bars + STAGES);  // targets of the split
-
-  const int s = p.split0 + blockIdx.x;
-  const int64_t r0 = (int64_t)(((unsigned long long)p.n * (unsigned long long)s) / (unsigned long long)p.S);
-  const int64_t r1 = (int64_t)(((unsigned long long)p.n * (unsigned long long)(s + 1)) / (unsigned long long)p.S);
-  const int64_t ntile = (r1 - r0 + R - 1) / R;
-  const Tx* X = reinterpret_cast<const Tx*>(p.X);
-  for (int64_t q = tid; q < r1 - r0; q += T1)
-    ysm[q] = p.loss == 0 ? p.y[r0 + q] : (double)p.labels[r0 + q];
-
-  double wr[NG][V][CC];
-#pragma unroll
-  for (int k = 0; k < NG; ++k)
-#pragma unroll
-    for (int q = 0; q < V; ++q)
-#pragma unroll
-      for (int c = 0; c < CC; ++c) {
-        const int j = (tid + k * T1) * V + q;
-        wr[k][q][c] = j < d ? p.w[c * d + j] : 0.0;
-      }
-  if (tid == 0) {
-    for (int st = 0; st < STAGES; ++st) mbar_init(&bars[st], 1);
-    fence_mbar_init();
-  }
-  __syncthreads();
-  auto issue = [&](int64_t tile) {
-    const int st = (int)(tile % STAGES);
-    const int64_t row = r0 + tile * R;
-    const int64_t rows = (r1 - row) < R ? (r1 - row) : R;
-    const uint32_t bytes = (uint32_t)(rows * ld * sizeof(Tx));
-    mbar_expect_tx(&bars[st], bytes);
-    bulk_g2s(stages + (size_t)st * stage_elems, X + row * ld, bytes, &bars[st]);
-  };
-  if (tid == 0)
-    for (int64_t t = 0; t < ntile && t < STAGES; ++t) issue(t);
-
-  double gacc[NG][V][CC];
-#pragma unroll
-  for (int k = 0; k < NG; ++k)
-#pragma unroll
-    for (int q = 0; q < V; ++q)
-#pragma unroll
-      for (int c = 0; c < CC; ++c) gacc[k][q][c] = 0.0;
-  double la = 0.0;
-  bool gval[NG];
-#pragma unroll
-  for (int k = 0; k < NG; ++k) gval[k] = FULLG || (tid + k * T1 < ngroups);
-  // every warp evaluates the loss derivatives itself: lane (fr, fc) = (row, class)
-  const int fr = lane / CC, fc = lane % CC;
-
-  for (int64_t i = 0; i < ntile; ++i) {
-    const int st = (int)(i % STAGES);
-    const int64_t rowb = r0 + i * R;
-    const int nr = (int)((r1 - rowb) < R ? (r1 - rowb) : R);
-    const bool act = (lane < NV) && (fr < nr);
-    const double tgt = act ? ysm[rowb - r0 + fr] : 0.0;
-    mbar_wait(&bars[st], (uint32_t)((i / STAGES) & 1));
-    const Tx* xs = stages + (size_t)st * stage_elems;
-    double xr[R][NG][V];
-    double acc[NV];
-#pragma unroll
-    for (int v = 0; v < NV; ++v) acc[v] = 0.0;
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-      const bool rv = (r < nr);
-#pragma unroll
-      for (int k = 0; k < NG; ++k) {
-        if (rv && gval[k]) {
-          load_group<Tx>(xs + (size_t)r * ld + (tid + k * T1) * V, xr[r][k]);
-        } else {
-#pragma unroll
-          for (int q = 0; q < V; ++q) xr[r][k][q] = 0.0;
-        }
-      }
-    }
-#pragma unroll
-    for (int r = 0; r < R; ++r)
-#pragma unroll
-      for (int k = 0; k < NG; ++k)
-#pragma unroll
-        for (int q = 0; q < V; ++q)
-#pragma unroll
-          for (int c = 0; c < CC; ++c) acc[r * CC + c] = fma(xr[r][k][q], wr[k][q][c], acc[r * CC + c]);
-    reduce_scatter_n<NV>(acc, lane);
-    double* rb = red + (size_t)(i & 1) * NW * NV;
-    if ((lane & ((32 >> LG) - 1)) == 0) rb[wid * NV + (lane >> (5 - LG))] = acc[0];
-    __syncthreads();
-    // x of this tile now lives in registers: its stage can be refilled
-    if (tid == 0 && i + STAGES < ntile) issue(i + STAGES);
-
-    // logit of (fr, fc): warps summed in order (same in every warp)
-    double lg = 0.0;
-    if (lane < NV) {
-      // all loads first (independent), then the in-order chain of adds
-      lg = rb[lane];
-      for (int w2 = 1; w2 < NW; ++w2) lg = lg + rb[w2 * NV + lane];
-    }
-    double pr, lt = 0.0;
-    if (p.loss == 0) {
-      pr = lg - tgt;
-      lt = __dmul_rn(__dmul_rn(0.5, pr), pr);
-    } else {
-      const int lab = (int)tgt;
-      const int base = (fr * CC) & 31;
-      double mx = 0.0;
-#pragma unroll
-      for (int c = 0; c < CC; ++c) {
-        const double v = __shfl_sync(0xffffffffu, lg, (base + c) & 31);
-        mx = c == 0 ? v : (v > mx ? v : mx);
-      }
-      const double e = hexp(lg - mx);
-      double ssum = __shfl_sync(0xffffffffu, e, base);
-#pragma unroll
-      for (int c = 1; c < CC; ++c) ssum = ssum + __shfl_sync(0xffffffffu, e, (base + c) & 31);
-      const double lab_logit = __shfl_sync(0xffffffffu, lg, (base + lab) & 31);
-      pr = e / ssum;
-      if (fc == lab) pr = pr - 1.0;
-      if (wid == 0 && fc == 0) lt = (mx + hlog(ssum)) - lab_logit;
-    }
-    double dlr[NV];
-#pragma unroll
-    for (int v = 0; v < NV; ++v) dlr[v] = __shfl_sync(0xffffffffu, pr, v);
-    if (wid == 0 && p.write_loss) {
-#pragma unroll
-      for (int r = 0; r < R; ++r) {
-        const double t = __shfl_sync(0xffffffffu, lt, r * CC);
-        if (r < nr) la = la + t;
-      }
-    }
-    // rows beyond nr: skipped
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-      if (r < nr) {
-#pragma unroll
-        for (int k = 0; k < NG; ++k)
-#pragma unroll
-          for (int q = 0; q < V; ++q)
-#pragma unroll
-            for (int c = 0; c < CC; ++c) gacc[k][q][c] = fma(dlr[r * CC + c], xr[r][k][q], gacc[k][q][c]);
-      }
-    }
-  }
-
-  double* out = p.partials + (size_t)blockIdx.x * (D + 1);
-#pragma unroll
-  for (int k = 0; k < NG; ++k) {
-    const int g = tid + k * T1;
-#pragma unroll
-    for (int q = 0; q < V; ++q) {
-      const int j = g * V + q;
-      if (g < ngroups && j < d)
-#pragma unroll
-        for (int c = 0; c < CC; ++c) out[(size_t)c * d + j] = gacc[k][q][c];
-    }
-  }
-  if (tid == 0 && p.write_loss) out[D] = la;
-}
-
 // pairwise tree over the splits, in passes: thread (group o, coordinate k)
 // combines G = 2^m consecutive splits with a register tree (pairs, then
 // pairs of pairs, ...), i.e. one complete subtree of the global pairwise
@@ -670,86 +284,6 @@ __global__ void k_samples(uint64_t state0, int64_t total, int opt2, uint64_t T, 
 }
 
 // ---------------------------------------------------------------- dispatch
-size_t fast_smem_bytes(int ld, int elem, int threads, int R, int CC, int stages) {
-  size_t b = (size_t)stages * R * ld * elem;
-  b += 2 * ((size_t)(threads / 32) * R * CC * 8 + (size_t)R * CC * 8 + (size_t)R * 8);
-  return (b + 7) / 8 * 8 + stages * 8;
-}
-
-template <class Tx, int NG, int CC, int R, int STAGES>
-static cudaError_t launch_fast_t(const FgLaunch& L, const FgParams& p, cudaStream_t st) {
-  auto kern = k1_fast<Tx, NG, CC, R, STAGES>;
-  const size_t smem = fast_smem_bytes(L.ld, (int)sizeof(Tx), L.threads, R, CC, STAGES);
-  if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  kern<<<L.nsplit_local, L.threads, smem, st>>>(p);
-  return cudaGetLastError();
-}
-
-// fast-path shapes: (NG, R, STAGES); R rows per tile, STAGES-deep bulk-copy ring
-template <class Tx, int CC>
-static cudaError_t launch_fast_cc(const FgLaunch& L, const FgParams& p, cudaStream_t st) {
-  switch (L.ng * 1000 + L.rows * 10 + L.stages) {
-    case 1086: return launch_fast_t<Tx, 1, CC, 8, 6>(L, p, st);
-    case 1046: return launch_fast_t<Tx, 1, CC, 4, 6>(L, p, st);
-    case 1026: return launch_fast_t<Tx, 1, CC, 2, 6>(L, p, st);
-    case 1016: return launch_fast_t<Tx, 1, CC, 1, 6>(L, p, st);
-    case 2046: return launch_fast_t<Tx, 2, CC, 4, 6>(L, p, st);
-    case 2026: return launch_fast_t<Tx, 2, CC, 2, 6>(L, p, st);
-    case 2016: return launch_fast_t<Tx, 2, CC, 1, 6>(L, p, st);
-    case 4026: return launch_fast_t<Tx, 4, CC, 2, 6>(L, p, st);
-    case 4016: return launch_fast_t<Tx, 4, CC, 1, 6>(L, p, st);
-    case 4013: return launch_fast_t<Tx, 4, CC, 1, 3>(L, p, st);
-    case 4023: return launch_fast_t<Tx, 4, CC, 2, 3>(L, p, st);
-    case 8013: return launch_fast_t<Tx, 8, CC, 1, 3>(L, p, st);
-    case 8016: return launch_fast_t<Tx, 8, CC, 1, 6>(L, p, st);
-    default: return cudaErrorInvalidConfiguration;
-  }
-}
-
-template <class Tx, int NG, int CC, int R, int STAGES, int TB>
-static cudaError_t launch_reg_tb(const FgLaunch& L, const FgParams& p, cudaStream_t st) {
-  const size_t smem = (size_t)STAGES * R * L.ld * sizeof(Tx) + 2 * (size_t)(L.threads / 32) * R * CC * 8 +
-                      STAGES * 8 + 8 * (size_t)((p.n + p.S - 1) / p.S + 1);
-  if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
-  const bool fullg = ((p.d + VecT<Tx>::V - 1) / VecT<Tx>::V) == NG * L.threads;
-  cudaError_t e;
-  if (fullg) {
-    auto kern = k1_reg<Tx, NG, CC, R, STAGES, true, TB>;
-    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    kern<<<L.nsplit_local, L.threads, smem, st>>>(p);
-  } else {
-    auto kern = k1_reg<Tx, NG, CC, R, STAGES, false, TB>;
-    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    kern<<<L.nsplit_local, L.threads, smem, st>>>(p);
-  }
-  return cudaGetLastError();
-}
-
-template <class Tx, int NG, int CC, int R, int STAGES>
-static cudaError_t launch_reg_t(const FgLaunch& L, const FgParams& p, cudaStream_t st) {
-  if (L.threads <= 128) return launch_reg_tb<Tx, NG, CC, R, STAGES, 128>(L, p, st);
-  return launch_reg_tb<Tx, NG, CC, R, STAGES, 512>(L, p, st);
-}
-
-template <class Tx, int CC>
-static cudaError_t launch_reg_cc(const FgLaunch& L, const FgParams& p, cudaStream_t st) {
-  switch (L.ng * 1000 + L.rows * 10 + L.stages) {
-    case 1084: return launch_reg_t<Tx, 1, CC, 8, 4>(L, p, st);
-    case 1044: return launch_reg_t<Tx, 1, CC, 4, 4>(L, p, st);
-    case 1024: return launch_reg_t<Tx, 1, CC, 2, 4>(L, p, st);
-    case 2044: return launch_reg_t<Tx, 2, CC, 4, 4>(L, p, st);
-    case 2024: return launch_reg_t<Tx, 2, CC, 2, 4>(L, p, st);
-    case 2014: return launch_reg_t<Tx, 2, CC, 1, 4>(L, p, st);
-    case 4024: return launch_reg_t<Tx, 4, CC, 2, 4>(L, p, st);
-    case 4014: return launch_reg_t<Tx, 4, CC, 1, 4>(L, p, st);
-    default: return cudaErrorInvalidConfiguration;
-  }
-}
-
 template <class Tx, int NG, int CT>
 static cudaError_t launch_fg_t(const FgLaunch& L, const FgParams& p, cudaStream_t st) {
   constexpr int R = 2, STAGES = 4;
@@ -795,29 +329,6 @@ size_t fg_smem_bytes(int ld, int elem, int D, int C, int threads, int R, int sta
 cudaError_t launch_fullgrad(const FgLaunch& L, const FgParams& p, cudaStream_t st) {
   if (L.fast == 3) return launch_fullgrad_smx(L, p, st);
   if (L.fast == 4) return launch_fullgrad_stream(L, p, st);
-  if (L.fast == 2) {
-    switch (L.dtype * 10 + p.C) {
-      case 1: return launch_reg_cc<double, 1>(L, p, st);
-      case 2: return launch_reg_cc<double, 2>(L, p, st);
-      case 11: return launch_reg_cc<float, 1>(L, p, st);
-      case 12: return launch_reg_cc<float, 2>(L, p, st);
-      case 21: return launch_reg_cc<__nv_bfloat16, 1>(L, p, st);
-      case 22: return launch_reg_cc<__nv_bfloat16, 2>(L, p, st);
-      default: return cudaErrorInvalidConfiguration;
-    }
-  }
-  if (L.fast) {
-    const int cc = p.C;
-    switch (L.dtype * 10 + cc) {
-      case 1: return launch_fast_cc<double, 1>(L, p, st);
-      case 2: return launch_fast_cc<double, 2>(L, p, st);
-      case 11: return launch_fast_cc<float, 1>(L, p, st);
-      case 12: return launch_fast_cc<float, 2>(L, p, st);
-      case 21: return launch_fast_cc<__nv_bfloat16, 1>(L, p, st);
-      case 22: return launch_fast_cc<__nv_bfloat16, 2>(L, p, st);
-      default: return cudaErrorInvalidConfiguration;
-    }
-  }
   switch (L.dtype) {
     case 0: return launch_fg_dt<double>(L, p, st);
     case 1: return launch_fg_dt<float>(L, p, st);

@@ -1,6 +1,5 @@
-// k_fullgrad_stream.cu -- K1 for the HBM-bound shapes (C <= 2 outputs per
-// feature, i.e. least squares and 2-class softmax; BASELINE C1/C3/C4): a
-// persistent streaming kernel.
+// k_fullgrad_stream.cu -- K1 for the HBM-bound shapes (least squares and
+// 2-class softmax; BASELINE C1/C3/C4): a persistent streaming kernel.
 //
 // Reference: Objective::full_gradient + Objective::loss in one HBM pass
 // (proj/src/objectives.cpp:258-311 and :193-223; squared rows :274-276,
@@ -15,11 +14,15 @@
 //     its slice of w~ and of the split's gradient columns live in registers,
 //     the tile's x slice is converted to fp64 once and reused by the dot and
 //     the gradient phase;
-//   * per tile ONE __syncthreads: warp reduce-scatter of the R x C partial
-//     logits -> shared (parity double-buffered) -> every warp sums the NW
-//     warp partials of its lane's slot (fully unrolled) and evaluates the
-//     loss derivative itself (squared: e = x.w - y; softmax: lane-parallel),
-//     so no second barrier broadcasts it.
+//   * per tile ONE __syncthreads: warp reduce-scatter of the R partial row
+//     dots -> shared (parity double-buffered) -> every warp sums the NW warp
+//     partials of its lane's row (fully unrolled) and evaluates the loss
+//     derivative itself, so no second barrier broadcasts it;
+//   * two classes (CC == 2) use the logistic form: the softmax depends only
+//     on s = x.(w1 - w0), so ONE dot and ONE gradient column per row (the
+//     other column is its exact negation) -- half the fp64 work and half the
+//     registers of two softmax logits, which is what lets the bf16 C4 sweep
+//     stream at HBM speed.  Formulas: oracle/halp_oracle.c mirror_logistic_row.
 //
 // Floating-point order = k1_reg / k1_fullgrad = oracle MIRROR mode (DESIGN.md
 // "Reduction orders"): row dot = sequential fma over the thread's groups,
@@ -95,9 +98,10 @@ template <class Tx, int CC, int NW, int NG, int R, int STAGES, bool FULLG>
 __global__ void __launch_bounds__(NW * 32, 1) k1_stream(FgParams p, int nloc) {
   constexpr int V = VecK<Tx>::V;
   constexpr int T1 = NW * 32;
-  constexpr int NV = R * CC;
+  constexpr int NV = R;  // one dot per row (squared: x.w; two classes: x.(w1 - w0))
   constexpr int LG = Log2<NV>::v;
-  static_assert((NV & (NV - 1)) == 0 && NV <= 32, "R*C must be a power of two <= 32");
+  static_assert(CC == 1 || CC == 2, "least squares or two classes");
+  static_assert((NV & (NV - 1)) == 0 && NV <= 32, "R must be a power of two <= 32");
   extern __shared__ __align__(128) unsigned char smem[];
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int d = p.d, D = d * CC, ld = p.ld;
@@ -109,18 +113,16 @@ __global__ void __launch_bounds__(NW * 32, 1) k1_stream(FgParams p, int nloc) {
   const Tx* X = reinterpret_cast<const Tx*>(p.X);
   const unsigned long long nn = (unsigned long long)p.n, SS = (unsigned long long)p.S;
 
-  double wr[NG][V][CC];
+  double wr[NG][V];  // w (squared) or w1 - w0 (two classes)
   bool gval[NG];
 #pragma unroll
   for (int k = 0; k < NG; ++k) {
     gval[k] = FULLG || (tid + k * T1 < ngroups);
 #pragma unroll
-    for (int q = 0; q < V; ++q)
-#pragma unroll
-      for (int c = 0; c < CC; ++c) {
-        const int j = (tid + k * T1) * V + q;
-        wr[k][q][c] = j < d ? p.w[c * d + j] : 0.0;
-      }
+    for (int q = 0; q < V; ++q) {
+      const int j = (tid + k * T1) * V + q;
+      wr[k][q] = j >= d ? 0.0 : CC == 1 ? p.w[j] : p.w[d + j] - p.w[j];
+    }
   }
   if (tid == 0) {
 #pragma unroll
@@ -159,8 +161,8 @@ __global__ void __launch_bounds__(NW * 32, 1) k1_stream(FgParams p, int nloc) {
 #pragma unroll 1
     for (int j = 0; j < STAGES; ++j) issue(j);
 
-  // lane (fr, fc) = (row, class) of the loss-derivative slot it evaluates
-  const int fr = lane / CC, fc = lane % CC;
+  // lane fr < R evaluates the loss derivative of row fr of every tile
+  const int fr = lane;
   int64_t jseq = 0;  // consumer position in the CTA's tile sequence
 
 #pragma unroll 1
@@ -168,13 +170,11 @@ __global__ void __launch_bounds__(NW * 32, 1) k1_stream(FgParams p, int nloc) {
     const int64_t r0 = (int64_t)(nn * (unsigned long long)(p.split0 + ls) / SS);
     const int64_t r1 = (int64_t)(nn * (unsigned long long)(p.split0 + ls + 1) / SS);
     const int64_t ntile = (r1 - r0 + R - 1) / R;
-    double gacc[NG][V][CC];
+    double gacc[NG][V];
 #pragma unroll
     for (int k = 0; k < NG; ++k)
 #pragma unroll
-      for (int q = 0; q < V; ++q)
-#pragma unroll
-        for (int c = 0; c < CC; ++c) gacc[k][q][c] = 0.0;
+      for (int q = 0; q < V; ++q) gacc[k][q] = 0.0;
     double la = 0.0;
     // targets of the slot rows, one tile ahead
     double tgt = 0.0;
@@ -214,9 +214,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k1_stream(FgParams p, int nloc) {
 #pragma unroll
           for (int k = 0; k < NG; ++k)
 #pragma unroll
-            for (int q = 0; q < V; ++q)
-#pragma unroll
-              for (int c = 0; c < CC; ++c) acc[r * CC + c] = fma(xr[r][k][q], wr[k][q][c], acc[r * CC + c]);
+            for (int q = 0; q < V; ++q) acc[r] = fma(xr[r][k][q], wr[k][q], acc[r]);
         reduce_scatter_k<NV>(acc, lane);
         if ((lane & ((32 >> LG) - 1)) == 0) rb[wid * NV + (lane >> (5 - LG))] = acc[0];
         __syncthreads();
@@ -238,22 +236,16 @@ __global__ void __launch_bounds__(NW * 32, 1) k1_stream(FgParams p, int nloc) {
           pr = lg - tcur;
           lt = __dmul_rn(__dmul_rn(0.5, pr), pr);
         } else {
+          // two-class softmax, logistic form (mirror_logistic_row): s = lg
           const int lab = (int)tcur;
-          const int base = (fr * CC) & 31;
-          double mx = 0.0;
-#pragma unroll
-          for (int c = 0; c < CC; ++c) {
-            const double v = __shfl_sync(0xffffffffu, lg, (base + c) & 31);
-            mx = c == 0 ? v : (v > mx ? v : mx);
+          const double q = hexp(-fabs(lg));
+          const double den = 1.0 + q;
+          const double p0 = (lg > 0.0 ? q : 1.0) / den;
+          pr = lab == 0 ? p0 - 1.0 : p0;
+          if (wid == 0 && lane < NV) {
+            const double a = lab == 0 ? lg : -lg;
+            lt = (a > 0.0 ? a : 0.0) + hlog(den);
           }
-          const double e = hexp(lg - mx);
-          double ssum = __shfl_sync(0xffffffffu, e, base);
-#pragma unroll
-          for (int c = 1; c < CC; ++c) ssum = ssum + __shfl_sync(0xffffffffu, e, (base + c) & 31);
-          const double lab_logit = __shfl_sync(0xffffffffu, lg, (base + lab) & 31);
-          pr = e / ssum;
-          if (fc == lab) pr = pr - 1.0;
-          if (wid == 0 && fc == 0 && lane < NV) lt = (mx + hlog(ssum)) - lab_logit;
         }
         double dlr[NV];
 #pragma unroll
@@ -261,7 +253,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k1_stream(FgParams p, int nloc) {
         if (wid == 0) {
 #pragma unroll
           for (int r = 0; r < R; ++r) {
-            const double t = __shfl_sync(0xffffffffu, lt, r * CC);
+            const double t = __shfl_sync(0xffffffffu, lt, r);
             if (FULL || r < nr) la = la + t;
           }
         }
@@ -271,9 +263,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k1_stream(FgParams p, int nloc) {
 #pragma unroll
             for (int k = 0; k < NG; ++k)
 #pragma unroll
-              for (int q = 0; q < V; ++q)
-#pragma unroll
-                for (int c = 0; c < CC; ++c) gacc[k][q][c] = fma(dlr[r * CC + c], xr[r][k][q], gacc[k][q][c]);
+              for (int q = 0; q < V; ++q) gacc[k][q] = fma(dlr[r], xr[r][k][q], gacc[k][q]);
           }
         }
       };
@@ -289,9 +279,10 @@ __global__ void __launch_bounds__(NW * 32, 1) k1_stream(FgParams p, int nloc) {
 #pragma unroll
         for (int q = 0; q < V; ++q) {
           const int j = g * V + q;
-          if (j < d)
-#pragma unroll
-            for (int c = 0; c < CC; ++c) out[(size_t)c * d + j] = gacc[k][q][c];
+          if (j < d) {
+            out[j] = gacc[k][q];
+            if (CC == 2) out[(size_t)d + j] = -gacc[k][q];  // class 1 = -class 0, exactly
+          }
         }
       }
     }
@@ -303,7 +294,8 @@ __global__ void __launch_bounds__(NW * 32, 1) k1_stream(FgParams p, int nloc) {
 size_t stream_smem_bytes(int ld, int elem, int warps, int R, int CC, int stages) {
   size_t b = (size_t)stages * R * ld * elem;
   b = (b + 15) / 16 * 16;
-  b += (size_t)2 * warps * R * CC * 8 + (size_t)stages * 8;
+  (void)CC;
+  b += (size_t)2 * warps * R * 8 + (size_t)stages * 8;
   return b;
 }
 

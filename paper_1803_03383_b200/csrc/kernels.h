@@ -22,10 +22,9 @@ struct FgParams {
 };
 struct FgLaunch {
   int dtype, ng, ct, threads, ld, nsplit_local;
-  int fast, rows, stages;  // fast: 1/2 register-resident paths for C <= 2, 3 softmax C >= 3, 4 streaming C <= 2; rows per tile, ring depth
+  int fast, rows, stages;  // fast: 0 generic, 3 softmax C >= 3, 4 streaming C <= 2; rows per tile, ring depth
 };
 size_t fg_smem_bytes(int ld, int elem, int D, int C, int threads, int R, int stages);
-size_t fast_smem_bytes(int ld, int elem, int threads, int R, int CC, int stages);
 cudaError_t launch_fullgrad(const FgLaunch& L, const FgParams& p, cudaStream_t st);
 // softmax with 3..15 classes (FgLaunch.fast == 3), k_fullgrad_smx.cu
 size_t smx_smem_bytes(int ld, int elem, int d, int C, int threads, int64_t split_rows);

@@ -48,3 +48,31 @@ def test_mirror_vs_ref_codes_identical(oracle, plan):
     a = oracle.run_halp(obj, cfg, plan=plan, trace_steps=8000)
     b = oracle.run_halp(obj, cfg, trace_steps=8000)
     assert (a.trace != b.trace).sum() == 0
+
+
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_two_class_logistic_form_matches_reference_softmax(oracle, dtype):
+    """K1 evaluates two-class softmax rows in the logistic form (one dot with
+    w1 - w0, class-1 column = -class-0 column; oracle mirror_logistic_row).
+    Against the reference's own two-logit softmax rows (REF order,
+    objectives.cpp:206-217, 277-283) it agrees to rounding: 1e-12 relative on
+    the gradient (norm-wise) and the loss, at a random iterate and at w = 0."""
+    import numpy as np
+
+    import paper_1803_03383_b200 as H
+
+    rng = np.random.default_rng(5)
+    n, d = 3000, 48
+    X = rng.standard_normal((n, d)) / np.sqrt(d)
+    wstar = rng.standard_normal(d)
+    lab = (rng.random(n) < 1.0 / (1.0 + np.exp(-X @ wstar))).astype(np.int32)
+    if dtype == "f32":
+        X = X.astype(np.float32)
+    obj = oracle.OracleObjective(X, labels=lab, num_classes=2, l2=1e-5)
+    plan = H.oracle_plan_for(n, d, 2, dtype)
+    for w in (rng.standard_normal(2 * d), np.zeros(2 * d)):
+        gm, gr = obj.full_gradient(w, plan=plan), obj.full_gradient(w)
+        assert np.linalg.norm(gm - gr) <= 1e-12 * np.linalg.norm(gr)
+        lm, lr = obj.loss_value(w, plan=plan), obj.loss_value(w)
+        assert abs(lm - lr) <= 1e-12 * abs(lr)
+    assert abs(obj.loss_value(np.zeros(2 * d), plan=plan) - np.log(2.0)) <= 1e-15

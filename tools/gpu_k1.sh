@@ -1,6 +1,6 @@
 #!/bin/bash
 mkdir -p gpurun_out
 timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
-timeout 900 python tools/fg_sweep.py c3 "" HALP_FG_KERNEL=2 HALP_FG_NG=4 HALP_FG_NG=4,HALP_FG_STAGES=6 HALP_FG_STAGES=6 > gpurun_out/fg_c3.log 2>&1
-timeout 900 python tools/fg_sweep.py c4 "" HALP_FG_KERNEL=2 HALP_FG_STAGES=6 > gpurun_out/fg_c4.log 2>&1
+timeout 900 python tools/fg_sweep.py c4 "" HALP_FG_ROWS=4 > gpurun_out/fg_c4.log 2>&1
+timeout 900 python tools/fg_sweep.py c3 "" > gpurun_out/fg_c3.log 2>&1
 echo done
