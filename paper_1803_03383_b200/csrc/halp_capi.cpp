@@ -82,9 +82,16 @@ struct Nccl {
 
 struct ShardPlan {
   int64_t S = 1, split_begin = 0, split_end = 1, row_begin = 0, row_end = 0;
+  int sub = 1;
+  int64_t cta_splits() const { return (split_end - split_begin) / sub; }
 };
 
-ShardPlan make_shard_plan(int64_t n, int d, int C, int dtype, int world, int rank) {
+// Split grid of the full-gradient pass.  S counts MIRROR splits (the leaves
+// of the pairwise reduction tree); a launched CTA split covers `sub` of them
+// (the warp-per-row kernel combines its warps' splits on chip), and one
+// (D+1) partial is written per CTA split: S/sub of them, <= 4096, within an
+// eighth of X's bytes.  Ranks own aligned, equal blocks of CTA splits.
+ShardPlan make_shard_plan(int64_t n, int d, int C, int dtype, int world, int rank, int sub) {
   ShardPlan sp;
   const int64_t D1 = (int64_t)d * C + 1;
   const double xbytes = (double)n * d * elem_size(dtype);
@@ -92,11 +99,13 @@ ShardPlan make_shard_plan(int64_t n, int d, int C, int dtype, int world, int ran
   int64_t S = 1;
   while (S * 2 <= 4096 && S * 2 <= std::max<int64_t>(1, n / 2) && (double)(S * 2) * D1 * 8.0 <= budget) S *= 2;
   if (S < world) S = next_pow2(world);
-  sp.S = S;
-  sp.split_begin = S / world * rank;
-  sp.split_end = S / world * (rank + 1);
-  sp.row_begin = (int64_t)((unsigned __int128)n * sp.split_begin / S);
-  sp.row_end = (int64_t)((unsigned __int128)n * sp.split_end / S);
+  sub = std::max(1, sub);
+  sp.S = S * sub;
+  sp.sub = sub;
+  sp.split_begin = S / world * rank * sub;
+  sp.split_end = S / world * (rank + 1) * sub;
+  sp.row_begin = (int64_t)((unsigned __int128)n * sp.split_begin / sp.S);
+  sp.row_end = (int64_t)((unsigned __int128)n * sp.split_end / sp.S);
   return sp;
 }
 
@@ -210,6 +219,7 @@ struct halp_problem {
   int64_t trace_cap = 0;
   halp_timing timing{};
   int64_t create_h2d = 0;  // bytes uploaded by halp_problem_create
+  int x_finite = 0;        // bf16 X checked finite (K1 integer-conversion path)
   Events ev_fg, ev_fin, ev_in, ev_smp;
 
   ~halp_problem() {
@@ -276,6 +286,86 @@ bool plan_stream(int d, int C, int dtype, FgLaunch* out) {
   return true;
 }
 
+// K1 two-class plan (k_fullgrad_ws.cu): the streaming kernel's thread layout
+// plus a finisher warp; R by the register budget of two x buffers.
+bool ws_shape_ok(int nw, int ng, int r, int st) {
+#define HALP_WS_OK(NW, NG, R, ST) \
+  if (nw == NW && ng == NG && r == R && st == ST) return true;
+  HALP_WS_SHAPES(HALP_WS_OK)
+#undef HALP_WS_OK
+  return false;
+}
+
+bool plan_ws(int d, int C, int dtype, FgLaunch* out) {
+  // opt-in (HALP_FG_WS=1): the single finisher warp's dependent chain
+  // (~370 instructions per 4-row tile) bounds it below the streaming kernel
+  if (C != 2 || env_int("HALP_FG_WS", 0) == 0) return false;
+  const int es = elem_size(dtype);
+  const int V = 16 / es;
+  const int ld = (int)(((int64_t)d * es + 15) / 16 * 16 / es);
+  const int ngroups = (d + V - 1) / V;
+  int NG = 1;
+  while (ngroups > 256 * NG) NG *= 2;
+  if (NG > 4) return false;
+  int T1 = 32;
+  while (T1 < 512 && T1 * NG < ngroups) T1 *= 2;
+  if (T1 * NG < ngroups) return false;
+  const int nw = T1 / 32;
+  const int stages = (int)env_int("HALP_FG_STAGES", 4);
+  int R = (int)env_int("HALP_FG_ROWS", 0);
+  if (R <= 0) {
+    R = 8;
+    const int reg_cap = std::min(255, 65536 / (T1 + 32));
+    auto regs = [&](int r) { return 2 * (2 * r * NG * V + 2 * NG * V + r) + 48; };
+    while (R > 1 && (regs(R) > reg_cap || (int64_t)R * ld * es > 32 * 1024 || !ws_shape_ok(nw, NG, R, stages))) R /= 2;
+  }
+  if (!ws_shape_ok(nw, NG, R, stages)) return false;
+  if (ws_smem_bytes(ld, es, nw, R, stages) > 110 * 1024) return false;
+  *out = FgLaunch{dtype, NG, C, T1, ld, 0, 6, R, stages, 1};
+  return true;
+}
+
+// K1 warp-per-row plan (k_fullgrad_rows.cu): rows of <= 32 x GPL sixteen-byte
+// groups, GPL <= 4; 8 warps per CTA, each on its own MIRROR split.
+bool rows_shape_ok(int gpl, int nwc, int rt, int st) {
+#define HALP_ROWS_OK(GPL, NWC, RT, ST) \
+  if (gpl == GPL && nwc == NWC && rt == RT && st == ST) return true;
+  HALP_ROWS_SHAPES(HALP_ROWS_OK)
+#undef HALP_ROWS_OK
+  return false;
+}
+
+bool plan_rows(int d, int C, int dtype, FgLaunch* out) {
+  // opt-in (HALP_FG_WARPROWS=1): measured slower than the streaming kernels at C4
+  if (C > 2 || env_int("HALP_FG_GENERIC", 0) != 0 || env_int("HALP_FG_WARPROWS", 0) == 0) return false;
+  const int es = elem_size(dtype);
+  const int V = 16 / es;
+  const int ld = (int)(((int64_t)d * es + 15) / 16 * 16 / es);
+  const int ngroups = (d + V - 1) / V;
+  int gpl = 1;
+  while (32 * gpl < ngroups) gpl *= 2;
+  if (gpl > 4) return false;
+  const int nwc = 8;
+  static const int pref[][2] = {{4, 4}, {2, 4}, {2, 3}, {1, 6}};
+  for (const auto& c : pref) {
+    if (!rows_shape_ok(gpl, nwc, c[0], c[1])) continue;
+    if (rows_smem_bytes(ld, es, d, nwc, c[0], c[1]) > 220 * 1024) continue;
+    *out = FgLaunch{dtype, gpl, C, nwc * 32, ld, 0, 5, c[0], c[1], nwc};
+    return true;
+  }
+  return false;
+}
+
+// MIRROR splits per launched split for this shape (the K1 plan's `sub`)
+int fg_sub_for(int d, int C, int dtype) {
+  FgLaunch fl;
+  return plan_rows(d, C, dtype, &fl) ? fl.sub : 1;
+}
+
+ShardPlan shard_plan_for(int64_t n, int d, int C, int dtype, int world, int rank) {
+  return make_shard_plan(n, d, C, dtype, world, rank, fg_sub_for(d, C, dtype));
+}
+
 // kernel plan as a pure function of the problem shape (CPU-callable)
 int plan_for(int64_t n, int d, int C, int dtype, KernelPlan* kp) {
   (void)n;
@@ -291,10 +381,11 @@ int plan_for(int64_t n, int d, int C, int dtype, KernelPlan* kp) {
   if (CT > C) CT = (int)next_pow2(C);
   kp->fg = FgLaunch{dtype, NG, CT, T1, ld, 0, 0, 2, 4};
   kp->fg_passes = (C + CT - 1) / CT;
-  // persistent streaming kernel (C <= 2; HALP_FG_GENERIC=1 forces the generic kernel for least squares)
+  // narrow rows: one warp per row; else the persistent streaming kernel
+  // (C <= 2; HALP_FG_GENERIC=1 forces the generic kernel for least squares)
   if (C <= 2 && env_int("HALP_FG_GENERIC", 0) == 0) {
     FgLaunch fl;
-    if (plan_stream(d, C, dtype, &fl)) {
+    if (plan_rows(d, C, dtype, &fl) || plan_ws(d, C, dtype, &fl) || plan_stream(d, C, dtype, &fl)) {
       kp->fg = fl;
       kp->fg_passes = 1;
     } else if (C == 2) {
@@ -306,7 +397,7 @@ int plan_for(int64_t n, int d, int C, int dtype, KernelPlan* kp) {
   } else {
     const size_t smem = fg_smem_bytes(ld, es, d * C, C, T1, 2, 4);
     // softmax with 3..15 classes: one-pass kernel with a 32-slot reduce-scatter
-    const int64_t S_ = make_shard_plan(n, d, C, dtype, 1, 0).S;
+    const int64_t S_ = make_shard_plan(n, d, C, dtype, 1, 0, 1).S;
     const int Ts = (int)((ngroups + 31) / 32 * 32);
     if (C >= 3 && ngroups <= 256 && V * C <= 64 && !(es == 2 && C < 8) && env_int("HALP_FG_GENERIC", 0) == 0 &&
         smx_smem_bytes(ld, es, d, C, Ts, (n + S_ - 1) / S_ + 1) <= 220 * 1024) {
@@ -363,7 +454,7 @@ int choose_plans(halp_problem* p) {
 
 int ensure_workspace(halp_problem* p) {
   const int64_t D1 = p->D + 1;
-  const int64_t nloc = p->sp.split_end - p->sp.split_begin;
+  const int64_t nloc = p->sp.cta_splits();
   if (!p->w) {
     cudaStream_t st = p->stream;
     CU(dalloc(&p->w, sizeof(double) * p->D, st));
@@ -391,15 +482,18 @@ int ensure_workspace(halp_problem* p) {
   return HALP_OK;
 }
 
+FgParams fg_params(const halp_problem* p, int pass) {
+  return FgParams{p->X, p->n, p->d, p->ld, p->C, p->loss, p->y, p->labels, p->w,
+                  (int)p->sp.S, (int)p->sp.split_begin, pass * p->fg.ct, pass == 0, p->partials, p->x_finite};
+}
+
 // K1 + split tree (+ all-gather) + finalize at p->w; stats -> host
 int full_pass(halp_problem* p, double* gn, double* delta, double* loss, double mu, int bits, double delta_min) {
   const int64_t D1 = p->D + 1;
-  const int nloc = (int)(p->sp.split_end - p->sp.split_begin);
+  const int nloc = (int)p->sp.cta_splits();
   CU(cudaEventRecord(p->ev_fg.a, p->stream));
   for (int pass = 0; pass < p->fg_passes; ++pass) {
-    FgParams fp{p->X, p->n, p->d, p->ld, p->C, p->loss, p->y, p->labels, p->w,
-                (int)p->sp.S, (int)p->sp.split_begin, pass * p->fg.ct, pass == 0, p->partials,
-                (int)env_int("HALP_FG_VARIANT", 0)};
+    FgParams fp = fg_params(p, pass);
     FgLaunch L = p->fg;
     L.nsplit_local = nloc;
     CU(launch_fullgrad(L, fp, p->stream));
@@ -496,7 +590,7 @@ int halp_shard_plan(int64_t n, int32_t d, int32_t C, int32_t dtype, int32_t worl
                     int64_t* split_end, int64_t* splits_total, int64_t* row_begin, int64_t* row_end) {
   if (n < 1 || d < 1 || C < 1 || world < 1 || rank < 0 || rank >= world || (world & (world - 1)))
     return fail(HALP_INVALID_INPUT, "halp_shard_plan: bad arguments (world must be a power of two)");
-  ShardPlan sp = make_shard_plan(n, d, C, dtype, world, rank);
+  ShardPlan sp = shard_plan_for(n, d, C, dtype, world, rank);
   *split_begin = sp.split_begin;
   *split_end = sp.split_end;
   *splits_total = sp.S;
@@ -512,8 +606,8 @@ int halp_plan_for(int64_t n, int32_t d, int32_t C, int32_t dtype, int32_t world,
   KernelPlan kp;
   int rc = plan_for(n, d, C, dtype, &kp);
   if (rc) return rc;
-  const ShardPlan sp = make_shard_plan(n, d, C, dtype, world, rank);
-  out->fg_threads = kp.fg.threads;
+  const ShardPlan sp = shard_plan_for(n, d, C, dtype, world, rank);
+  out->fg_threads = kp.fg.fast == 5 ? 32 : kp.fg.threads;  // the row dot's thread count (MIRROR)
   out->fg_vec = 16 / elem_size(dtype);
   out->fg_splits = (int32_t)sp.S;
   out->in_ctas = kp.in.ctas;
@@ -623,7 +717,7 @@ int halp_problem_create(const halp_problem_desc* desc, halp_problem** out) {
       return bail(fail(HALP_CUDA_ERROR, "copy of labels failed"));
     if (!dev_in) p->create_h2d += (int64_t)p->n * 4;
   }
-  p->sp = make_shard_plan(p->n, p->d, C, p->dtype, world, p->rank);
+  p->sp = shard_plan_for(p->n, p->d, C, p->dtype, world, p->rank);
   int rc = choose_plans(p);
   if (rc) return bail(rc);
   if (world > 1) {
@@ -636,6 +730,18 @@ int halp_problem_create(const halp_problem_desc* desc, halp_problem** out) {
   }
   rc = ensure_workspace(p);
   if (rc) return bail(rc);
+  // bf16 two-class sweeps may convert X with integer ops (k1_stream); that
+  // needs every element finite, checked once here on the device
+  if (p->dtype == HALP_BF16 && C == 2 && env_int("HALP_FG_F2F", 0) == 0) {
+    int* flag = nullptr;
+    int bad = 1;
+    if (dalloc(&flag, sizeof(int), p->stream) != cudaSuccess || cudaMemsetAsync(flag, 0, sizeof(int), p->stream) ||
+        launch_nonfinite_bf16(p->X, p->n * (int64_t)p->ld, flag, p->stream) ||
+        cudaMemcpyAsync(&bad, flag, sizeof(int), cudaMemcpyDeviceToHost, p->stream) ||
+        cudaStreamSynchronize(p->stream) || cudaFreeAsync(flag, p->stream))
+      return bail(fail(HALP_CUDA_ERROR, "finiteness check of X failed"));
+    p->x_finite = bad ? 0 : 1;
+  }
   // the caller may release its host buffers when create returns
   if (cudaStreamSynchronize(p->stream) != cudaSuccess) return bail(fail(HALP_CUDA_ERROR, "upload of the dataset failed"));
   p->timing.h2d_bytes = p->create_h2d;
@@ -647,7 +753,7 @@ void halp_problem_destroy(halp_problem* p) { delete p; }
 
 int halp_problem_plan(const halp_problem* p, halp_plan* out) {
   if (!p || !out) return fail(HALP_INVALID_INPUT, "halp_problem_plan: null argument");
-  out->fg_threads = p->fg.threads;
+  out->fg_threads = p->fg.fast == 5 ? 32 : p->fg.threads;
   out->fg_vec = 16 / elem_size(p->dtype);
   out->fg_splits = (int32_t)p->sp.S;
   out->in_ctas = p->in.ctas;
@@ -690,16 +796,14 @@ int halp_bench_full_gradient(halp_problem* p, int reps, double* ms_per_pass) {
   if (!p || reps < 1) return fail(HALP_INVALID_INPUT, "halp_bench_full_gradient: bad arguments");
   CU(cudaSetDevice(p->device));
   const int64_t D1 = p->D + 1;
-  const int nloc = (int)(p->sp.split_end - p->sp.split_begin);
+  const int nloc = (int)p->sp.cta_splits();
   cudaEvent_t a, b;
   CU(cudaEventCreate(&a));
   CU(cudaEventCreate(&b));
   CU(cudaEventRecord(a, p->stream));
   for (int r = 0; r < reps; ++r) {
     for (int pass = 0; pass < p->fg_passes; ++pass) {
-      FgParams fp{p->X, p->n, p->d, p->ld, p->C, p->loss, p->y, p->labels, p->w,
-                  (int)p->sp.S, (int)p->sp.split_begin, pass * p->fg.ct, pass == 0, p->partials,
-                (int)env_int("HALP_FG_VARIANT", 0)};
+      FgParams fp = fg_params(p, pass);
       FgLaunch L = p->fg;
       L.nsplit_local = nloc;
       CU(launch_fullgrad(L, fp, p->stream));
@@ -905,7 +1009,7 @@ extern "C" int halp_batch_create(const halp_batch_desc* desc, halp_batch** out) 
   };
   const int es = elem_size(b->dtype);
   b->ld = (int)(((int64_t)b->d * es + 15) / 16 * 16 / es);
-  b->splits = (int)std::max<int64_t>(4, make_shard_plan(b->n, b->d, 1, b->dtype, 1, 0).S);
+  b->splits = (int)std::max<int64_t>(4, make_shard_plan(b->n, b->d, 1, b->dtype, 1, 0, 1).S);
   const bool dev_in = desc->mem == HALP_MEM_DEVICE;
   const size_t rows_total = (size_t)b->nprob * b->n;
   if (cudaStreamCreateWithFlags(&b->stream, cudaStreamNonBlocking) != cudaSuccess)

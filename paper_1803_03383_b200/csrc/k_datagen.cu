@@ -125,4 +125,30 @@ cudaError_t launch_datagen(const GenParams& p, cudaStream_t st) {
   }
 }
 
+// any non-finite bf16 (exponent field all ones) -> *flag = 1; grid-stride,
+// 16-byte loads (problem creation only, for the K1 integer-conversion path)
+__global__ void k_nonfinite_bf16(const uint4* __restrict__ X, int64_t vecs, int* flag) {
+  int bad = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < vecs; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint4 v = X[i];
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) bad |= ((w[q] & 0x7F80u) == 0x7F80u) | ((w[q] & 0x7F800000u) == 0x7F800000u);
+  }
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flag, 1);
+}
+
+cudaError_t launch_nonfinite_bf16(const void* X, int64_t elems, int* flag, cudaStream_t st) {
+  // rows are padded to 16 bytes with zeros, so elems is a multiple of 8
+  const int64_t vecs = elems / 8;
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  int64_t blocks = (vecs + 255) / 256;
+  if (blocks > (int64_t)sms * 8) blocks = (int64_t)sms * 8;
+  if (blocks < 1) blocks = 1;
+  k_nonfinite_bf16<<<(int)blocks, 256, 0, st>>>(reinterpret_cast<const uint4*>(X), vecs, flag);
+  return cudaGetLastError();
+}
+
 }  // namespace halp

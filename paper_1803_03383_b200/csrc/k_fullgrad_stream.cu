@@ -28,6 +28,8 @@
 // "Reduction orders"): row dot = sequential fma over the thread's groups,
 // warp xor butterfly 16..1, warps summed in order; gradient column =
 // sequential fma over the split's rows; loss = sequential over the rows.
+#include <type_traits>
+
 #include "halp_device.cuh"
 #include "kernels.h"
 
@@ -59,6 +61,29 @@ __device__ __forceinline__ void load_group_k(const Tx* p, double* out) {
   } else {
     out[0] = __longlong_as_double(((long long)raw.y << 32) | raw.x);
     out[1] = __longlong_as_double(((long long)raw.w << 32) | raw.z);
+  }
+}
+
+// bf16 group -> fp64 scaled by 2^-896, with integer ops only (no F2F on the
+// XU pipe): the f32 pattern f of a bf16 maps to the double with the same sign,
+// exponent FIELD and leading mantissa bits, i.e. exactly x * 2^-896 for every
+// finite x (normal, subnormal, zero).  Used with w' = w * 2^896 and
+// dl' = dl * 2^896, products x'*w' and dl'*x' equal x*w and dl*x exactly,
+// so every fma rounds exactly as with the F2F-converted x.  Requires finite
+// x (checked at problem creation) and |w|, |dl| < 2^126 (checked per launch /
+// bounded by 1 for the two-class derivative).
+template <class Tx>
+__device__ __forceinline__ void load_group_scaled(const Tx* p, double* out) {
+  static_assert(sizeof(Tx) == 2, "bf16 only");
+  const uint4 raw = *reinterpret_cast<const uint4*>(p);
+  const uint32_t wds[4] = {raw.x, raw.y, raw.z, raw.w};
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const uint32_t w = wds[q];
+    const uint32_t hlo = ((w << 16) & 0x80000000u) | ((w << 13) & 0x0FFFE000u);
+    const uint32_t hhi = (w & 0x80000000u) | ((w >> 3) & 0x0FFFE000u);
+    out[2 * q] = __hiloint2double((int)hlo, 0);
+    out[2 * q + 1] = __hiloint2double((int)hhi, 0);
   }
 }
 
@@ -109,7 +134,8 @@ __global__ void __launch_bounds__(NW * 32, 1) k1_stream(FgParams p, int nloc) {
   const int64_t stage_elems = (int64_t)R * ld;
   Tx* stages = reinterpret_cast<Tx*>(smem);
   double* red = reinterpret_cast<double*>(smem + (size_t)STAGES * stage_elems * sizeof(Tx));  // [2][NW][NV]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(red + 2 * NW * NV);
+  double* lts = red + 2 * NW * NV;  // [2][R] per-row losses (two classes), parity double-buffered
+  uint64_t* bars = reinterpret_cast<uint64_t*>(lts + 2 * R);
   const Tx* X = reinterpret_cast<const Tx*>(p.X);
   const unsigned long long nn = (unsigned long long)p.n, SS = (unsigned long long)p.S;
 
@@ -124,12 +150,26 @@ __global__ void __launch_bounds__(NW * 32, 1) k1_stream(FgParams p, int nloc) {
       wr[k][q] = j >= d ? 0.0 : CC == 1 ? p.w[j] : p.w[d + j] - p.w[j];
     }
   }
+  // bf16 two-class sweeps convert x with integer ops in the 2^-896-scaled
+  // domain (load_group_scaled) when X is known finite and |w1 - w0| < 2^126
+  constexpr bool SCALE_OK = std::is_same<Tx, __nv_bfloat16>::value && CC == 2;
+  bool ok = SCALE_OK && p.x_finite;
+#pragma unroll
+  for (int k = 0; k < NG; ++k)
+#pragma unroll
+    for (int q = 0; q < V; ++q) ok = ok && fabs(wr[k][q]) < 0x1.0p126;
   if (tid == 0) {
 #pragma unroll
     for (int st = 0; st < STAGES; ++st) mbar_init(&bars[st], 1);
     fence_mbar_init();
   }
-  __syncthreads();
+  const bool scaled = __syncthreads_and(ok) != 0;
+  if (scaled) {
+#pragma unroll
+    for (int k = 0; k < NG; ++k)
+#pragma unroll
+      for (int q = 0; q < V; ++q) wr[k][q] = __dmul_rn(wr[k][q], 0x1.0p896);
+  }
 
   // ---- producer (thread 0): the CTA's tile sequence across its splits ----
   int ls_p = blockIdx.x;
@@ -165,6 +205,8 @@ __global__ void __launch_bounds__(NW * 32, 1) k1_stream(FgParams p, int nloc) {
   const int fr = lane;
   int64_t jseq = 0;  // consumer position in the CTA's tile sequence
 
+  auto run = [&](auto scaled_tag) {
+  constexpr bool SC = SCALE_OK && decltype(scaled_tag)::value;
 #pragma unroll 1
   for (int ls = blockIdx.x; ls < nloc; ls += gridDim.x) {
     const int64_t r0 = (int64_t)(nn * (unsigned long long)(p.split0 + ls) / SS);
@@ -176,17 +218,18 @@ __global__ void __launch_bounds__(NW * 32, 1) k1_stream(FgParams p, int nloc) {
 #pragma unroll
       for (int q = 0; q < V; ++q) gacc[k][q] = 0.0;
     double la = 0.0;
-    // targets of the slot rows, one tile ahead
-    double tgt = 0.0;
-    if (lane < NV && r0 + fr < r1) tgt = CC == 1 ? p.y[r0 + fr] : (double)p.labels[r0 + fr];
+    // targets of the slot rows, one tile ahead (kept raw: used one tile later)
+    using TgtT = std::conditional_t<CC == 1, double, int32_t>;
+    TgtT tgt = 0;
+    if (lane < NV && r0 + fr < r1) tgt = CC == 1 ? (TgtT)p.y[r0 + fr] : (TgtT)p.labels[r0 + fr];
 
 #pragma unroll 1
     for (int64_t i = 0; i < ntile; ++i, ++jseq) {
       const int64_t rowb = r0 + i * R;
       const int nr = (int)((r1 - rowb) < R ? (r1 - rowb) : R);
-      const double tcur = tgt;
+      const TgtT tcur = tgt;
       if (lane < NV && rowb + R + fr < r1)
-        tgt = CC == 1 ? p.y[rowb + R + fr] : (double)p.labels[rowb + R + fr];
+        tgt = CC == 1 ? (TgtT)p.y[rowb + R + fr] : (TgtT)p.labels[rowb + R + fr];
       const int st = (int)(jseq % STAGES);
       mbar_wait(&bars[st], (uint32_t)((jseq / STAGES) & 1));
       const Tx* xs = stages + st * stage_elems;
@@ -203,7 +246,8 @@ __global__ void __launch_bounds__(NW * 32, 1) k1_stream(FgParams p, int nloc) {
 #pragma unroll
           for (int k = 0; k < NG; ++k) {
             if ((FULL || r < nr) && gval[k]) {
-              load_group_k<Tx>(xs + (int64_t)r * ld + (tid + k * T1) * V, xr[r][k]);
+              if constexpr (SC) load_group_scaled<Tx>(xs + (int64_t)r * ld + (tid + k * T1) * V, xr[r][k]);
+              else load_group_k<Tx>(xs + (int64_t)r * ld + (tid + k * T1) * V, xr[r][k]);
             } else {
 #pragma unroll
               for (int q = 0; q < V; ++q) xr[r][k][q] = 0.0;
@@ -242,15 +286,23 @@ __global__ void __launch_bounds__(NW * 32, 1) k1_stream(FgParams p, int nloc) {
           const double den = 1.0 + q;
           const double p0 = (lg > 0.0 ? q : 1.0) / den;
           pr = lab == 0 ? p0 - 1.0 : p0;
-          if (wid == 0 && lane < NV) {
+          if constexpr (SC) pr = __dmul_rn(pr, 0x1.0p896);  // |pr| <= 1: exact
+          // the loss terms (a log per row) rotate over the warps; warp 0 sums
+          // them in row order one tile later (after the next barrier)
+          if (wid == (int)(jseq % NW) && lane < NV) {
             const double a = lab == 0 ? lg : -lg;
-            lt = (a > 0.0 ? a : 0.0) + hlog(den);
+            lts[(jseq & 1) * R + lane] = (a > 0.0 ? a : 0.0) + hlog(den);
+          }
+          if (wid == 0 && i > 0) {
+            const double* lp = lts + ((jseq - 1) & 1) * R;  // previous tile: full
+#pragma unroll
+            for (int r = 0; r < R; ++r) la = la + lp[r];
           }
         }
         double dlr[NV];
 #pragma unroll
         for (int v = 0; v < NV; ++v) dlr[v] = __shfl_sync(0xffffffffu, pr, v);
-        if (wid == 0) {
+        if (CC == 1 && wid == 0) {
 #pragma unroll
           for (int r = 0; r < R; ++r) {
             const double t = __shfl_sync(0xffffffffu, lt, r);
@@ -270,6 +322,14 @@ __global__ void __launch_bounds__(NW * 32, 1) k1_stream(FgParams p, int nloc) {
       if (nr == R) body(BoolTag<true>{});
       else body(BoolTag<false>{});
     }
+    if constexpr (CC == 2) {  // the split's last tile's loss terms
+      __syncthreads();
+      if (wid == 0 && ntile > 0) {
+        const int nr_last = (int)(r1 - (r0 + (ntile - 1) * R));
+        const double* lp = lts + ((jseq - 1) & 1) * R;
+        for (int r = 0; r < nr_last; ++r) la = la + lp[r];
+      }
+    }
 
     double* out = p.partials + (size_t)ls * (D + 1);
 #pragma unroll
@@ -288,6 +348,9 @@ __global__ void __launch_bounds__(NW * 32, 1) k1_stream(FgParams p, int nloc) {
     }
     if (tid == 0) out[D] = la;
   }
+  };
+  if (scaled) run(BoolTag<true>{});
+  else run(BoolTag<false>{});
 }
 
 // ------------------------------------------------------------------ dispatch
@@ -295,7 +358,7 @@ size_t stream_smem_bytes(int ld, int elem, int warps, int R, int CC, int stages)
   size_t b = (size_t)stages * R * ld * elem;
   b = (b + 15) / 16 * 16;
   (void)CC;
-  b += (size_t)2 * warps * R * 8 + (size_t)stages * 8;
+  b += (size_t)2 * warps * R * 8 + (size_t)2 * R * 8 + (size_t)stages * 8;
   return b;
 }
 

@@ -79,6 +79,48 @@ def test_fullgrad_softmax_bitexact(H, oracle, C, d, n):
     assert abs(gl - o.loss_value(w)) <= 1e-12 * abs(gl)
 
 
+@pytest.mark.parametrize("d,n", [(1024, 4096), (200, 3001), (24, 517)])
+def test_fullgrad_two_class_bf16_integer_conversion(H, oracle, d, n):
+    """bf16 two-class sweeps convert x with integer ops in the 2^-896-scaled
+    domain (k_fullgrad_stream.cu load_group_scaled).  Bit-identical to the
+    oracle's exact upcast on data that exercises every bf16 class: zeros of
+    both signs, subnormals, the smallest / largest normal exponents."""
+    rng = np.random.default_rng(d)
+    X = rng.standard_normal((n, d)) / np.sqrt(d)
+    X[rng.random((n, d)) < 0.1] = 0.0
+    X[rng.random((n, d)) < 0.02] *= 2.0 ** -130  # bf16 subnormals
+    X[rng.random((n, d)) < 0.01] *= 2.0 ** 100
+    Xb = bf16_bits(X)
+    Xb[0, 0] = 0x8000  # -0.0
+    Xb[1, 1] = 0x0001  # smallest subnormal
+    Xb[2, 2] = 0x7F7F  # largest finite
+    lab = rng.integers(0, 2, n).astype(np.int32)
+    g, o = objs(H, oracle, Xb, labels=lab, C=2, l2=1e-5)
+    plan = g.oracle_plan()
+    for w in (rng.standard_normal(2 * d) * 1e-3, np.zeros(2 * d), rng.standard_normal(2 * d) * 1e30):
+        gg, gl = g._fullpass(w)
+        assert np.array_equal(gg, o.full_gradient(w, plan=plan))
+        assert gl == o.loss_value(w, plan=plan)
+
+
+def test_fullgrad_two_class_bf16_nonfinite_x(H, oracle):
+    """A non-finite x disables the integer conversion (checked at creation):
+    results follow IEEE arithmetic exactly like the oracle's (NaN / inf)."""
+    rng = np.random.default_rng(3)
+    n, d = 600, 64
+    X = rng.standard_normal((n, d))
+    Xb = bf16_bits(X)
+    Xb[5, 7] = 0x7F80  # +inf
+    lab = rng.integers(0, 2, n).astype(np.int32)
+    g, o = objs(H, oracle, Xb, labels=lab, C=2, l2=0.0)
+    w = rng.standard_normal(2 * d)
+    gg, gl = g._fullpass(w)
+    og = o.full_gradient(w, plan=g.oracle_plan())
+    assert np.array_equal(gg, og, equal_nan=True)
+    ol = o.loss_value(w, plan=g.oracle_plan())
+    assert gl == ol or (math.isnan(gl) and math.isnan(ol))
+
+
 def rows_equal(grows, orows):
     assert len(grows) == len(orows)
     for a, b in zip(grows, orows):

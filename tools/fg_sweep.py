@@ -13,12 +13,16 @@ if w == "c3":
     n, d = 4194304, 4096
     X, y = H.generate("regression", n, d, dtype="f32", noise_sd=0.1, seed=3)
     obj = H.Objective(H.Dataset(X, targets=y), H.LossFamily.Squared, 0.0); b = n * d * 4 + n * 8
+elif w == "c1":
+    n, d = 8192, 256
+    X, y = H.generate("regression", n, d, dtype="f32", noise_sd=0.01, seed=0)
+    obj = H.Objective(H.Dataset(X, targets=y), H.LossFamily.Squared, 0.0); b = n * d * 4 + n * 8
 else:
     n, d = 16777216, 1024
     X, y = H.generate("logistic", n, d, dtype="bf16", x_scale=d ** -0.5, seed=4)
     obj = H.Objective(H.Dataset(X, labels=y, num_classes=2), H.LossFamily.Softmax, 1e-5); b = n * d * 2 + n * 4
 obj.bench_full_gradient(2)
-ms = obj.bench_full_gradient(10)
+ms = obj.bench_full_gradient(10 if w != "c1" else 200)
 p = obj.plan()
 print("RESULT %s %.3f ms %.1f GB/s frac %.3f plan thr=%d rows=%d stages=%d splits=%d" % (
     w, ms, b / ms / 1e6, b / ms / 1e6 / 6553.3, p["fg_threads"], p["fg_rows_per_stage"], p["fg_stages"], p["fg_splits"]))
