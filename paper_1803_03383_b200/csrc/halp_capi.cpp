@@ -82,16 +82,13 @@ struct Nccl {
 
 struct ShardPlan {
   int64_t S = 1, split_begin = 0, split_end = 1, row_begin = 0, row_end = 0;
-  int sub = 1;
-  int64_t cta_splits() const { return (split_end - split_begin) / sub; }
+  int64_t local_splits() const { return split_end - split_begin; }
 };
 
-// Split grid of the full-gradient pass.  S counts MIRROR splits (the leaves
-// of the pairwise reduction tree); a launched CTA split covers `sub` of them
-// (the warp-per-row kernel combines its warps' splits on chip), and one
-// (D+1) partial is written per CTA split: S/sub of them, <= 4096, within an
-// eighth of X's bytes.  Ranks own aligned, equal blocks of CTA splits.
-ShardPlan make_shard_plan(int64_t n, int d, int C, int dtype, int world, int rank, int sub) {
+// Split grid of the full-gradient pass: S splits (the leaves of the pairwise
+// reduction tree, one (D+1) partial each), a power of two <= 4096 within an
+// eighth of X's bytes; ranks own aligned, equal blocks of splits.
+ShardPlan make_shard_plan(int64_t n, int d, int C, int dtype, int world, int rank) {
   ShardPlan sp;
   const int64_t D1 = (int64_t)d * C + 1;
   const double xbytes = (double)n * d * elem_size(dtype);
@@ -99,11 +96,9 @@ ShardPlan make_shard_plan(int64_t n, int d, int C, int dtype, int world, int ran
   int64_t S = 1;
   while (S * 2 <= 4096 && S * 2 <= std::max<int64_t>(1, n / 2) && (double)(S * 2) * D1 * 8.0 <= budget) S *= 2;
   if (S < world) S = next_pow2(world);
-  sub = std::max(1, sub);
-  sp.S = S * sub;
-  sp.sub = sub;
-  sp.split_begin = S / world * rank * sub;
-  sp.split_end = S / world * (rank + 1) * sub;
+  sp.S = S;
+  sp.split_begin = S / world * rank;
+  sp.split_end = S / world * (rank + 1);
   sp.row_begin = (int64_t)((unsigned __int128)n * sp.split_begin / sp.S);
   sp.row_end = (int64_t)((unsigned __int128)n * sp.split_end / sp.S);
   return sp;
@@ -286,84 +281,8 @@ bool plan_stream(int d, int C, int dtype, FgLaunch* out) {
   return true;
 }
 
-// K1 two-class plan (k_fullgrad_ws.cu): the streaming kernel's thread layout
-// plus a finisher warp; R by the register budget of two x buffers.
-bool ws_shape_ok(int nw, int ng, int r, int st) {
-#define HALP_WS_OK(NW, NG, R, ST) \
-  if (nw == NW && ng == NG && r == R && st == ST) return true;
-  HALP_WS_SHAPES(HALP_WS_OK)
-#undef HALP_WS_OK
-  return false;
-}
-
-bool plan_ws(int d, int C, int dtype, FgLaunch* out) {
-  // opt-in (HALP_FG_WS=1): the single finisher warp's dependent chain
-  // (~370 instructions per 4-row tile) bounds it below the streaming kernel
-  if (C != 2 || env_int("HALP_FG_WS", 0) == 0) return false;
-  const int es = elem_size(dtype);
-  const int V = 16 / es;
-  const int ld = (int)(((int64_t)d * es + 15) / 16 * 16 / es);
-  const int ngroups = (d + V - 1) / V;
-  int NG = 1;
-  while (ngroups > 256 * NG) NG *= 2;
-  if (NG > 4) return false;
-  int T1 = 32;
-  while (T1 < 512 && T1 * NG < ngroups) T1 *= 2;
-  if (T1 * NG < ngroups) return false;
-  const int nw = T1 / 32;
-  const int stages = (int)env_int("HALP_FG_STAGES", 4);
-  int R = (int)env_int("HALP_FG_ROWS", 0);
-  if (R <= 0) {
-    R = 8;
-    const int reg_cap = std::min(255, 65536 / (T1 + 32));
-    auto regs = [&](int r) { return 2 * (2 * r * NG * V + 2 * NG * V + r) + 48; };
-    while (R > 1 && (regs(R) > reg_cap || (int64_t)R * ld * es > 32 * 1024 || !ws_shape_ok(nw, NG, R, stages))) R /= 2;
-  }
-  if (!ws_shape_ok(nw, NG, R, stages)) return false;
-  if (ws_smem_bytes(ld, es, nw, R, stages) > 110 * 1024) return false;
-  *out = FgLaunch{dtype, NG, C, T1, ld, 0, 6, R, stages, 1};
-  return true;
-}
-
-// K1 warp-per-row plan (k_fullgrad_rows.cu): rows of <= 32 x GPL sixteen-byte
-// groups, GPL <= 4; 8 warps per CTA, each on its own MIRROR split.
-bool rows_shape_ok(int gpl, int nwc, int rt, int st) {
-#define HALP_ROWS_OK(GPL, NWC, RT, ST) \
-  if (gpl == GPL && nwc == NWC && rt == RT && st == ST) return true;
-  HALP_ROWS_SHAPES(HALP_ROWS_OK)
-#undef HALP_ROWS_OK
-  return false;
-}
-
-bool plan_rows(int d, int C, int dtype, FgLaunch* out) {
-  // opt-in (HALP_FG_WARPROWS=1): measured slower than the streaming kernels at C4
-  if (C > 2 || env_int("HALP_FG_GENERIC", 0) != 0 || env_int("HALP_FG_WARPROWS", 0) == 0) return false;
-  const int es = elem_size(dtype);
-  const int V = 16 / es;
-  const int ld = (int)(((int64_t)d * es + 15) / 16 * 16 / es);
-  const int ngroups = (d + V - 1) / V;
-  int gpl = 1;
-  while (32 * gpl < ngroups) gpl *= 2;
-  if (gpl > 4) return false;
-  const int nwc = 8;
-  static const int pref[][2] = {{4, 4}, {2, 4}, {2, 3}, {1, 6}};
-  for (const auto& c : pref) {
-    if (!rows_shape_ok(gpl, nwc, c[0], c[1])) continue;
-    if (rows_smem_bytes(ld, es, d, nwc, c[0], c[1]) > 220 * 1024) continue;
-    *out = FgLaunch{dtype, gpl, C, nwc * 32, ld, 0, 5, c[0], c[1], nwc};
-    return true;
-  }
-  return false;
-}
-
-// MIRROR splits per launched split for this shape (the K1 plan's `sub`)
-int fg_sub_for(int d, int C, int dtype) {
-  FgLaunch fl;
-  return plan_rows(d, C, dtype, &fl) ? fl.sub : 1;
-}
-
 ShardPlan shard_plan_for(int64_t n, int d, int C, int dtype, int world, int rank) {
-  return make_shard_plan(n, d, C, dtype, world, rank, fg_sub_for(d, C, dtype));
+  return make_shard_plan(n, d, C, dtype, world, rank);
 }
 
 // kernel plan as a pure function of the problem shape (CPU-callable)
@@ -381,11 +300,10 @@ int plan_for(int64_t n, int d, int C, int dtype, KernelPlan* kp) {
   if (CT > C) CT = (int)next_pow2(C);
   kp->fg = FgLaunch{dtype, NG, CT, T1, ld, 0, 0, 2, 4};
   kp->fg_passes = (C + CT - 1) / CT;
-  // narrow rows: one warp per row; else the persistent streaming kernel
-  // (C <= 2; HALP_FG_GENERIC=1 forces the generic kernel for least squares)
+  // persistent streaming kernel (C <= 2; HALP_FG_GENERIC=1 forces the generic kernel for least squares)
   if (C <= 2 && env_int("HALP_FG_GENERIC", 0) == 0) {
     FgLaunch fl;
-    if (plan_rows(d, C, dtype, &fl) || plan_ws(d, C, dtype, &fl) || plan_stream(d, C, dtype, &fl)) {
+    if (plan_stream(d, C, dtype, &fl)) {
       kp->fg = fl;
       kp->fg_passes = 1;
     } else if (C == 2) {
@@ -397,7 +315,7 @@ int plan_for(int64_t n, int d, int C, int dtype, KernelPlan* kp) {
   } else {
     const size_t smem = fg_smem_bytes(ld, es, d * C, C, T1, 2, 4);
     // softmax with 3..15 classes: one-pass kernel with a 32-slot reduce-scatter
-    const int64_t S_ = make_shard_plan(n, d, C, dtype, 1, 0, 1).S;
+    const int64_t S_ = make_shard_plan(n, d, C, dtype, 1, 0).S;
     const int Ts = (int)((ngroups + 31) / 32 * 32);
     if (C >= 3 && ngroups <= 256 && V * C <= 64 && !(es == 2 && C < 8) && env_int("HALP_FG_GENERIC", 0) == 0 &&
         smx_smem_bytes(ld, es, d, C, Ts, (n + S_ - 1) / S_ + 1) <= 220 * 1024) {
@@ -454,7 +372,7 @@ int choose_plans(halp_problem* p) {
 
 int ensure_workspace(halp_problem* p) {
   const int64_t D1 = p->D + 1;
-  const int64_t nloc = p->sp.cta_splits();
+  const int64_t nloc = p->sp.local_splits();
   if (!p->w) {
     cudaStream_t st = p->stream;
     CU(dalloc(&p->w, sizeof(double) * p->D, st));
@@ -490,7 +408,7 @@ FgParams fg_params(const halp_problem* p, int pass) {
 // K1 + split tree (+ all-gather) + finalize at p->w; stats -> host
 int full_pass(halp_problem* p, double* gn, double* delta, double* loss, double mu, int bits, double delta_min) {
   const int64_t D1 = p->D + 1;
-  const int nloc = (int)p->sp.cta_splits();
+  const int nloc = (int)p->sp.local_splits();
   CU(cudaEventRecord(p->ev_fg.a, p->stream));
   for (int pass = 0; pass < p->fg_passes; ++pass) {
     FgParams fp = fg_params(p, pass);
@@ -607,7 +525,7 @@ int halp_plan_for(int64_t n, int32_t d, int32_t C, int32_t dtype, int32_t world,
   int rc = plan_for(n, d, C, dtype, &kp);
   if (rc) return rc;
   const ShardPlan sp = shard_plan_for(n, d, C, dtype, world, rank);
-  out->fg_threads = kp.fg.fast == 5 ? 32 : kp.fg.threads;  // the row dot's thread count (MIRROR)
+  out->fg_threads = kp.fg.threads;
   out->fg_vec = 16 / elem_size(dtype);
   out->fg_splits = (int32_t)sp.S;
   out->in_ctas = kp.in.ctas;
@@ -753,7 +671,7 @@ void halp_problem_destroy(halp_problem* p) { delete p; }
 
 int halp_problem_plan(const halp_problem* p, halp_plan* out) {
   if (!p || !out) return fail(HALP_INVALID_INPUT, "halp_problem_plan: null argument");
-  out->fg_threads = p->fg.fast == 5 ? 32 : p->fg.threads;
+  out->fg_threads = p->fg.threads;
   out->fg_vec = 16 / elem_size(p->dtype);
   out->fg_splits = (int32_t)p->sp.S;
   out->in_ctas = p->in.ctas;
@@ -796,7 +714,7 @@ int halp_bench_full_gradient(halp_problem* p, int reps, double* ms_per_pass) {
   if (!p || reps < 1) return fail(HALP_INVALID_INPUT, "halp_bench_full_gradient: bad arguments");
   CU(cudaSetDevice(p->device));
   const int64_t D1 = p->D + 1;
-  const int nloc = (int)p->sp.cta_splits();
+  const int nloc = (int)p->sp.local_splits();
   cudaEvent_t a, b;
   CU(cudaEventCreate(&a));
   CU(cudaEventCreate(&b));
@@ -1009,7 +927,7 @@ extern "C" int halp_batch_create(const halp_batch_desc* desc, halp_batch** out) 
   };
   const int es = elem_size(b->dtype);
   b->ld = (int)(((int64_t)b->d * es + 15) / 16 * 16 / es);
-  b->splits = (int)std::max<int64_t>(4, make_shard_plan(b->n, b->d, 1, b->dtype, 1, 0, 1).S);
+  b->splits = (int)std::max<int64_t>(4, make_shard_plan(b->n, b->d, 1, b->dtype, 1, 0).S);
   const bool dev_in = desc->mem == HALP_MEM_DEVICE;
   const size_t rows_total = (size_t)b->nprob * b->n;
   if (cudaStreamCreateWithFlags(&b->stream, cudaStreamNonBlocking) != cudaSuccess)

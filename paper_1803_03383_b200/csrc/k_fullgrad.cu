@@ -329,8 +329,6 @@ size_t fg_smem_bytes(int ld, int elem, int D, int C, int threads, int R, int sta
 cudaError_t launch_fullgrad(const FgLaunch& L, const FgParams& p, cudaStream_t st) {
   if (L.fast == 3) return launch_fullgrad_smx(L, p, st);
   if (L.fast == 4) return launch_fullgrad_stream(L, p, st);
-  if (L.fast == 5) return launch_fullgrad_rows(L, p, st);
-  if (L.fast == 6) return launch_fullgrad_ws(L, p, st);
   switch (L.dtype) {
     case 0: return launch_fg_dt<double>(L, p, st);
     case 1: return launch_fg_dt<float>(L, p, st);

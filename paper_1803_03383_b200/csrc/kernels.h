@@ -22,10 +22,7 @@ struct FgParams {
 };
 struct FgLaunch {
   int dtype, ng, ct, threads, ld, nsplit_local;
-  int fast, rows, stages;  // fast: 0 generic, 3 softmax C >= 3, 4 streaming C <= 2, 5 warp-per-row C <= 2,
-                           // 6 two-class warp-specialized;
-                           // rows per tile, ring depth
-  int sub;                 // MIRROR splits per launched split (warp-per-row kernel: warps per CTA), 0 = 1
+  int fast, rows, stages;  // fast: 0 generic, 3 softmax C >= 3, 4 streaming C <= 2; rows per tile, ring depth
 };
 size_t fg_smem_bytes(int ld, int elem, int D, int C, int threads, int R, int stages);
 cudaError_t launch_fullgrad(const FgLaunch& L, const FgParams& p, cudaStream_t st);
@@ -43,17 +40,6 @@ cudaError_t launch_fullgrad_smx(const FgLaunch& L, const FgParams& p, cudaStream
   X(8, 4, 2, 4) X(16, 4, 1, 4) X(16, 2, 2, 6) X(8, 2, 2, 6) X(8, 4, 2, 6) X(4, 1, 4, 6)
 size_t stream_smem_bytes(int ld, int elem, int warps, int R, int CC, int stages);
 cudaError_t launch_fullgrad_stream(const FgLaunch& L, const FgParams& p, cudaStream_t st);
-// two-class warp-specialized pipeline (FgLaunch.fast == 6), k_fullgrad_ws.cu.
-// Shapes (NW compute warps, NG groups/thread, R rows/tile, ring depth); one extra finisher warp.
-// (wider rows spill the two x buffers: they take the streaming kernel)
-#define HALP_WS_SHAPES(X) X(1, 1, 4, 4) X(2, 1, 4, 4) X(4, 1, 4, 4) X(4, 1, 4, 6) X(4, 1, 2, 4) X(8, 1, 2, 4)
-size_t ws_smem_bytes(int ld, int elem, int warps, int R, int stages);
-cudaError_t launch_fullgrad_ws(const FgLaunch& L, const FgParams& p, cudaStream_t st);
-// warp-per-row kernel for narrow rows (FgLaunch.fast == 5), k_fullgrad_rows.cu.
-// Shapes (GPL groups per lane, NWC warps = splits per CTA, RT rows/tile, ring depth).
-#define HALP_ROWS_SHAPES(X) X(1, 8, 4, 4) X(2, 8, 4, 4) X(2, 8, 2, 4) X(4, 8, 2, 4) X(4, 8, 1, 6) X(4, 8, 2, 3)
-size_t rows_smem_bytes(int ld, int elem, int d, int warps, int RT, int stages);
-cudaError_t launch_fullgrad_rows(const FgLaunch& L, const FgParams& p, cudaStream_t st);
 cudaError_t launch_split_tree(const double* partials, int nsplit, int D1, double* out, double* scratch,
                               cudaStream_t st);
 
