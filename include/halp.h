@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define HALP_ABI_VERSION 1
+#define HALP_ABI_VERSION 2
 
 typedef enum {
   HALP_OK = 0,
@@ -163,15 +163,17 @@ int halp_bench_full_gradient(halp_problem* p, int reps, double* ms_per_pass);
 
 /* ---- batched independent problems (one persistent CTA per problem) ---- */
 typedef struct {
-  const void*   X;           /* [nprob][n][d] row-major */
+  const void*   X;           /* [nprob][n][d] row-major, or [n][d] when shared */
   int32_t       dtype;
   int32_t       mem;
   int64_t       n;
   int32_t       d;
   int32_t       nprob;
-  const double* y;           /* [nprob][n] */
+  const double* y;           /* [nprob][n], or [n] when shared */
   double        l2;
   int32_t       device;
+  int32_t       shared;      /* 1: every problem solves the SAME dataset (grid searches,
+                                harness.cpp:379-447) with its own config; ABI >= 2 */
 } halp_batch_desc;
 
 typedef struct halp_batch halp_batch;

@@ -67,7 +67,7 @@ class Plan(C.Structure):
 class BatchDesc(C.Structure):
     _fields_ = [
         ("X", C.c_void_p), ("dtype", C.c_int32), ("mem", C.c_int32), ("n", C.c_int64), ("d", C.c_int32),
-        ("nprob", C.c_int32), ("y", C.c_void_p), ("l2", C.c_double), ("device", C.c_int32),
+        ("nprob", C.c_int32), ("y", C.c_void_p), ("l2", C.c_double), ("device", C.c_int32), ("shared", C.c_int32),
     ]
 
 

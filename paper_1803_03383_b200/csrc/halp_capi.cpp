@@ -888,6 +888,7 @@ extern "C" int halp_datagen(const halp_datagen_desc* desc, int32_t device, void*
 
 struct halp_batch {
   int device = 0, dtype = 0, d = 0, ld = 0, nprob = 0, splits = 4;
+  bool shared = false;
   int64_t n = 0;
   double l2 = 0.0;
   void* X = nullptr;
@@ -929,7 +930,8 @@ extern "C" int halp_batch_create(const halp_batch_desc* desc, halp_batch** out) 
   b->ld = (int)(((int64_t)b->d * es + 15) / 16 * 16 / es);
   b->splits = (int)std::max<int64_t>(4, make_shard_plan(b->n, b->d, 1, b->dtype, 1, 0).S);
   const bool dev_in = desc->mem == HALP_MEM_DEVICE;
-  const size_t rows_total = (size_t)b->nprob * b->n;
+  b->shared = desc->shared != 0;
+  const size_t rows_total = (size_t)(b->shared ? 1 : b->nprob) * b->n;
   if (cudaStreamCreateWithFlags(&b->stream, cudaStreamNonBlocking) != cudaSuccess)
     return bail(fail(HALP_CUDA_ERROR, "cudaStreamCreate failed"));
   if (cudaMalloc(&b->X, rows_total * b->ld * es) != cudaSuccess) return bail(fail(HALP_CUDA_ERROR, "cudaMalloc(X)"));
@@ -1023,6 +1025,7 @@ extern "C" int halp_batch_run(halp_batch* b, const halp_config* cfgs, halp_recor
   bp.dtype = b->dtype;
   bp.n = b->n;
   bp.nprob = P;
+  bp.x_rows_per_prob = b->shared ? 0 : b->n;
   bp.y = b->y;
   bp.l2 = b->l2;
   bp.alpha = (const double*)dev(alpha.data(), 8 * P);

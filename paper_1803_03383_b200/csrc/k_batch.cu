@@ -75,8 +75,9 @@ __global__ void __launch_bounds__(128) k5_batch(BatchParams p) {
   const int d = p.d, D = d, ld = p.ld;
   const int64_t n = p.n;
   const int S = p.splits;
-  const Tx* X = reinterpret_cast<const Tx*>(p.X) + (size_t)prob * n * ld;
-  const double* y = p.y + (size_t)prob * n;
+  // own dataset per problem, or one dataset shared by all (grid searches: x_rows_per_prob = 0)
+  const Tx* X = reinterpret_cast<const Tx*>(p.X) + (size_t)prob * p.x_rows_per_prob * ld;
+  const double* y = p.y + (size_t)prob * p.x_rows_per_prob;
 
   __shared__ double w_s[264], g_s[264], wsum[4][257];  // iterate, g~, warp subtree roots (+loss)
   __shared__ double stats[4];

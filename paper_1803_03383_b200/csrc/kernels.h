@@ -106,7 +106,8 @@ struct BatchParams {
   int ld, d, dtype;
   int64_t n;
   int nprob;
-  const double* y;      // [nprob][n]
+  int64_t x_rows_per_prob;  // n (own data per problem) or 0 (one dataset shared by every problem)
+  const double* y;      // [nprob][n] or [n]
   double l2;
   const double* alpha;  // per problem
   const double* mu;

@@ -385,12 +385,144 @@ def run(obj: Objective, cfg: OptimizerConfig) -> RunRecord:
     raise UnsupportedError(f"algorithm {Algorithm(cfg.algorithm).name} is not on the B200 hot path")
 
 
-def run_prepared(obj: Objective, cfg: OptimizerConfig) -> RunRecord:
-    """harness.cpp:296-312: a diverged run is returned, not raised."""
+def run_prepared(obj: Objective, cfg: OptimizerConfig, data_seed: int = 0) -> RunRecord:
+    """harness.cpp:296-312: a diverged run is returned, not raised.  data_seed
+    only feeds LM-HALP's dataset quantization (not on the B200 path)."""
+    del data_seed
     try:
         return run(obj, cfg)
     except DivergenceError as e:
         return e.partial
+
+
+# ---------------------------------------------------------------- grid search
+@dataclass
+class GridAxis:
+    """lpopt::GridAxis (harness.hpp:92-95)."""
+
+    param: str
+    values: List[float]
+
+
+@dataclass
+class GridOutcome:
+    """lpopt::GridOutcome (harness.hpp:97-102)."""
+
+    params: dict = field(default_factory=dict)
+    per_seed: List[float] = field(default_factory=list)  # +inf for diverged seeds
+    mean_metric: float = 0.0
+    status: str = "ok"
+
+
+@dataclass
+class GridResult:
+    """lpopt::GridResult (harness.hpp:104-108)."""
+
+    points: List[GridOutcome] = field(default_factory=list)
+    best_index: int = 0
+    best_config: Optional[OptimizerConfig] = None
+
+
+def _apply_param(cfg: OptimizerConfig, param: str, v: float) -> None:
+    """harness.cpp:45-61"""
+    if param == "alpha":
+        cfg.alpha = v
+    elif param == "delta":
+        cfg.delta = v
+    elif param == "mu":
+        cfg.mu = v
+    elif param == "bits":
+        cfg.bits = int(_llround(v))
+    elif param == "epochs":
+        cfg.epochs = int(_llround(v))
+    elif param == "inner":
+        cfg.inner_steps = int(_llround(v))
+    else:
+        raise InvalidInputError(f"grid: unknown parameter '{param}'")
+
+
+def _llround(v: float) -> int:
+    """std::llround: halves away from zero"""
+    return int(math.floor(v + 0.5)) if v >= 0 else -int(math.floor(-v + 0.5))
+
+
+def _final_metric(rec: RunRecord, metric: str) -> float:
+    """harness.cpp:63-66"""
+    if not rec.rows:
+        return math.inf
+    return rec.rows[-1].loss if metric == "loss" else rec.rows[-1].grad_norm
+
+
+def _batchable(obj: Objective, cfgs) -> bool:
+    return (obj.loss_family() == LossFamily.Squared and obj.dim() <= 256 and obj.ds.X is not None
+            and all(c.algorithm == Algorithm.Halp for c in cfgs))
+
+
+def grid_search(obj: Objective, base: OptimizerConfig, axes, seeds, metric: str = "grad_norm",
+                data_seed: int = 0) -> GridResult:
+    """lpopt::grid_search (harness.cpp:379-447): exhaustive Cartesian search,
+    axes in name order with the listed value order (last axis fastest), the
+    seed-mean of the final metric per point, diverged seeds count as +inf, and
+    the first point reaching the minimum wins.  Every (point, seed) run is an
+    independent run_prepared; on the B200 they all run at once -- one K5
+    launch over the objective's dataset shared by every run (least squares,
+    d <= 256) -- or one after another through run_prepared otherwise.  The
+    records are the reference's per run (bit-identical to the oracle's MIRROR
+    runs with the batch plan), so the outcome is."""
+    if metric not in ("grad_norm", "loss"):
+        raise InvalidInputError("grid: metric must be grad_norm or loss")
+    seeds = [int(s) for s in seeds]
+    if not seeds:
+        raise InvalidInputError("grid: need at least one seed")
+    axes = sorted((GridAxis(a.param, list(a.values)) for a in axes), key=lambda a: a.param)
+    for i, a in enumerate(axes):
+        if not a.values:
+            raise InvalidInputError(f"grid: axis '{a.param}' has no values")
+        if i > 0 and a.param == axes[i - 1].param:
+            raise InvalidInputError(f"grid: duplicate axis '{a.param}'")
+    # enumerate the points (odometer, last axis fastest) and their per-seed configs
+    import copy
+    import itertools
+
+    points, cfgs = [], []
+    for combo in itertools.product(*[a.values for a in axes]):
+        cfg = copy.deepcopy(base)
+        params = {}
+        for a, v in zip(axes, combo):
+            _apply_param(cfg, a.param, float(v))
+            params[a.param] = float(v)
+        points.append((params, cfg))
+        for sd in seeds:
+            c = copy.deepcopy(cfg)
+            c.seed = sd
+            cfgs.append(c)
+    if _batchable(obj, cfgs):
+        ds = obj.ds
+        b = BatchProblems(ds.X, ds.targets, l2=obj.l2(), device=obj.device, nprob=len(cfgs))
+        recs = b.run(cfgs)
+    else:
+        recs = [run_prepared(obj, c, data_seed) for c in cfgs]
+    res = GridResult()
+    best = math.inf
+    for pi, (params, cfg) in enumerate(points):
+        out = GridOutcome(params=params, status="ok")
+        total = 0.0
+        for si in range(len(seeds)):
+            rec = recs[pi * len(seeds) + si]
+            m = _final_metric(rec, metric)
+            if rec.status == "diverged" or not math.isfinite(m):
+                m = math.inf
+                out.status = "diverged"
+            out.per_seed.append(m)
+            total += m
+        out.mean_metric = total / float(len(seeds))
+        if pi == 0 or out.mean_metric < best:
+            best = out.mean_metric
+            res.best_index = pi
+            res.best_config = copy.deepcopy(cfg)
+            res.best_config.seed = base.seed
+        res.points.append(out)
+    return res
 
 
 def halp_scale(grad_norm: float, mu: float, bits: int) -> float:
@@ -410,11 +542,13 @@ class BatchProblems:
     batched kernel K5: one CTA per problem runs the whole run_halp.
 
     X: [nprob, n, d] (numpy float64/float32/bf16-as-uint16, or a CUDA tensor),
-    y: [nprob, n].  run(cfgs) returns one RunRecord per problem; a problem that
-    diverges gets status "diverged" and its partial record (run_prepared
-    semantics, harness.cpp:309-311) instead of an exception."""
+    y: [nprob, n]; or X: [n, d], y: [n] with `nprob` given -- one dataset
+    shared by every problem (each with its own config: grid searches).
+    run(cfgs) returns one RunRecord per problem; a problem that diverges gets
+    status "diverged" and its partial record (run_prepared semantics,
+    harness.cpp:309-311) instead of an exception."""
 
-    def __init__(self, X, y, l2: float = 0.0, device: int = 0):
+    def __init__(self, X, y, l2: float = 0.0, device: int = 0, nprob: Optional[int] = None):
         dev = _is_torch_cuda(X)
         if dev:
             import torch
@@ -427,10 +561,18 @@ class BatchProblems:
             y = np.ascontiguousarray(y, dtype=np.float64)
             xptr, yptr = X.ctypes.data, y.ctypes.data
         self._keep = [X, y]
-        nprob, n, d = (int(v) for v in X.shape)
-        self.nprob, self.n, self.d = nprob, n, d
-        desc = A.BatchDesc(xptr, _x_dtype(X), A.MEM_DEVICE if dev else A.MEM_HOST, n, d, nprob, yptr, float(l2),
-                           device)
+        shared = len(X.shape) == 2
+        if shared:
+            if nprob is None or nprob < 1:
+                raise InvalidInputError("BatchProblems: a shared dataset needs nprob >= 1")
+            n, d = (int(v) for v in X.shape)
+        else:
+            nprob, n, d = (int(v) for v in X.shape)
+        if tuple(int(v) for v in y.shape) != ((n,) if shared else (nprob, n)):
+            raise InvalidInputError("Objective: squared loss needs one target per row")
+        self.nprob, self.n, self.d, self.shared = int(nprob), n, d, shared
+        desc = A.BatchDesc(xptr, _x_dtype(X), A.MEM_DEVICE if dev else A.MEM_HOST, n, d, self.nprob, yptr, float(l2),
+                           device, 1 if shared else 0)
         h = C.c_void_p()
         rc = A.lib().halp_batch_create(C.byref(desc), C.byref(h))
         if rc:
