@@ -859,8 +859,17 @@ static int validate_config(const oq_objective* o, const oq_config* c) {
     return OQ_INVALID_INPUT;
   }
   if (!(isfinite(c->delta_min) && c->delta_min > 0.0)) { set_err("optimizer: delta_min must be positive"); return OQ_INVALID_INPUT; }
-  if (c->bits < 2 || c->bits > 64) { set_err("optimizer: bits must be in [2, 64]"); return OQ_INVALID_INPUT; }
-  if (!(isfinite(c->mu) && c->mu > 0.0)) { set_err("optimizer: mu must be positive for bit-centered runs"); return OQ_INVALID_INPUT; }
+  if (c->algorithm == OQ_ALGO_LP_SVRG) { /* uses_fixed_scale */
+    if (c->bits < 2 || c->bits > 64) { set_err("optimizer: bits must be in [2, 64]"); return OQ_INVALID_INPUT; }
+    if (!(isfinite(c->delta) && c->delta > 0.0)) {
+      set_err("optimizer: delta must be positive for fixed-scale runs");
+      return OQ_INVALID_INPUT;
+    }
+  }
+  if (c->algorithm == OQ_ALGO_HALP) { /* uses_bit_centering */
+    if (c->bits < 2 || c->bits > 64) { set_err("optimizer: bits must be in [2, 64]"); return OQ_INVALID_INPUT; }
+    if (!(isfinite(c->mu) && c->mu > 0.0)) { set_err("optimizer: mu must be positive for bit-centered runs"); return OQ_INVALID_INPUT; }
+  }
   return OQ_OK;
 }
 
@@ -921,7 +930,7 @@ static void measure(const oq_objective* o, const double* wt, const oq_config* cf
     *gn = mirror_norm(gt, o->d * o->C);
   }
   *delta = 0.0;
-  if (isfinite(*gn) && *gn > 0.0) {
+  if (cfg->algorithm == OQ_ALGO_HALP && isfinite(*gn) && *gn > 0.0) {
     double s = oq_halp_scale(*gn, cfg->mu, cfg->bits);
     *delta = s > cfg->delta_min ? s : cfg->delta_min;
   }
@@ -1054,4 +1063,160 @@ done:
   if (rc == OQ_DIVERGED) rec->steps_taken = 0;
   free(wt); free(z); free(wz); free(u); free(g1); free(g2); free(gt); free(x); free(code); free(snap);
   return rc;
+}
+
+/* Component gradients at w (g1) and wt (g2) of row i, REF or MIRROR order
+ * (MIRROR = the inner-loop kernel's dots, k_inner.cu). */
+static void component_pair(const oq_objective* o, const oq_plan* plan, const double* x, int64_t i, const double* w,
+                           const double* wt, double* g1, double* g2) {
+  const int d = o->d, C = o->C;
+  if (!plan) {
+    ref_component_gradient(o, x, i, w, g1);
+    ref_component_gradient(o, x, i, wt, g2);
+    return;
+  }
+  double la[64], lb[64];
+  mirror_inner_dots(x, w, wt, d, C, plan, la, lb);
+  if (o->loss == OQ_SQUARED) {
+    const double e1 = la[0] - o->y[i], e2 = lb[0] - o->y[i];
+    for (int j = 0; j < d; ++j) {
+      g1[j] = e1 * x[j] + o->l2 * w[j];
+      g2[j] = e2 * x[j] + o->l2 * wt[j];
+    }
+  } else {
+    const int y = o->labels[i];
+    mirror_softmax_dl_k3(la, C, y);
+    mirror_softmax_dl_k3(lb, C, y);
+    for (int c = 0; c < C; ++c)
+      for (int j = 0; j < d; ++j) {
+        const size_t q = (size_t)c * d + j;
+        g1[q] = x[j] * la[c] + o->l2 * w[q];
+        g2[q] = x[j] * lb[c] + o->l2 * wt[q];
+      }
+  }
+}
+
+/* optimizers.cpp:258-296 run_svrg (lp = 0) and :336-385 run_lp_svrg (lp = 1).
+ * SVRG: w -= alpha*((g1 - g2) + gt), no finiteness check inside the epoch;
+ * LP-SVRG: the iterate is Q(u) at the fixed scale cfg->delta (one rounding
+ * draw per coordinate, the initial iterate quantized once), a non-finite u
+ * is a blow-up row.  Rows carry delta = 0 (SVRG) / cfg->delta (LP-SVRG). */
+static int run_svrg_family(const oq_objective* o, const oq_config* cfg, const oq_plan* plan, oq_record* rec, int lp) {
+  int rc = check_objective(o);
+  if (rc) return rc;
+  rc = validate_config(o, cfg);
+  if (rc) return rc;
+  const int d = o->d, C = o->C, D = d * C;
+  const int64_t n = o->n;
+  const int64_t T = oq_resolve_inner_steps(cfg, n);
+  if (T < 1) { set_err("optimizer: epoch length must be >= 1"); return OQ_INVALID_INPUT; }
+  const double rdelta = lp ? cfg->delta : 0.0;
+  oq_rng sample, rounder;
+  oq_rng_init(&sample, cfg->seed, 0);
+  oq_rng_init(&rounder, cfg->seed, 1);
+  double* wt = (double*)calloc((size_t)D, sizeof(double));
+  double* w = (double*)malloc(sizeof(double) * (size_t)D);
+  double* snapw = (double*)malloc(sizeof(double) * (size_t)D);
+  double* u = (double*)malloc(sizeof(double) * (size_t)D);
+  double* g1 = (double*)malloc(sizeof(double) * (size_t)D);
+  double* g2 = (double*)malloc(sizeof(double) * (size_t)D);
+  double* gt = (double*)malloc(sizeof(double) * (size_t)D);
+  double* x = (double*)malloc(sizeof(double) * (size_t)d);
+  int64_t* wt_lp = (int64_t*)calloc((size_t)D, sizeof(int64_t));
+  int64_t* w_lp = (int64_t*)calloc((size_t)D, sizeof(int64_t));
+  int64_t* snap_lp = (int64_t*)calloc((size_t)D, sizeof(int64_t));
+  if (cfg->init) memcpy(wt, cfg->init, sizeof(double) * (size_t)D);
+  if (lp) { /* wt_lp = quantize_vector(w0), wt = to_real(wt_lp) */
+    for (int q = 0; q < D; ++q) {
+      const double uu = oq_next_uniform(&rounder);
+      int err = 0;
+      wt_lp[q] = oq_quantize_code(wt[q], cfg->delta, cfg->bits, uu, &err);
+      if (err) { set_err("quantize: non-finite input"); rc = OQ_INVALID_INPUT; goto done; }
+    }
+    for (int q = 0; q < D; ++q) wt[q] = (double)wt_lp[q] * cfg->delta;
+  }
+  rec->rows_n = 0;
+  rec->status = OQ_STATUS_OK;
+  rec->steps_taken = 0;
+  rec->inner_fp_vector_ops = 0;
+  rec->fullgrad_seconds = 0.0;
+  rec->inner_seconds = 0.0;
+  recorder r = {cfg, rec, now_s(), 0.0, D};
+  int64_t steps = 0, traced = 0;
+  const int fgth = rec->fullgrad_threads > 0 ? rec->fullgrad_threads : 1;
+  for (int k = 0; k < cfg->epochs; ++k) {
+    double gn, dl, loss;
+    measure(o, wt, cfg, plan, fgth, gt, &gn, &dl, &loss, &rec->fullgrad_seconds);
+    rc = rec_boundary(&r, (double)steps / (double)n, wt, loss, gn, rdelta, k == 0);
+    if (rc) goto done;
+    int64_t t_pick = -1;
+    if (cfg->option == 1) t_pick = (int64_t)oq_next_index(&sample, (uint64_t)T);
+    memcpy(w, wt, sizeof(double) * (size_t)D);
+    memcpy(snapw, wt, sizeof(double) * (size_t)D);
+    memcpy(w_lp, wt_lp, sizeof(int64_t) * (size_t)D);
+    memcpy(snap_lp, wt_lp, sizeof(int64_t) * (size_t)D);
+    const double ti0 = now_s();
+    for (int64_t t = 0; t < T; ++t) {
+      if (t == t_pick) {
+        if (lp) memcpy(snap_lp, w_lp, sizeof(int64_t) * (size_t)D);
+        else memcpy(snapw, w, sizeof(double) * (size_t)D);
+      }
+      const int64_t i = (int64_t)oq_next_index(&sample, (uint64_t)n);
+      load_row(o, i, x);
+      component_pair(o, plan, x, i, w, wt, g1, g2);
+      if (!lp) {
+        for (int q = 0; q < D; ++q) w[q] = w[q] - cfg->alpha * ((g1[q] - g2[q]) + gt[q]);
+        continue;
+      }
+      int finite = 1;
+      for (int q = 0; q < D; ++q) {
+        u[q] = w[q] - cfg->alpha * ((g1[q] - g2[q]) + gt[q]);
+        if (!isfinite(u[q])) finite = 0;
+      }
+      if (!finite) {
+        rc = rec_boundary(&r, (double)(steps + t + 1) / (double)n, u, INFINITY, INFINITY, cfg->delta, 1);
+        goto done;
+      }
+      for (int q = 0; q < D; ++q) {
+        const double uu = oq_next_uniform(&rounder);
+        w_lp[q] = oq_quantize_code(u[q], cfg->delta, cfg->bits, uu, NULL);
+      }
+      for (int q = 0; q < D; ++q) w[q] = (double)w_lp[q] * cfg->delta;
+      if (rec->trace_codes && traced + D <= rec->trace_cap) {
+        memcpy(rec->trace_codes + traced, w_lp, sizeof(int64_t) * (size_t)D);
+        traced += D;
+      }
+    }
+    rec->inner_seconds += now_s() - ti0;
+    rec->inner_fp_vector_ops += (uint64_t)((lp ? 7 : 5) * T); /* 2 component gradients (2 each) + the update (+ quantize, to_real) */
+    if (lp) {
+      memcpy(wt_lp, cfg->option == 1 ? snap_lp : w_lp, sizeof(int64_t) * (size_t)D);
+      for (int q = 0; q < D; ++q) wt[q] = (double)wt_lp[q] * cfg->delta;
+    } else {
+      memcpy(wt, cfg->option == 1 ? snapw : w, sizeof(double) * (size_t)D);
+    }
+    steps += T;
+  }
+  {
+    double gn, dl, loss;
+    measure(o, wt, cfg, plan, fgth, gt, &gn, &dl, &loss, &rec->fullgrad_seconds);
+    rc = rec_boundary(&r, (double)steps / (double)n, wt, loss, gn, rdelta, 1);
+    if (rc) goto done;
+  }
+  memcpy(rec->final_iterate, wt, sizeof(double) * (size_t)D);
+  rec->steps_taken = steps;
+done:
+  if (rc == OQ_DIVERGED) rec->steps_taken = 0;
+  free(wt); free(w); free(snapw); free(u); free(g1); free(g2); free(gt); free(x);
+  free(wt_lp); free(w_lp); free(snap_lp);
+  return rc;
+}
+
+int oq_run(const oq_objective* o, const oq_config* cfg, const oq_plan* plan, oq_record* rec) {
+  switch (cfg->algorithm) {
+    case OQ_ALGO_HALP: return oq_run_halp(o, cfg, plan, rec);
+    case OQ_ALGO_SVRG: return run_svrg_family(o, cfg, plan, rec, 0);
+    case OQ_ALGO_LP_SVRG: return run_svrg_family(o, cfg, plan, rec, 1);
+    default: set_err("oracle: algorithm not restated"); return OQ_INVALID_INPUT;
+  }
 }

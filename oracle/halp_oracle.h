@@ -115,7 +115,11 @@ typedef struct {
   double   delta_min;
   double   divergence_limit;
   const double* init;            /* NULL => zeros */
+  double   delta;                /* fixed scale of LP-SVRG (OptimizerConfig::delta) */
+  int32_t  algorithm;            /* lpopt::Algorithm: 1 Svrg, 3 LpSvrg, 4 Halp */
 } oq_config;
+
+enum { OQ_ALGO_SVRG = 1, OQ_ALGO_LP_SVRG = 3, OQ_ALGO_HALP = 4 };
 
 typedef struct {
   double   pass, seconds, loss, grad_norm, delta;
@@ -143,6 +147,9 @@ typedef struct {
 } oq_record;
 
 int      oq_run_halp(const oq_objective* o, const oq_config* cfg, const oq_plan* plan, oq_record* rec);
+/* run_svrg / run_lp_svrg (optimizers.cpp:258-296, 336-385) and the run()
+ * dispatch (optimizers.cpp:629-639) over the algorithms the B200 builds */
+int      oq_run(const oq_objective* o, const oq_config* cfg, const oq_plan* plan, oq_record* rec);
 int64_t  oq_resolve_inner_steps(const oq_config* cfg, int64_t n);
 uint64_t oq_hash_vector(const double* v, int64_t len);
 const char* oq_last_error(void);

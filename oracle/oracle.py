@@ -51,7 +51,7 @@ class _Config(C.Structure):
         ("alpha", C.c_double), ("epochs", C.c_int32), ("inner_steps", C.c_int64), ("bits", C.c_int32),
         ("mu", C.c_double), ("option", C.c_int32), ("full_grad_period", C.c_int32), ("seed", C.c_uint64),
         ("metric_every_passes", C.c_double), ("delta_min", C.c_double), ("divergence_limit", C.c_double),
-        ("init", C.c_void_p),
+        ("init", C.c_void_p), ("delta", C.c_double), ("algorithm", C.c_int32),
     ]
 
 
@@ -97,6 +97,7 @@ def lib():
         L.oq_full_gradient.argtypes = [C.POINTER(_Objective), C.c_void_p, C.c_int, C.POINTER(_Plan), C.c_void_p]
         L.oq_component_gradient.argtypes = [C.POINTER(_Objective), C.c_int64, C.c_void_p, C.POINTER(_Plan), C.c_void_p]
         L.oq_run_halp.argtypes = [C.POINTER(_Objective), C.POINTER(_Config), C.POINTER(_Plan), C.POINTER(_Record)]
+        L.oq_run.argtypes = [C.POINTER(_Objective), C.POINTER(_Config), C.POINTER(_Plan), C.POINTER(_Record)]
         L.oq_hash_vector.restype = C.c_uint64
         L.oq_hash_vector.argtypes = [C.c_void_p, C.c_int64]
         L.oq_last_error.restype = C.c_char_p
@@ -274,7 +275,8 @@ def _plan(p):
 
 @dataclass
 class OracleConfig:
-    """HALP fields of lpopt::OptimizerConfig (optimizers.hpp:31-47)."""
+    """lpopt::OptimizerConfig fields of the restated algorithms (optimizers.hpp:31-47);
+    algorithm: 1 Svrg, 3 LpSvrg, 4 Halp (run() dispatches, run_halp forces 4)."""
 
     alpha: float = 1e-3
     epochs: int = 1
@@ -288,6 +290,8 @@ class OracleConfig:
     delta_min: float = 1e-300
     divergence_limit: float = 1e12
     init: Optional[np.ndarray] = None
+    delta: float = 0.0
+    algorithm: int = 4
 
 
 @dataclass
@@ -305,19 +309,30 @@ class OracleRecord:
 
 def run_halp(obj: OracleObjective, cfg: OracleConfig, plan=None, trace_steps: int = 0,
              fullgrad_threads: int = 1, rows_cap: int = 0) -> OracleRecord:
+    """optimizers.cpp:387-459"""
+    return _run(obj, cfg, plan, trace_steps, fullgrad_threads, rows_cap, 4)
+
+
+def run(obj: OracleObjective, cfg: OracleConfig, plan=None, trace_steps: int = 0, fullgrad_threads: int = 1,
+        rows_cap: int = 0) -> OracleRecord:
+    """lpopt::run (optimizers.cpp:629-639) over Svrg (1), LpSvrg (3), Halp (4)"""
+    return _run(obj, cfg, plan, trace_steps, fullgrad_threads, rows_cap, int(cfg.algorithm))
+
+
+def _run(obj, cfg, plan, trace_steps, fullgrad_threads, rows_cap, algorithm) -> OracleRecord:
     init = None
     if cfg.init is not None:
         init = np.ascontiguousarray(cfg.init, dtype=np.float64)
     c = _Config(cfg.alpha, cfg.epochs, cfg.inner_steps, cfg.bits, cfg.mu, cfg.option, cfg.full_grad_period,
                 cfg.seed, cfg.metric_every_passes, cfg.delta_min, cfg.divergence_limit,
-                init.ctypes.data if init is not None else None)
+                init.ctypes.data if init is not None else None, cfg.delta, algorithm)
     cap = rows_cap or (cfg.epochs + 2)
     rows = (_Row * cap)()
     fin = np.zeros(obj.dim, dtype=np.float64)
     tr = np.zeros(trace_steps * obj.dim, dtype=np.int64) if trace_steps else None
     rec = _Record(rows, cap, 0, fin.ctypes.data, 0, 0, 0, tr.ctypes.data if tr is not None else None,
                   tr.size if tr is not None else 0, 0.0, 0.0, fullgrad_threads)
-    rc = lib().oq_run_halp(C.byref(obj._s), C.byref(c), _plan(plan), C.byref(rec))
+    rc = lib().oq_run(C.byref(obj._s), C.byref(c), _plan(plan), C.byref(rec))
     if rc not in (0, 2):
         _check(rc)
     out = OracleRecord()

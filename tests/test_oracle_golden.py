@@ -78,3 +78,26 @@ def test_golden_packet_width_is_sse2(oracle, obj):
     finally:
         L.oq_set_ref_lanes(2)
     assert counts[2] == 12 and counts[2] > counts[1] and counts[2] > counts[4], counts
+
+
+@pytest.mark.parametrize("name,algo,kw,tol", [("svrg", 1, {}, 1e-9),
+                                              ("lp-svrg-8", 3, dict(delta=0.7, bits=8), 1e-15),
+                                              ("lp-svrg-16", 3, dict(delta=0.003, bits=16), 1e-15)])
+@pytest.mark.parametrize("seed", [1, 2, 3, 4, 5])
+def test_golden_svrg_family(oracle, obj, name, algo, kw, tol, seed):
+    """run_svrg / run_lp_svrg (optimizers.cpp:258-296, 336-385) restated,
+    against the golden traces svrg / lp-svrg-{8,16}_seed{1..5}.csv (spec rows
+    specs/regression_floor.json:8,11-12): every row within 1e-9 (SVRG) and
+    1e-15 (LP-SVRG, whose fixed-scale iterate makes it all but bit-exact)."""
+    cfg = oracle.OracleConfig(alpha=5e-3, epochs=25, inner_steps=2000, seed=seed, algorithm=algo, **kw)
+    rec = oracle.run(obj, cfg)
+    gold = GOLD["traces"][f"{name}_seed{seed}"]
+    assert len(rec.rows) == len(gold) == 26 and rec.status == "ok" and rec.steps_taken == 50000
+    assert rec.inner_fp_vector_ops == (5 if algo == 1 else 7) * 2000 * 25  # instr counters per step
+    for k, (a, b) in enumerate(zip(rec.rows, gold)):
+        assert a["pass_"] == float(b["pass"])
+        for f in ("loss", "grad_norm", "delta"):
+            bv = float(b[f])
+            assert abs(a[f] - bv) <= tol * abs(bv), (k, f, a[f], bv)
+    man = GOLD["manifest"][f"{name}_seed{seed}"]
+    assert rec.rows[-1]["grad_norm"] == pytest.approx(man["final_grad_norm"], rel=max(tol, 1e-12))
