@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define HALP_ABI_VERSION 2
+#define HALP_ABI_VERSION 3
 
 typedef enum {
   HALP_OK = 0,
@@ -74,7 +74,8 @@ typedef struct {
 
 typedef struct halp_problem halp_problem;
 
-/* HALP fields of lpopt::OptimizerConfig (optimizers.hpp:31-47) */
+/* lpopt::OptimizerConfig (optimizers.hpp:31-47): the fields of the
+ * algorithms this library runs (Halp; Svrg and LpSvrg on the same kernels) */
 typedef struct {
   double        alpha;
   int32_t       epochs;
@@ -88,7 +89,12 @@ typedef struct {
   double        delta_min;
   double        divergence_limit;
   const double* init;                 /* host, d*num_outputs doubles, NULL => zeros */
+  double        delta;                /* fixed scale of LpSvrg (OptimizerConfig::delta); ABI >= 3 */
+  int32_t       algorithm;            /* HALP_ALGO_*: lpopt::Algorithm numbering; ABI >= 3 */
 } halp_config;
+
+/* lpopt::Algorithm values halp_run accepts (optimizers.hpp:13-15) */
+enum { HALP_ALGO_SVRG = 1, HALP_ALGO_LP_SVRG = 3, HALP_ALGO_HALP = 4 };
 
 /* lpopt::MetricRow (optimizers.hpp:49-58), HALP subset */
 typedef struct {

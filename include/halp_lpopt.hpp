@@ -166,11 +166,14 @@ class Objective {
   halp_problem* h_ = nullptr;
 };
 
-// lpopt::run_halp (optimizers.cpp:387-459)
-inline RunRecord run_halp(const Objective& obj, const OptimizerConfig& cfg) {
+namespace detail {
+// one of the device algorithms (HALP_ALGO_*) through halp_run
+inline RunRecord run_algo(const Objective& obj, const OptimizerConfig& cfg, int algo) {
   if (!cfg.init.empty() && (int)cfg.init.size() != obj.dim())
     throw InvalidInputError("optimizer: init length does not match objective");
   halp_config c{};
+  c.algorithm = algo;
+  c.delta = cfg.delta;
   c.alpha = cfg.alpha;
   c.epochs = cfg.epochs;
   c.inner_steps = cfg.inner_steps;
@@ -213,11 +216,29 @@ inline RunRecord run_halp(const Objective& obj, const OptimizerConfig& cfg) {
   fill();
   return out;
 }
+}  // namespace detail
 
-// lpopt::run (optimizers.cpp:629-639): the Halp branch
+// lpopt::run_halp (optimizers.cpp:387-459)
+inline RunRecord run_halp(const Objective& obj, const OptimizerConfig& cfg) {
+  return detail::run_algo(obj, cfg, HALP_ALGO_HALP);
+}
+// lpopt::run_svrg (optimizers.cpp:258-296)
+inline RunRecord run_svrg(const Objective& obj, const OptimizerConfig& cfg) {
+  return detail::run_algo(obj, cfg, HALP_ALGO_SVRG);
+}
+// lpopt::run_lp_svrg (optimizers.cpp:336-385)
+inline RunRecord run_lp_svrg(const Objective& obj, const OptimizerConfig& cfg) {
+  return detail::run_algo(obj, cfg, HALP_ALGO_LP_SVRG);
+}
+
+// lpopt::run (optimizers.cpp:629-639): the branches this library runs on the B200
 inline RunRecord run(const Objective& obj, const OptimizerConfig& cfg) {
-  if (cfg.algorithm == Algorithm::Halp) return run_halp(obj, cfg);
-  throw UnsupportedError("only Algorithm::Halp is on the B200 path");
+  switch (cfg.algorithm) {
+    case Algorithm::Halp: return run_halp(obj, cfg);
+    case Algorithm::Svrg: return run_svrg(obj, cfg);
+    case Algorithm::LpSvrg: return run_lp_svrg(obj, cfg);
+    default: throw UnsupportedError("algorithm not on the B200 path (Sgd, LpSgd, LmHalp)");
+  }
 }
 
 // harness.cpp:296-312

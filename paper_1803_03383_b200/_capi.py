@@ -32,7 +32,7 @@ class Config(C.Structure):
         ("alpha", C.c_double), ("epochs", C.c_int32), ("inner_steps", C.c_int64), ("bits", C.c_int32),
         ("mu", C.c_double), ("option", C.c_int32), ("full_grad_period", C.c_int32), ("seed", C.c_uint64),
         ("metric_every_passes", C.c_double), ("delta_min", C.c_double), ("divergence_limit", C.c_double),
-        ("init", C.c_void_p),
+        ("init", C.c_void_p), ("delta", C.c_double), ("algorithm", C.c_int32),
     ]
 
 

@@ -201,6 +201,7 @@ struct halp_problem {
   InLaunch in{};
   int fg_passes = 1;
   // workspace
+  double *zb0 = nullptr, *zb1 = nullptr;  // K3 z0 / zc_out ping-pong (SVRG, LP-SVRG)
   double *w = nullptr, *w2 = nullptr, *g = nullptr, *partials = nullptr, *rank_sum = nullptr, *gathered = nullptr,
          *stats = nullptr, *u_out = nullptr, *tree_scratch = nullptr;
   int64_t* idx = nullptr;
@@ -222,7 +223,7 @@ struct halp_problem {
     // stream-ordered frees back into the device pool (no device-wide sync)
     for (void* ptr : {(void*)w, (void*)w2, (void*)g, (void*)partials, (void*)rank_sum, (void*)gathered, (void*)stats,
                       (void*)u_out, (void*)idx, (void*)codes, (void*)blow, (void*)trace_dev, (void*)y,
-                      (void*)labels, (void*)tree_scratch})
+                      (void*)labels, (void*)tree_scratch, (void*)zb0, (void*)zb1})
       if (ptr) cudaFreeAsync(ptr, stream);
     if (own_X && X) cudaFreeAsync(X, stream);
     if (comm) Nccl::get().commDestroy(comm);
@@ -386,6 +387,8 @@ int ensure_workspace(halp_problem* p) {
     CU(dalloc(&p->stats, sizeof(double) * 4, st));
     CU(dalloc(&p->codes, sizeof(long long) * p->D, st));
     CU(dalloc(&p->blow, sizeof(int), st));
+    CU(dalloc(&p->zb0, sizeof(double) * p->D, st));
+    CU(dalloc(&p->zb1, sizeof(double) * p->D, st));
     int rc = rng_tables(p->device, p->D, &p->pow_tab, &p->jump_tab);
     if (rc) return rc;
     CU(cudaEventCreate(&p->ev_fg.a));
@@ -480,6 +483,23 @@ struct Recorder {
 };
 
 // optimizers.cpp:36-97 (HALP checks)
+// fixed_point.cpp:30-50 quantize_code (host: LP-SVRG's one-time quantization
+// of the initial iterate; the device quantizer is quantize_fast in K3)
+int64_t host_quantize_code(double x, double delta, int bits, double u) {
+  const int64_t maxc = bits == 64 ? INT64_MAX : (int64_t)((1ULL << (bits - 1)) - 1);
+  const int64_t minc = bits == 64 ? INT64_MIN : -(int64_t)(1ULL << (bits - 1));
+  const double t = x / delta;
+  if (t >= (double)maxc) return maxc;
+  if (t <= (double)minc) return minc;
+  const double snapped = std::nearbyint(t);
+  if (snapped * delta == x) return (int64_t)snapped;
+  const double fl = std::floor(t);
+  const double frac = t - fl;
+  int64_t code = (int64_t)fl;
+  if (frac > 0.0 && u < frac) ++code;
+  return code;
+}
+
 int validate(const halp_problem* p, const halp_config* c) {
   if (!(std::isfinite(c->alpha) && c->alpha >= 0.0)) return fail(HALP_INVALID_INPUT, "optimizer: alpha must be finite and >= 0");
   if (c->epochs < 0) return fail(HALP_INVALID_INPUT, "optimizer: epochs must be >= 0");
@@ -490,8 +510,18 @@ int validate(const halp_problem* p, const halp_config* c) {
   if (!(std::isfinite(c->divergence_limit) && c->divergence_limit > 0.0))
     return fail(HALP_INVALID_INPUT, "optimizer: divergence_limit must be positive");
   if (!(std::isfinite(c->delta_min) && c->delta_min > 0.0)) return fail(HALP_INVALID_INPUT, "optimizer: delta_min must be positive");
-  if (c->bits < 2 || c->bits > 64) return fail(HALP_INVALID_INPUT, "optimizer: bits must be in [2, 64]");
-  if (!(std::isfinite(c->mu) && c->mu > 0.0)) return fail(HALP_INVALID_INPUT, "optimizer: mu must be positive for bit-centered runs");
+  if (c->algorithm != HALP_ALGO_HALP && c->algorithm != HALP_ALGO_SVRG && c->algorithm != HALP_ALGO_LP_SVRG)
+    return fail(HALP_UNSUPPORTED, "optimizer: algorithm not on the B200 path (Svrg, LpSvrg, Halp are)");
+  if (c->algorithm == HALP_ALGO_LP_SVRG) {  // uses_fixed_scale
+    if (c->bits < 2 || c->bits > 64) return fail(HALP_INVALID_INPUT, "optimizer: bits must be in [2, 64]");
+    if (!(std::isfinite(c->delta) && c->delta > 0.0))
+      return fail(HALP_INVALID_INPUT, "optimizer: delta must be positive for fixed-scale runs");
+  }
+  if (c->algorithm == HALP_ALGO_HALP) {  // uses_bit_centering
+    if (c->bits < 2 || c->bits > 64) return fail(HALP_INVALID_INPUT, "optimizer: bits must be in [2, 64]");
+    if (!(std::isfinite(c->mu) && c->mu > 0.0))
+      return fail(HALP_INVALID_INPUT, "optimizer: mu must be positive for bit-centered runs");
+  }
   if (c->option != 0 && c->option != 1) return fail(HALP_INVALID_INPUT, "optimizer: option must be 0 (I) or 1 (II)");
   (void)p;
   return HALP_OK;
@@ -739,10 +769,16 @@ int halp_bench_full_gradient(halp_problem* p, int reps, double* ms_per_pass) {
 }
 
 int halp_run(halp_problem* p, const halp_config* cfg, halp_record* rec) {
+  // lpopt::run_halp (optimizers.cpp:387-459), run_svrg (:258-296) and
+  // run_lp_svrg (:336-385): one epoch loop, K1 + K2 at the boundary, K4 + K3
+  // inside; the three differ in the K3 mode and in how z / the scale start.
   if (!p || !cfg || !rec) return fail(HALP_INVALID_INPUT, "halp_run: null argument");
   int rc = validate(p, cfg);
   if (rc) return rc;
   CU(cudaSetDevice(p->device));
+  const int algo = cfg->algorithm;
+  const bool halp = algo == HALP_ALGO_HALP, lp = algo == HALP_ALGO_LP_SVRG;
+  const int mode = halp ? 0 : lp ? 1 : 2;
   const int64_t n = p->n, D = p->D;
   const int64_t T = cfg->inner_steps > 0 ? cfg->inner_steps : (int64_t)cfg->full_grad_period * n;
   if (T < 1) return fail(HALP_INVALID_INPUT, "optimizer: epoch length must be >= 1");
@@ -753,10 +789,34 @@ int halp_run(halp_problem* p, const halp_config* cfg, halp_record* rec) {
     CU(dalloc(&p->idx, sizeof(int64_t) * T, p->stream));
     p->idx_cap = T;
   }
+  const auto& jt = JumpTables::get();
+  const uint64_t s_sample = rng_seed_state(cfg->seed, 0);  // kSampleStream
+  const uint64_t s_round = rng_seed_state(cfg->seed, 1);   // kRoundStream
   std::vector<double> wh(D, 0.0);
   if (cfg->init) std::memcpy(wh.data(), cfg->init, sizeof(double) * D);
+  // z at the start of the first epoch: HALP resets it per epoch (Q(0));
+  // LP-SVRG quantizes the initial iterate once (D rounding draws); SVRG holds w itself
+  std::vector<double> z0(D, 0.0);
+  if (lp) {
+    uint64_t st = s_round;
+    for (int64_t q = 0; q < D; ++q) {
+      st = xs_step_host(st);
+      const double u = (double)((st * 0x2545F4914F6CDD1DULL) >> 11) * 0x1.0p-53;
+      if (!std::isfinite(wh[q])) return fail(HALP_INVALID_INPUT, "quantize: input must be finite");
+      z0[q] = (double)host_quantize_code(wh[q], cfg->delta, cfg->bits, u);
+    }
+    for (int64_t q = 0; q < D; ++q) wh[q] = z0[q] * cfg->delta;  // to_real
+  } else if (!halp) {
+    z0 = wh;
+  }
   CU(cudaMemcpyAsync(p->w, wh.data(), sizeof(double) * D, cudaMemcpyHostToDevice, p->stream));
   p->timing.h2d_bytes += sizeof(double) * D;
+  double* zin = p->zb0;
+  double* zout = p->zb1;
+  if (!halp) {
+    CU(cudaMemcpyAsync(zin, z0.data(), sizeof(double) * D, cudaMemcpyHostToDevice, p->stream));
+    p->timing.h2d_bytes += sizeof(double) * D;
+  }
 
   // trace buffer (test hook)
   int64_t traced = 0;
@@ -773,29 +833,34 @@ int halp_run(halp_problem* p, const halp_config* cfg, halp_record* rec) {
   rec->inner_fp_vector_ops = 0;
   rec->inner_lp_vector_ops = 0;
   Recorder r{cfg, rec, now_s(), 0.0, (int)D};
-  const auto& jt = JumpTables::get();
-  const uint64_t s_sample = rng_seed_state(cfg->seed, 0);  // kSampleStream
-  const uint64_t s_round = rng_seed_state(cfg->seed, 1);   // kRoundStream
-  const double hi = cfg->bits == 64 ? (double)INT64_MAX : (double)((1LL << (cfg->bits - 1)) - 1);
-  const double lo = cfg->bits == 64 ? (double)INT64_MIN : (double)(-(1LL << (cfg->bits - 1)));
-  const long long maxc = cfg->bits == 64 ? INT64_MAX : (1LL << (cfg->bits - 1)) - 1;
-  const long long minc = cfg->bits == 64 ? INT64_MIN : -(1LL << (cfg->bits - 1));
+  const int bits = halp || lp ? cfg->bits : 64;
+  const double hi = bits == 64 ? (double)INT64_MAX : (double)((1LL << (bits - 1)) - 1);
+  const double lo = bits == 64 ? (double)INT64_MIN : (double)(-(1LL << (bits - 1)));
+  const long long maxc = bits == 64 ? INT64_MAX : (1LL << (bits - 1)) - 1;
+  const long long minc = bits == 64 ? INT64_MIN : -(1LL << (bits - 1));
+  // instr counters per inner step: two component gradients (2 each) + the
+  // update (+ quantize_vector, to_real; HALP counts both its updates)
+  const uint64_t ops_per_step = halp ? 8 : lp ? 7 : 5;
+  const double mu = halp ? cfg->mu : 1.0;
   int64_t steps = 0;
   bool converged = false;
   for (int k = 0; k < cfg->epochs && !converged; ++k) {
     double gn, delta, loss;
-    rc = full_pass(p, &gn, &delta, &loss, cfg->mu, cfg->bits, cfg->delta_min);
+    rc = full_pass(p, &gn, &delta, &loss, mu, bits, cfg->delta_min);
     if (rc) return rc;
     CU(cudaMemcpy(wh.data(), p->w, sizeof(double) * D, cudaMemcpyDeviceToHost));
     p->timing.d2h_bytes += sizeof(double) * D;
-    rc = r.boundary((double)steps / (double)n, wh.data(), loss, gn, delta, k == 0 || gn == 0.0);
+    const double row_delta = halp ? delta : lp ? cfg->delta : 0.0;
+    rc = r.boundary((double)steps / (double)n, wh.data(), loss, gn, row_delta, k == 0 || (halp && gn == 0.0));
     if (rc) return rc;
-    if (gn == 0.0) {
+    if (halp && gn == 0.0) {
       rec->status = HALP_STATUS_CONVERGED;
       converged = true;
       break;
     }
-    if (!(std::isfinite(delta) && delta > 0.0)) return fail(HALP_INVALID_INPUT, "LPRepr: delta must be positive and finite");
+    if (halp && !(std::isfinite(delta) && delta > 0.0))
+      return fail(HALP_INVALID_INPUT, "LPRepr: delta must be positive and finite");
+    const double kdelta = halp ? delta : lp ? cfg->delta : 1.0;
     // sample stream: epoch k starts after k*(T+opt2) draws; option II draws t_pick first
     const uint64_t sbase = jt.jump(s_sample, (uint64_t)k * (uint64_t)(T + opt2));
     int64_t t_pick = -1;
@@ -808,14 +873,17 @@ int halp_run(halp_problem* p, const halp_config* cfg, halp_record* rec) {
     CU(launch_samples(s0, T, 0, (uint64_t)T, (uint64_t)n, p->pow_tab, p->idx, nullptr, p->stream));
     ++p->timing.kernel_launches;
     CU(cudaEventRecord(p->ev_smp.b, p->stream));
-    // rounding stream: epoch k starts after k*D*(T+1) draws; Q(0) takes D of them
-    const uint64_t r0 = jt.jump(s_round, (uint64_t)k * (uint64_t)D * (uint64_t)(T + 1) + (uint64_t)D);
+    // rounding stream at step 0 of epoch k: HALP k*D*(T+1) + D (Q(0) per epoch);
+    // LP-SVRG D + k*D*T (the initial quantization once); SVRG draws none
+    const uint64_t rdraws = halp ? (uint64_t)k * (uint64_t)D * (uint64_t)(T + 1) + (uint64_t)D
+                                 : (uint64_t)D + (uint64_t)k * (uint64_t)D * (uint64_t)T;
+    const uint64_t r0 = jt.jump(s_round, rdraws);
     CU(cudaMemsetAsync(p->blow, 0xFF, sizeof(int), p->stream));
-    const double rcp = 1.0 / delta;
-    InParams ip{p->X, p->ld, p->d, p->C, (int)D, p->loss, n, p->y, p->labels, p->l2, cfg->alpha, delta, hi, lo, maxc,
+    const double rcp = 1.0 / kdelta;
+    InParams ip{p->X, p->ld, p->d, p->C, (int)D, p->loss, n, p->y, p->labels, p->l2, cfg->alpha, kdelta, hi, lo, maxc,
                 minc, std::isfinite(rcp) && rcp != 0.0 && env_int("HALP_IEEE_DIV", 0) == 0 ? rcp : 0.0, p->w, p->w2,
                 p->g, p->idx, T, t_pick, r0, p->pow_tab, p->jump_tab, p->codes, tr_steps > 0 ? p->trace_dev : nullptr,
-                tr_steps, p->blow, p->u_out};
+                tr_steps, p->blow, p->u_out, mode, halp ? nullptr : zin, halp ? nullptr : zout};
     CU(cudaEventRecord(p->ev_in.a, p->stream));
     CU(launch_inner(p->in, ip, p->stream));
     ++p->timing.kernel_launches;
@@ -839,26 +907,27 @@ int halp_run(halp_problem* p, const halp_config* cfg, halp_record* rec) {
       traced += cnt;
     }
     if (blow >= 0) {
-      // Recorder::blowup (optimizers.cpp:156-160, 432-434)
+      // Recorder::blowup (optimizers.cpp:156-160; HALP :432-434, LP-SVRG :370-372)
       p->timing.inner_steps += blow + 1;
       std::vector<double> u(D);
       CU(cudaMemcpy(u.data(), p->u_out, sizeof(double) * D, cudaMemcpyDeviceToHost));
-      return r.boundary((double)(steps + blow + 1) / (double)n, u.data(), INFINITY, INFINITY, delta, true);
+      return r.boundary((double)(steps + blow + 1) / (double)n, u.data(), INFINITY, INFINITY, kdelta, true);
     }
     p->timing.inner_steps += T;
-    std::swap(p->w, p->w2);
-    rec->inner_fp_vector_ops += (uint64_t)(8 * T);
+    std::swap(p->w, p->w2);  // w~ += z (HALP) / w~ = the epoch's (snapshot) iterate
+    std::swap(zin, zout);    // next epoch starts from this epoch's (snapshot) codes
+    rec->inner_fp_vector_ops += ops_per_step * (uint64_t)T;
     steps += T;
   }
   if (!converged) {
     double gn, delta, loss;
-    rc = full_pass(p, &gn, &delta, &loss, cfg->mu, cfg->bits, cfg->delta_min);
+    rc = full_pass(p, &gn, &delta, &loss, mu, bits, cfg->delta_min);
     if (rc) return rc;
     CU(cudaMemcpy(wh.data(), p->w, sizeof(double) * D, cudaMemcpyDeviceToHost));
     p->timing.d2h_bytes += sizeof(double) * D;
-    rc = r.boundary((double)steps / (double)n, wh.data(), loss, gn, delta, true);
+    rc = r.boundary((double)steps / (double)n, wh.data(), loss, gn, halp ? delta : lp ? cfg->delta : 0.0, true);
     if (rc) return rc;
-    if (gn == 0.0) rec->status = HALP_STATUS_CONVERGED;
+    if (halp && gn == 0.0) rec->status = HALP_STATUS_CONVERGED;
   } else {
     CU(cudaMemcpy(wh.data(), p->w, sizeof(double) * D, cudaMemcpyDeviceToHost));
   }
@@ -987,6 +1056,7 @@ extern "C" int halp_batch_run(halp_batch* b, const halp_config* cfgs, halp_recor
   int max_rows = 2;
   for (int q = 0; q < P; ++q) {
     const halp_config& c = cfgs[q];
+    if (c.algorithm != HALP_ALGO_HALP) return fail(HALP_UNSUPPORTED, "halp_batch_run: Algorithm::Halp only");
     int rc = validate(nullptr, &c);
     if (rc) {
       g_err = "problem " + std::to_string(q) + ": " + g_err;

@@ -243,8 +243,8 @@ __global__ void __launch_bounds__(256, 1) k3_inner(InParams p) {
     wt[i] = valid[i] ? p.w[k] : 0.0;
     gt[i] = valid[i] ? p.g[k] : 0.0;
     l2w[i] = __dmul_rn(l2, wt[i]);
-    code[i] = 0.0;
-    snap[i] = 0.0;
+    code[i] = (valid[i] && p.z0) ? p.z0[k] : 0.0;
+    snap[i] = code[i];
     up[i] = 0.0;
     Ua[i] = 0.0;
   }
@@ -259,6 +259,9 @@ __global__ void __launch_bounds__(256, 1) k3_inner(InParams p) {
   // vector row loads when the thread's coordinates are aligned and in one class
   const bool vecx = (d % M == 0) && (ld % M == 0);
   const int64_t T = p.T;
+  // HALP: wz = w~ + z; LP-SVRG / SVRG: the iterate is z itself (base 0)
+  const bool base0 = p.mode != 0;
+  const bool fp_inner = p.mode == 2;
   uint64_t rs = jump_count(p.rstate0, (uint64_t)(k0 < D ? k0 : 0), p.pow_tab);
 
   // rows of steps 0 and 1 in flight (raw), the index of step 2 loaded
@@ -301,7 +304,8 @@ __global__ void __launch_bounds__(256, 1) k3_inner(InParams p) {
 #pragma unroll
         for (int i = 0; i < M; ++i) {
           if (!valid[i]) continue;
-          const double wz = wt[i] + __dmul_rn(code[i], delta);
+          const double zz = __dmul_rn(code[i], delta);
+          const double wz = base0 ? zz : wt[i] + zz;
           a0 = fma(xc[i], wz, a0);
           b0 = fma(xc[i], wt[i], b0);
         }
@@ -309,7 +313,8 @@ __global__ void __launch_bounds__(256, 1) k3_inner(InParams p) {
 #pragma unroll
         for (int i = 0; i < M; ++i) {
           if (!valid[i]) continue;
-          const double wz = wt[i] + __dmul_rn(code[i], delta);
+          const double zz = __dmul_rn(code[i], delta);
+          const double wz = base0 ? zz : wt[i] + zz;
           if (cls[i] == cS) {
             a0 = fma(xc[i], wz, a0);
             b0 = fma(xc[i], wt[i], b0);
@@ -396,7 +401,7 @@ __global__ void __launch_bounds__(256, 1) k3_inner(InParams p) {
     }
     K3_MARK(1);
     // ---- work independent of the exchange, done while it is in flight ----
-    if (!last) {
+    if (!last && !fp_inner) {
       uint64_t s = rs;
 #pragma unroll
       for (int i = 0; i < M; ++i) {
@@ -552,22 +557,23 @@ __global__ void __launch_bounds__(256, 1) k3_inner(InParams p) {
 
     // ---- element-wise update + stochastic rounding (branch-free) ----
     bool bad = false, slow_any = false;
-    bool slow[M];
+    bool slow[M] = {};
 #pragma unroll
     for (int i = 0; i < M; ++i) {
       const bool inA = cls[i] == cA;
       const double pp1 = inA ? p1A : p1B, pp2 = inA ? p2A : p2B;
       const double z = __dmul_rn(code[i], delta);
-      const double wz = wt[i] + z;
+      const double wz = base0 ? z : wt[i] + z;
       const double g1 = __dmul_rn(pp1, xc[i]) + __dmul_rn(l2, wz);
       const double g2 = __dmul_rn(pp2, xc[i]) + l2w[i];
       const double u = z - __dmul_rn(alpha, (g1 - g2) + gt[i]);
       up[i] = u;
       bad |= valid[i] && !isfinite(u);
-      code[i] = quantize_fast(u, delta, rcp, p.hi, p.lo, Ua[i], slow[i]);
-      slow_any |= valid[i] && slow[i];
+      code[i] = fp_inner ? u : quantize_fast(u, delta, rcp, p.hi, p.lo, Ua[i], slow[i]);
+      slow_any |= !fp_inner && valid[i] && slow[i];
     }
-    if (slow_any || wide || rcp == 0.0) {  // IEEE-division path for the rare operands
+    if (fp_inner) bad = false;  // SVRG: no finiteness check inside the epoch (optimizers.cpp:283-286)
+    if (!fp_inner && (slow_any || wide || rcp == 0.0)) {  // IEEE-division path for the rare operands
 #pragma unroll
       for (int i = 0; i < M; ++i)
         if (valid[i] && (slow[i] || wide || rcp == 0.0))
@@ -592,8 +598,10 @@ __global__ void __launch_bounds__(256, 1) k3_inner(InParams p) {
   for (int i = 0; i < M; ++i) {
     if (!valid[i]) continue;
     const double zc = p.t_pick >= 0 ? snap[i] : code[i];
-    p.w_out[k0 + i] = wt[i] + __dmul_rn(zc, delta);
-    p.codes_out[k0 + i] = __double2ll_rn(code[i]);
+    const double zr = __dmul_rn(zc, delta);
+    p.w_out[k0 + i] = base0 ? zr : wt[i] + zr;
+    p.codes_out[k0 + i] = fp_inner ? 0 : __double2ll_rn(code[i]);
+    if (p.zc_out) p.zc_out[k0 + i] = zc;
   }
 #ifdef HALP_K3_PROF
   if (prof_on)

@@ -81,6 +81,12 @@ struct InParams {
   int64_t trace_steps;
   int* blow_step;            // -1 or failing step index
   double* u_out;             // [D] update vector of the failing step
+  // algorithm: 0 HALP (wz = w~ + z, z = Q(u)), 1 LP-SVRG (fixed scale: the
+  // iterate itself is quantized, wz = z), 2 SVRG (fp64 iterate in z, delta = 1,
+  // no rounding, no blow-up check); w is the anchor of g2 in every mode
+  int mode;
+  const double* z0;          // [D] initial z values (code * delta units: codes) or null = 0
+  double* zc_out;            // [D] codes of the epoch's result (snapshot under option II) or null
 };
 struct InLaunch {
   int dtype, ctas, threads, per, nslot_pow2;

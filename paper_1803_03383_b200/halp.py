@@ -318,7 +318,7 @@ def _to_c_config(cfg: OptimizerConfig, keep: list) -> A.Config:
     return A.Config(float(cfg.alpha), int(cfg.epochs), int(cfg.inner_steps), int(cfg.bits), float(cfg.mu),
                     int(cfg.option), int(cfg.full_grad_period), int(cfg.seed) & (2**64 - 1),
                     float(cfg.metric_every_passes), float(cfg.delta_min), float(cfg.divergence_limit),
-                    init.ctypes.data if init is not None else None)
+                    init.ctypes.data if init is not None else None, float(cfg.delta), int(cfg.algorithm))
 
 
 def _record(rec: A.Record, rows, fin: np.ndarray) -> RunRecord:
@@ -352,8 +352,28 @@ def hash_vector(v) -> int:
 def run_halp(obj: Objective, cfg: OptimizerConfig, trace: Optional[np.ndarray] = None) -> RunRecord:
     """lpopt::run_halp (optimizers.cpp:387-459) on the B200.  `trace`, an
     int64 array, receives the z codes of every inner step (test hook)."""
+    return _run_algo(obj, cfg, Algorithm.Halp, trace)
+
+
+def run_svrg(obj: Objective, cfg: OptimizerConfig) -> RunRecord:
+    """lpopt::run_svrg (optimizers.cpp:258-296) on the same kernels: K1 at the
+    snapshot, K3 in full precision (z holds the fp64 iterate, no rounding)."""
+    return _run_algo(obj, cfg, Algorithm.Svrg, None)
+
+
+def run_lp_svrg(obj: Objective, cfg: OptimizerConfig, trace: Optional[np.ndarray] = None) -> RunRecord:
+    """lpopt::run_lp_svrg (optimizers.cpp:336-385): K3 with the iterate itself
+    quantized at the fixed scale cfg.delta (codes traced like HALP's z)."""
+    return _run_algo(obj, cfg, Algorithm.LpSvrg, trace)
+
+
+def _run_algo(obj: Objective, cfg: OptimizerConfig, algo: Algorithm, trace) -> RunRecord:
     if cfg.init is not None and np.asarray(cfg.init).size not in (0, obj.dim()):
         raise InvalidInputError("optimizer: init length does not match objective")
+    import copy
+
+    cfg = copy.copy(cfg)
+    cfg.algorithm = algo
     keep: list = []
     c = _to_c_config(cfg, keep)
     cap = max(cfg.epochs, 0) + 2
@@ -378,11 +398,15 @@ def run_halp(obj: Objective, cfg: OptimizerConfig, trace: Optional[np.ndarray] =
 
 
 def run(obj: Objective, cfg: OptimizerConfig) -> RunRecord:
-    """lpopt::run (optimizers.cpp:629-639): the Halp branch is the B200 path;
-    the other algorithms are outside this build's scope."""
+    """lpopt::run (optimizers.cpp:629-639): Halp, Svrg and LpSvrg run on the
+    B200; Sgd, LpSgd and LmHalp are outside this build's scope."""
     if cfg.algorithm == Algorithm.Halp:
         return run_halp(obj, cfg)
-    raise UnsupportedError(f"algorithm {Algorithm(cfg.algorithm).name} is not on the B200 hot path")
+    if cfg.algorithm == Algorithm.Svrg:
+        return run_svrg(obj, cfg)
+    if cfg.algorithm == Algorithm.LpSvrg:
+        return run_lp_svrg(obj, cfg)
+    raise UnsupportedError(f"algorithm {Algorithm(cfg.algorithm).name} is not on the B200 path")
 
 
 def run_prepared(obj: Objective, cfg: OptimizerConfig, data_seed: int = 0) -> RunRecord:
