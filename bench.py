@@ -178,6 +178,40 @@ def fullgrad_sweep(H, cfg, device, reps, world, rank, nccl_id):
     return ms, algo_bytes, pl
 
 
+GRID = dict(n=1000, d=64, alphas=17, mus=13, seeds=(1, 2, 3), epochs=10, T=2000)
+
+
+def grid_configs(H):
+    """the reference's conditioning-sweep grid (harness.cpp:462-468: 17 step
+    sizes x 13 scales per width) on one 1000 x 64 least-squares problem"""
+    alphas = [float(a) for a in np.logspace(-4, -1, GRID["alphas"])]
+    mus = [float(m) for m in np.logspace(-1, 2, GRID["mus"])]
+    base = H.OptimizerConfig(algorithm=H.Algorithm.Halp, alpha=1e-3, epochs=GRID["epochs"], inner_steps=GRID["T"],
+                             bits=8, mu=1.0, seed=0)
+    return base, [H.GridAxis("alpha", alphas), H.GridAxis("mu", mus)]
+
+
+def grid_bench(H, device):
+    """grid_search over the shared dataset: every (alpha, mu, seed) run in one K5 launch"""
+    import torch
+
+    X, y = H.generate("regression", GRID["n"], GRID["d"], dtype="f64", noise_sd=0.1, seed=42, device=device)
+    obj = H.Objective(H.Dataset(X, targets=y), H.LossFamily.Squared, 0.0, device=device)
+    base, axes = grid_configs(H)
+    H.grid_search(obj, base, [H.GridAxis("alpha", axes[0].values[:2]), H.GridAxis("mu", axes[1].values[:2])], [1])
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    res = H.grid_search(obj, base, axes, GRID["seeds"])
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t0
+    runs = len(res.points) * len(GRID["seeds"])
+    return {"workload": "grid_search (harness.cpp:379-447): 17 alpha x 13 mu x 3 seeds on one 1000x64 f64 "
+                        "least-squares problem, HALP b=8, T=2000, K=10; all runs in one K5 launch",
+            "runs": runs, "wall_ms": 1000.0 * dt, "runs_per_s": runs / dt, "device_ms": res.device_ms,
+            "best": {"alpha": res.best_config.alpha, "mu": res.best_config.mu,
+                     "grad_norm": res.points[res.best_index].mean_metric}}, (X.cpu().numpy(), y.cpu().numpy())
+
+
 def c5_batch(H, device, rank, reps=1):
     """BASELINE C5: 512 independent least-squares HALP problems per GPU (4096 x 128
     fp32 Gaussian, per-problem seeds, alpha log-uniform [1e-4, 1e-2], b in {8, 16}
@@ -366,6 +400,13 @@ def main():
                  "scaling": "weak (problems sharded, no collective)"}
         torch.cuda.empty_cache()
 
+    # ---------------- batched grid search (rank 0 of every replica) ----------------
+    grid, grid_data = None, None
+    if not args.no_batch:
+        barrier()
+        grid, grid_data = grid_bench(H, local)
+        torch.cuda.empty_cache()
+
     # ---------------- CPU baseline (rank 0, N=1 only) ----------------
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -383,6 +424,17 @@ def main():
                "sample": f"1 C2 epoch with T={sample_T} (inner loop scaled x{C2['n'] // sample_T} to T=N); "
                          "REF-order oracle, single thread like run_halp (optimizers.cpp:401)",
                "measured_seconds": dt}
+        if grid_data is not None:
+            # the reference's grid runs its points one after another (harness.cpp:415-417):
+            # time 6 of the grid's runs on one core
+            gX, gy = grid_data
+            go = O.OracleObjective(gX, y=gy)
+            t0 = time.perf_counter()
+            for a_ in (1e-3, 1e-2):
+                for sd in GRID["seeds"]:
+                    O.run_halp(go, O.OracleConfig(alpha=a_, epochs=GRID["epochs"], inner_steps=GRID["T"], bits=8,
+                                                  mu=1.0, seed=sd))
+            cpu["grid_runs_per_s"] = 6 / (time.perf_counter() - t0)
 
     if rank == 0:
         line = {
@@ -398,7 +450,7 @@ def main():
                            "share_of_epoch": tim["inner_ms"] / ms_total if world == 1 else None},
             "c2_fullgrad_ms_per_pass": tim["fullgrad_ms"] / c2_fg_passes,
             "loss_first_last": [first_loss, final_loss],
-            "fullgrad": fullgrad, "batch": batch, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "fullgrad": fullgrad, "batch": batch, "grid": grid, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": gpu_launches, "clocks": clocks,
         }
         print(json.dumps(line), flush=True)

@@ -678,6 +678,27 @@ int halp_problem_create(const halp_problem_desc* desc, halp_problem** out) {
   }
   rc = ensure_workspace(p);
   if (rc) return bail(rc);
+  // load and configure the planned K1 / K3 kernels now (lazy module loading
+  // would otherwise put a first-launch delay of several ms inside a solve's
+  // first epoch and inside its event-timed kernels)
+  {
+    FgLaunch L = p->fg;
+    L.nsplit_local = (int)p->sp.local_splits();
+    L.dry = 1;
+    FgParams fp = fg_params(p, 0);
+    if (launch_fullgrad(L, fp, p->stream) != cudaSuccess) return bail(fail(HALP_CUDA_ERROR, "K1 preparation failed"));
+    InLaunch IL = p->in;
+    IL.dry = 1;
+    InParams ip{};
+    ip.loss = p->loss;
+    ip.d = p->d;
+    ip.C = p->C;
+    ip.D = (int)p->D;
+    for (int mode = 0; mode < 2; ++mode) {
+      ip.mode = mode;
+      if (launch_inner(IL, ip, p->stream) != cudaSuccess) return bail(fail(HALP_CUDA_ERROR, "K3 preparation failed"));
+    }
+  }
   // bf16 two-class sweeps may convert X with integer ops (k1_stream); that
   // needs every element finite, checked once here on the device
   if (p->dtype == HALP_BF16 && C == 2 && env_int("HALP_FG_F2F", 0) == 0) {

@@ -294,6 +294,7 @@ static cudaError_t launch_fg_t(const FgLaunch& L, const FgParams& p, cudaStream_
   const size_t smem = fg_smem_bytes(L.ld, (int)sizeof(Tx), p.d * p.C, p.C, L.threads, R, STAGES);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
+  if (L.dry) return cudaSuccess;
   kern<<<L.nsplit_local, L.threads, smem, st>>>(p);
   return cudaGetLastError();
   }

@@ -223,6 +223,7 @@ static cudaError_t launch_smx_t(const FgLaunch& L, const FgParams& p, cudaStream
     auto kern = k1_smx<Tx, CC>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
+    if (L.dry) return cudaSuccess;
     kern<<<L.nsplit_local, L.threads, smem, st>>>(p);
     return cudaGetLastError();
   }

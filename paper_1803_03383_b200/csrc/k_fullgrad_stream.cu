@@ -378,6 +378,7 @@ cudaError_t launch_stream_k(const FgLaunch& L, const FgParams& p, cudaStream_t s
   if (per_sm < 1) return cudaErrorInvalidConfiguration;
   int grid = sms * per_sm;
   if (grid > L.nsplit_local) grid = L.nsplit_local;
+  if (L.dry) return cudaSuccess;
   kern<<<grid, NW * 32, smem, st>>>(p, L.nsplit_local);
   return cudaGetLastError();
 }

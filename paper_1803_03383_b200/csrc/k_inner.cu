@@ -143,7 +143,7 @@ struct K3Layout {
 // (arithmetic never produces it; NaN logits make receivers rescan for it).
 constexpr long long kFlagBits = 0x7FF4A1B2C3D4E5F6LL;
 
-template <class Tx, int M, bool CL, int KIND>
+template <class Tx, int M, bool CL, int KIND, bool BASE0>
 __global__ void __launch_bounds__(256, 1) k3_inner(InParams p) {
   constexpr int NSLOT = K3Layout<KIND>::NSLOT;
   constexpr int FLAG = K3Layout<KIND>::FLAG;
@@ -243,7 +243,7 @@ __global__ void __launch_bounds__(256, 1) k3_inner(InParams p) {
     wt[i] = valid[i] ? p.w[k] : 0.0;
     gt[i] = valid[i] ? p.g[k] : 0.0;
     l2w[i] = __dmul_rn(l2, wt[i]);
-    code[i] = (valid[i] && p.z0) ? p.z0[k] : 0.0;
+    code[i] = (BASE0 && valid[i] && p.z0) ? p.z0[k] : 0.0;
     snap[i] = code[i];
     up[i] = 0.0;
     Ua[i] = 0.0;
@@ -259,9 +259,9 @@ __global__ void __launch_bounds__(256, 1) k3_inner(InParams p) {
   // vector row loads when the thread's coordinates are aligned and in one class
   const bool vecx = (d % M == 0) && (ld % M == 0);
   const int64_t T = p.T;
-  // HALP: wz = w~ + z; LP-SVRG / SVRG: the iterate is z itself (base 0)
-  const bool base0 = p.mode != 0;
-  const bool fp_inner = p.mode == 2;
+  // HALP: wz = w~ + z; LP-SVRG / SVRG (BASE0 instantiations): the iterate is z itself
+  constexpr bool base0 = BASE0;
+  const bool fp_inner = BASE0 && p.mode == 2;
   uint64_t rs = jump_count(p.rstate0, (uint64_t)(k0 < D ? k0 : 0), p.pow_tab);
 
   // rows of steps 0 and 1 in flight (raw), the index of step 2 loaded
@@ -601,7 +601,7 @@ __global__ void __launch_bounds__(256, 1) k3_inner(InParams p) {
     const double zr = __dmul_rn(zc, delta);
     p.w_out[k0 + i] = base0 ? zr : wt[i] + zr;
     p.codes_out[k0 + i] = fp_inner ? 0 : __double2ll_rn(code[i]);
-    if (p.zc_out) p.zc_out[k0 + i] = zc;
+    if (BASE0 && p.zc_out) p.zc_out[k0 + i] = zc;
   }
 #ifdef HALP_K3_PROF
   if (prof_on)
@@ -617,19 +617,20 @@ __global__ void __launch_bounds__(256, 1) k3_inner(InParams p) {
   if (CL) cluster_sync_all();  // keep every CTA's shared memory alive until all remote stores landed
 }
 
-template <class Tx, int M, int KIND>
-static cudaError_t launch_in_t(const InLaunch& L, const InParams& p, cudaStream_t st) {
+template <class Tx, int M, int KIND, bool BASE0>
+static cudaError_t launch_in_b(const InLaunch& L, const InParams& p, cudaStream_t st) {
   if (L.ctas * L.threads / 32 > kMaxWarpsPerCluster) return cudaErrorInvalidConfiguration;
   const size_t smem = sizeof(double) * 2 * (size_t)(L.ctas * L.threads / 32) * K3Layout<KIND>::NSLOT;
   if (L.ctas == 1) {
-    auto kern = k3_inner<Tx, M, false, KIND>;
+    auto kern = k3_inner<Tx, M, false, KIND, BASE0>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
+    if (L.dry) return cudaSuccess;
     kern<<<1, L.threads, smem, st>>>(p);
     return cudaGetLastError();
   }
   if (L.ctas > 16) return cudaErrorInvalidConfiguration;
-  auto kern = k3_inner<Tx, M, true, KIND>;
+  auto kern = k3_inner<Tx, M, true, KIND, BASE0>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   if (e != cudaSuccess) return e;
   e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -646,7 +647,15 @@ static cudaError_t launch_in_t(const InLaunch& L, const InParams& p, cudaStream_
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  if (L.dry) return cudaSuccess;
   return cudaLaunchKernelEx(&cfg, kern, p);
+}
+
+// HALP (mode 0) and the base-0 modes (LP-SVRG, SVRG) are separate instantiations
+template <class Tx, int M, int KIND>
+static cudaError_t launch_in_t(const InLaunch& L, const InParams& p, cudaStream_t st) {
+  if (p.mode == 0) return launch_in_b<Tx, M, KIND, false>(L, p, st);
+  return launch_in_b<Tx, M, KIND, true>(L, p, st);
 }
 
 template <class Tx, int M>

@@ -23,6 +23,7 @@ struct FgParams {
 struct FgLaunch {
   int dtype, ng, ct, threads, ld, nsplit_local;
   int fast, rows, stages;  // fast: 0 generic, 3 softmax C >= 3, 4 streaming C <= 2; rows per tile, ring depth
+  int dry;                 // 1: set the kernel's attributes (loads it under lazy module loading), no launch
 };
 size_t fg_smem_bytes(int ld, int elem, int D, int C, int threads, int R, int stages);
 cudaError_t launch_fullgrad(const FgLaunch& L, const FgParams& p, cudaStream_t st);
@@ -90,6 +91,7 @@ struct InParams {
 };
 struct InLaunch {
   int dtype, ctas, threads, per, nslot_pow2;
+  int dry;  // 1: load + configure the kernel only (see FgLaunch::dry)
 };
 cudaError_t launch_inner(const InLaunch& L, const InParams& p, cudaStream_t st);
 

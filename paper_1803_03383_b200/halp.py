@@ -445,6 +445,7 @@ class GridResult:
     points: List[GridOutcome] = field(default_factory=list)
     best_index: int = 0
     best_config: Optional[OptimizerConfig] = None
+    device_ms: float = 0.0  # K5 kernel time of a batched grid (not in the reference's struct)
 
 
 def _apply_param(cfg: OptimizerConfig, param: str, v: float) -> None:
@@ -524,9 +525,11 @@ def grid_search(obj: Objective, base: OptimizerConfig, axes, seeds, metric: str 
         ds = obj.ds
         b = BatchProblems(ds.X, ds.targets, l2=obj.l2(), device=obj.device, nprob=len(cfgs))
         recs = b.run(cfgs)
+        device_ms = b.device_ms
     else:
         recs = [run_prepared(obj, c, data_seed) for c in cfgs]
-    res = GridResult()
+        device_ms = 0.0
+    res = GridResult(device_ms=device_ms)
     best = math.inf
     for pi, (params, cfg) in enumerate(points):
         out = GridOutcome(params=params, status="ok")

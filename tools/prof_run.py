@@ -21,7 +21,7 @@ def main(which):
         rec = H.run_halp(obj, H.OptimizerConfig(algorithm=H.Algorithm.Halp, alpha=0.01, epochs=1, inner_steps=steps,
                                                 bits=8, mu=2.5, seed=0))
         t = obj.timing()
-        print("c2", rec.rows[-1].loss, "inner us/step", 1000 * t["inner_ms"] / steps, t)
+        print("c2", rec.rows[-1].loss, "inner us/step", 1000 * t["inner_ms"] / steps, obj.plan(), t)
     elif which == "c3":
         X, y = H.generate("regression", 524288, 4096, dtype="f32", noise_sd=0.1, seed=3)
         obj = H.Objective(H.Dataset(X, targets=y), H.LossFamily.Squared, 0.0)
