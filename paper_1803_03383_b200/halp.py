@@ -419,6 +419,61 @@ def run_prepared(obj: Objective, cfg: OptimizerConfig, data_seed: int = 0) -> Ru
         return e.partial
 
 
+# ---------------------------------------------------------------- traces
+def format_double(x: float) -> str:
+    """lpopt::format_double (text.hpp:12-19): std::to_chars' shortest
+    round-trip form -- the fewest significant digits that read back to x, in
+    fixed or scientific notation, whichever is shorter (fixed on a tie);
+    exponents carry a sign and at least two digits (printf's %e); integral
+    values in fixed notation print their exact digits."""
+    x = float(x)
+    if math.isnan(x):
+        return "-nan" if math.copysign(1.0, x) < 0 else "nan"
+    if math.isinf(x):
+        return "-inf" if x < 0 else "inf"
+    sign = "-" if math.copysign(1.0, x) < 0 else ""
+    if x == 0.0:
+        return sign + "0"
+    # shortest round-trip digits (Python's repr is shortest round-trip too)
+    r = repr(abs(x))
+    mant, _, ex = r.partition("e")
+    e10 = int(ex) if ex else 0
+    ip, _, fp = mant.partition(".")
+    digits = (ip + fp).lstrip("0")
+    # decimal exponent of the first significant digit
+    if ip.strip("0"):
+        point = len(ip.lstrip("0")) + e10  # digits before the decimal point
+    else:
+        point = -(len(fp) - len(fp.lstrip("0"))) + e10
+    digits = digits.rstrip("0") or "0"
+    n = len(digits)
+    # scientific: d[.ddd]e+XX
+    sci_exp = point - 1
+    sci = digits[0] + ("." + digits[1:] if n > 1 else "") + ("e%+03d" % sci_exp)
+    # fixed
+    if point <= 0:
+        fixed = "0." + "0" * (-point) + digits
+    elif point >= n:
+        fixed = str(int(abs(x)))  # an integer: to_chars prints its exact digits
+    else:
+        fixed = digits[:point] + "." + digits[point:]
+    return sign + (fixed if len(fixed) <= len(sci) else sci)
+
+
+def write_run_csv(path: str, rec: RunRecord) -> None:
+    """lpopt::write_run_csv (harness.cpp:246-261): one row per MetricRow,
+    `pass,seconds,loss,grad_norm,delta`, every number by format_double."""
+    s = "pass,seconds,loss,grad_norm,delta\n"
+    for r in rec.rows:
+        s += ",".join(format_double(v) for v in (r.pass_, r.seconds, r.loss, r.grad_norm, r.delta)) + "\n"
+    import os
+
+    tmp = path + ".tmp"
+    with open(tmp, "w", newline="") as f:  # write_text_atomic: write then rename
+        f.write(s)
+    os.replace(tmp, path)
+
+
 # ---------------------------------------------------------------- grid search
 @dataclass
 class GridAxis:
