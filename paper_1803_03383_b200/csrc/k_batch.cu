@@ -68,7 +68,7 @@ __device__ __forceinline__ uint64_t fnv1a_doubles(const double* v, int len) {
 
 // NG groups of V features per lane (NG*V*32 >= d)
 template <class Tx, int NG, int M>
-__global__ void __launch_bounds__(128) k5_batch(BatchParams p) {
+__global__ void __launch_bounds__(128, (M <= 4) ? 4 : 1) k5_batch(BatchParams p) {
   constexpr int V = BVec<Tx>::V;
   const int prob = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
