@@ -93,8 +93,8 @@ typedef struct {
   int32_t       algorithm;            /* HALP_ALGO_*: lpopt::Algorithm numbering; ABI >= 3 */
 } halp_config;
 
-/* lpopt::Algorithm values halp_run accepts (optimizers.hpp:13-15) */
-enum { HALP_ALGO_SVRG = 1, HALP_ALGO_LP_SVRG = 3, HALP_ALGO_HALP = 4 };
+/* lpopt::Algorithm values halp_run accepts (optimizers.hpp:13-15; all but LmHalp) */
+enum { HALP_ALGO_SGD = 0, HALP_ALGO_SVRG = 1, HALP_ALGO_LP_SGD = 2, HALP_ALGO_LP_SVRG = 3, HALP_ALGO_HALP = 4 };
 
 /* lpopt::MetricRow (optimizers.hpp:49-58), HALP subset */
 typedef struct {

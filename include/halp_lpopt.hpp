@@ -231,13 +231,24 @@ inline RunRecord run_lp_svrg(const Objective& obj, const OptimizerConfig& cfg) {
   return detail::run_algo(obj, cfg, HALP_ALGO_LP_SVRG);
 }
 
+// lpopt::run_sgd (optimizers.cpp:229-256)
+inline RunRecord run_sgd(const Objective& obj, const OptimizerConfig& cfg) {
+  return detail::run_algo(obj, cfg, HALP_ALGO_SGD);
+}
+// lpopt::run_lp_sgd (optimizers.cpp:297-334)
+inline RunRecord run_lp_sgd(const Objective& obj, const OptimizerConfig& cfg) {
+  return detail::run_algo(obj, cfg, HALP_ALGO_LP_SGD);
+}
+
 // lpopt::run (optimizers.cpp:629-639): the branches this library runs on the B200
 inline RunRecord run(const Objective& obj, const OptimizerConfig& cfg) {
   switch (cfg.algorithm) {
     case Algorithm::Halp: return run_halp(obj, cfg);
     case Algorithm::Svrg: return run_svrg(obj, cfg);
     case Algorithm::LpSvrg: return run_lp_svrg(obj, cfg);
-    default: throw UnsupportedError("algorithm not on the B200 path (Sgd, LpSgd, LmHalp)");
+    case Algorithm::Sgd: return run_sgd(obj, cfg);
+    case Algorithm::LpSgd: return run_lp_sgd(obj, cfg);
+    default: throw UnsupportedError("algorithm not on the B200 path (LmHalp)");
   }
 }
 

@@ -859,7 +859,7 @@ static int validate_config(const oq_objective* o, const oq_config* c) {
     return OQ_INVALID_INPUT;
   }
   if (!(isfinite(c->delta_min) && c->delta_min > 0.0)) { set_err("optimizer: delta_min must be positive"); return OQ_INVALID_INPUT; }
-  if (c->algorithm == OQ_ALGO_LP_SVRG) { /* uses_fixed_scale */
+  if (c->algorithm == OQ_ALGO_LP_SVRG || c->algorithm == OQ_ALGO_LP_SGD) { /* uses_fixed_scale */
     if (c->bits < 2 || c->bits > 64) { set_err("optimizer: bits must be in [2, 64]"); return OQ_INVALID_INPUT; }
     if (!(isfinite(c->delta) && c->delta > 0.0)) {
       set_err("optimizer: delta must be positive for fixed-scale runs");
@@ -1212,8 +1212,103 @@ done:
   return rc;
 }
 
+/* optimizers.cpp:229-256 run_sgd (lp = 0) and :297-334 run_lp_sgd (lp = 1):
+ * w -= alpha*g (SGD, no in-epoch finiteness check) or w = Q(w - alpha*g) at
+ * the fixed scale (the initial iterate quantized once; blow-up rows). */
+static int run_sgd_family(const oq_objective* o, const oq_config* cfg, const oq_plan* plan, oq_record* rec, int lp) {
+  int rc = check_objective(o);
+  if (rc) return rc;
+  rc = validate_config(o, cfg);
+  if (rc) return rc;
+  const int d = o->d, C = o->C, D = d * C;
+  const int64_t n = o->n;
+  const int64_t T = oq_resolve_inner_steps(cfg, n);
+  if (T < 1) { set_err("optimizer: epoch length must be >= 1"); return OQ_INVALID_INPUT; }
+  const double rdelta = lp ? cfg->delta : 0.0;
+  oq_rng sample, rounder;
+  oq_rng_init(&sample, cfg->seed, 0);
+  oq_rng_init(&rounder, cfg->seed, 1);
+  double* w = (double*)calloc((size_t)D, sizeof(double));
+  double* u = (double*)malloc(sizeof(double) * (size_t)D);
+  double* g = (double*)malloc(sizeof(double) * (size_t)D);
+  double* g2 = (double*)malloc(sizeof(double) * (size_t)D);
+  double* gt = (double*)malloc(sizeof(double) * (size_t)D);
+  double* x = (double*)malloc(sizeof(double) * (size_t)d);
+  int64_t* w_lp = (int64_t*)calloc((size_t)D, sizeof(int64_t));
+  if (cfg->init) memcpy(w, cfg->init, sizeof(double) * (size_t)D);
+  if (lp) {
+    for (int q = 0; q < D; ++q) {
+      const double uu = oq_next_uniform(&rounder);
+      int err = 0;
+      w_lp[q] = oq_quantize_code(w[q], cfg->delta, cfg->bits, uu, &err);
+      if (err) { set_err("quantize: non-finite input"); rc = OQ_INVALID_INPUT; goto done; }
+    }
+    for (int q = 0; q < D; ++q) w[q] = (double)w_lp[q] * cfg->delta;
+  }
+  rec->rows_n = 0;
+  rec->status = OQ_STATUS_OK;
+  rec->steps_taken = 0;
+  rec->inner_fp_vector_ops = 0;
+  rec->fullgrad_seconds = 0.0;
+  rec->inner_seconds = 0.0;
+  recorder r = {cfg, rec, now_s(), 0.0, D};
+  int64_t steps = 0, traced = 0;
+  const int fgth = rec->fullgrad_threads > 0 ? rec->fullgrad_threads : 1;
+  for (int k = 0; k < cfg->epochs; ++k) {
+    double gn, dl, loss;
+    measure(o, w, cfg, plan, fgth, gt, &gn, &dl, &loss, &rec->fullgrad_seconds);
+    rc = rec_boundary(&r, (double)steps / (double)n, w, loss, gn, rdelta, k == 0);
+    if (rc) goto done;
+    const double ti0 = now_s();
+    for (int64_t t = 0; t < T; ++t) {
+      const int64_t i = (int64_t)oq_next_index(&sample, (uint64_t)n);
+      load_row(o, i, x);
+      component_pair(o, plan, x, i, w, w, g, g2);
+      if (!lp) {
+        for (int q = 0; q < D; ++q) w[q] = w[q] - cfg->alpha * g[q];
+        continue;
+      }
+      int finite = 1;
+      for (int q = 0; q < D; ++q) {
+        u[q] = w[q] - cfg->alpha * g[q];
+        if (!isfinite(u[q])) finite = 0;
+      }
+      if (!finite) {
+        rc = rec_boundary(&r, (double)(steps + t + 1) / (double)n, u, INFINITY, INFINITY, cfg->delta, 1);
+        goto done;
+      }
+      for (int q = 0; q < D; ++q) {
+        const double uu = oq_next_uniform(&rounder);
+        w_lp[q] = oq_quantize_code(u[q], cfg->delta, cfg->bits, uu, NULL);
+      }
+      for (int q = 0; q < D; ++q) w[q] = (double)w_lp[q] * cfg->delta;
+      if (rec->trace_codes && traced + D <= rec->trace_cap) {
+        memcpy(rec->trace_codes + traced, w_lp, sizeof(int64_t) * (size_t)D);
+        traced += D;
+      }
+    }
+    rec->inner_seconds += now_s() - ti0;
+    rec->inner_fp_vector_ops += (uint64_t)((lp ? 5 : 3) * T); /* component gradient (2) + update (+ quantize, to_real) */
+    steps += T;
+  }
+  {
+    double gn, dl, loss;
+    measure(o, w, cfg, plan, fgth, gt, &gn, &dl, &loss, &rec->fullgrad_seconds);
+    rc = rec_boundary(&r, (double)steps / (double)n, w, loss, gn, rdelta, 1);
+    if (rc) goto done;
+  }
+  memcpy(rec->final_iterate, w, sizeof(double) * (size_t)D);
+  rec->steps_taken = steps;
+done:
+  if (rc == OQ_DIVERGED) rec->steps_taken = 0;
+  free(w); free(u); free(g); free(g2); free(gt); free(x); free(w_lp);
+  return rc;
+}
+
 int oq_run(const oq_objective* o, const oq_config* cfg, const oq_plan* plan, oq_record* rec) {
   switch (cfg->algorithm) {
+    case OQ_ALGO_SGD: return run_sgd_family(o, cfg, plan, rec, 0);
+    case OQ_ALGO_LP_SGD: return run_sgd_family(o, cfg, plan, rec, 1);
     case OQ_ALGO_HALP: return oq_run_halp(o, cfg, plan, rec);
     case OQ_ALGO_SVRG: return run_svrg_family(o, cfg, plan, rec, 0);
     case OQ_ALGO_LP_SVRG: return run_svrg_family(o, cfg, plan, rec, 1);

@@ -116,10 +116,10 @@ typedef struct {
   double   divergence_limit;
   const double* init;            /* NULL => zeros */
   double   delta;                /* fixed scale of LP-SVRG (OptimizerConfig::delta) */
-  int32_t  algorithm;            /* lpopt::Algorithm: 1 Svrg, 3 LpSvrg, 4 Halp */
+  int32_t  algorithm;            /* lpopt::Algorithm: 0 Sgd, 1 Svrg, 2 LpSgd, 3 LpSvrg, 4 Halp */
 } oq_config;
 
-enum { OQ_ALGO_SVRG = 1, OQ_ALGO_LP_SVRG = 3, OQ_ALGO_HALP = 4 };
+enum { OQ_ALGO_SGD = 0, OQ_ALGO_SVRG = 1, OQ_ALGO_LP_SGD = 2, OQ_ALGO_LP_SVRG = 3, OQ_ALGO_HALP = 4 };
 
 typedef struct {
   double   pass, seconds, loss, grad_norm, delta;

@@ -276,7 +276,7 @@ def _plan(p):
 @dataclass
 class OracleConfig:
     """lpopt::OptimizerConfig fields of the restated algorithms (optimizers.hpp:31-47);
-    algorithm: 1 Svrg, 3 LpSvrg, 4 Halp (run() dispatches, run_halp forces 4)."""
+    algorithm: 0 Sgd, 1 Svrg, 2 LpSgd, 3 LpSvrg, 4 Halp (run() dispatches, run_halp forces 4)."""
 
     alpha: float = 1e-3
     epochs: int = 1
@@ -315,7 +315,7 @@ def run_halp(obj: OracleObjective, cfg: OracleConfig, plan=None, trace_steps: in
 
 def run(obj: OracleObjective, cfg: OracleConfig, plan=None, trace_steps: int = 0, fullgrad_threads: int = 1,
         rows_cap: int = 0) -> OracleRecord:
-    """lpopt::run (optimizers.cpp:629-639) over Svrg (1), LpSvrg (3), Halp (4)"""
+    """lpopt::run (optimizers.cpp:629-639) over Sgd (0), Svrg (1), LpSgd (2), LpSvrg (3), Halp (4)"""
     return _run(obj, cfg, plan, trace_steps, fullgrad_threads, rows_cap, int(cfg.algorithm))
 
 

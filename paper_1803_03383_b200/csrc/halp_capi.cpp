@@ -510,9 +510,9 @@ int validate(const halp_problem* p, const halp_config* c) {
   if (!(std::isfinite(c->divergence_limit) && c->divergence_limit > 0.0))
     return fail(HALP_INVALID_INPUT, "optimizer: divergence_limit must be positive");
   if (!(std::isfinite(c->delta_min) && c->delta_min > 0.0)) return fail(HALP_INVALID_INPUT, "optimizer: delta_min must be positive");
-  if (c->algorithm != HALP_ALGO_HALP && c->algorithm != HALP_ALGO_SVRG && c->algorithm != HALP_ALGO_LP_SVRG)
-    return fail(HALP_UNSUPPORTED, "optimizer: algorithm not on the B200 path (Svrg, LpSvrg, Halp are)");
-  if (c->algorithm == HALP_ALGO_LP_SVRG) {  // uses_fixed_scale
+  if (c->algorithm < HALP_ALGO_SGD || c->algorithm > HALP_ALGO_HALP)
+    return fail(HALP_UNSUPPORTED, "optimizer: algorithm not on the B200 path (LmHalp is not)");
+  if (c->algorithm == HALP_ALGO_LP_SVRG || c->algorithm == HALP_ALGO_LP_SGD) {  // uses_fixed_scale
     if (c->bits < 2 || c->bits > 64) return fail(HALP_INVALID_INPUT, "optimizer: bits must be in [2, 64]");
     if (!(std::isfinite(c->delta) && c->delta > 0.0))
       return fail(HALP_INVALID_INPUT, "optimizer: delta must be positive for fixed-scale runs");
@@ -798,12 +798,14 @@ int halp_run(halp_problem* p, const halp_config* cfg, halp_record* rec) {
   if (rc) return rc;
   CU(cudaSetDevice(p->device));
   const int algo = cfg->algorithm;
-  const bool halp = algo == HALP_ALGO_HALP, lp = algo == HALP_ALGO_LP_SVRG;
-  const int mode = halp ? 0 : lp ? 1 : 2;
+  const bool halp = algo == HALP_ALGO_HALP;
+  const bool lp = algo == HALP_ALGO_LP_SVRG || algo == HALP_ALGO_LP_SGD;  // fixed-scale quantized iterate
+  const bool sgd = algo == HALP_ALGO_SGD || algo == HALP_ALGO_LP_SGD;    // no variance reduction, no option II
+  const int mode = halp ? 0 : algo == HALP_ALGO_LP_SVRG ? 1 : algo == HALP_ALGO_SVRG ? 2 : algo == HALP_ALGO_SGD ? 3 : 4;
   const int64_t n = p->n, D = p->D;
   const int64_t T = cfg->inner_steps > 0 ? cfg->inner_steps : (int64_t)cfg->full_grad_period * n;
   if (T < 1) return fail(HALP_INVALID_INPUT, "optimizer: epoch length must be >= 1");
-  const int opt2 = cfg->option == 1;
+  const int opt2 = cfg->option == 1 && !sgd;
   p->timing = halp_timing{};
   if (p->idx_cap < T) {
     if (p->idx) cudaFreeAsync(p->idx, p->stream);
@@ -816,7 +818,7 @@ int halp_run(halp_problem* p, const halp_config* cfg, halp_record* rec) {
   std::vector<double> wh(D, 0.0);
   if (cfg->init) std::memcpy(wh.data(), cfg->init, sizeof(double) * D);
   // z at the start of the first epoch: HALP resets it per epoch (Q(0));
-  // LP-SVRG quantizes the initial iterate once (D rounding draws); SVRG holds w itself
+  // LP-SVRG / LP-SGD quantize the initial iterate once (D rounding draws); SVRG / SGD hold w itself
   std::vector<double> z0(D, 0.0);
   if (lp) {
     uint64_t st = s_round;
@@ -861,7 +863,7 @@ int halp_run(halp_problem* p, const halp_config* cfg, halp_record* rec) {
   const long long minc = bits == 64 ? INT64_MIN : -(1LL << (bits - 1));
   // instr counters per inner step: two component gradients (2 each) + the
   // update (+ quantize_vector, to_real; HALP counts both its updates)
-  const uint64_t ops_per_step = halp ? 8 : lp ? 7 : 5;
+  const uint64_t ops_per_step = halp ? 8 : sgd ? (lp ? 5 : 3) : (lp ? 7 : 5);
   const double mu = halp ? cfg->mu : 1.0;
   int64_t steps = 0;
   bool converged = false;

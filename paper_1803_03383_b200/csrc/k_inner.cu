@@ -259,9 +259,10 @@ __global__ void __launch_bounds__(256, 1) k3_inner(InParams p) {
   // vector row loads when the thread's coordinates are aligned and in one class
   const bool vecx = (d % M == 0) && (ld % M == 0);
   const int64_t T = p.T;
-  // HALP: wz = w~ + z; LP-SVRG / SVRG (BASE0 instantiations): the iterate is z itself
+  // HALP: wz = w~ + z; LP-SVRG / SVRG / SGD / LP-SGD (BASE0 instantiations): the iterate is z itself
   constexpr bool base0 = BASE0;
-  const bool fp_inner = BASE0 && p.mode == 2;
+  const bool fp_inner = BASE0 && (p.mode == 2 || p.mode == 3);  // SVRG, SGD: fp64 iterate
+  const bool plain = BASE0 && (p.mode == 3 || p.mode == 4);     // SGD, LP-SGD: u = w - alpha*g
   uint64_t rs = jump_count(p.rstate0, (uint64_t)(k0 < D ? k0 : 0), p.pow_tab);
 
   // rows of steps 0 and 1 in flight (raw), the index of step 2 loaded
@@ -566,13 +567,13 @@ __global__ void __launch_bounds__(256, 1) k3_inner(InParams p) {
       const double wz = base0 ? z : wt[i] + z;
       const double g1 = __dmul_rn(pp1, xc[i]) + __dmul_rn(l2, wz);
       const double g2 = __dmul_rn(pp2, xc[i]) + l2w[i];
-      const double u = z - __dmul_rn(alpha, (g1 - g2) + gt[i]);
+      const double u = plain ? z - __dmul_rn(alpha, g1) : z - __dmul_rn(alpha, (g1 - g2) + gt[i]);
       up[i] = u;
       bad |= valid[i] && !isfinite(u);
       code[i] = fp_inner ? u : quantize_fast(u, delta, rcp, p.hi, p.lo, Ua[i], slow[i]);
       slow_any |= !fp_inner && valid[i] && slow[i];
     }
-    if (fp_inner) bad = false;  // SVRG: no finiteness check inside the epoch (optimizers.cpp:283-286)
+    if (fp_inner) bad = false;  // SVRG / SGD: no finiteness check inside the epoch (optimizers.cpp:244-246, 283-286)
     if (!fp_inner && (slow_any || wide || rcp == 0.0)) {  // IEEE-division path for the rare operands
 #pragma unroll
       for (int i = 0; i < M; ++i)

@@ -84,7 +84,8 @@ struct InParams {
   double* u_out;             // [D] update vector of the failing step
   // algorithm: 0 HALP (wz = w~ + z, z = Q(u)), 1 LP-SVRG (fixed scale: the
   // iterate itself is quantized, wz = z), 2 SVRG (fp64 iterate in z, delta = 1,
-  // no rounding, no blow-up check); w is the anchor of g2 in every mode
+  // no rounding, no blow-up check), 3 SGD / 4 LP-SGD (as 2 / 1 with
+  // u = z - alpha*g1, no variance reduction); w is the anchor of g2
   int mode;
   const double* z0;          // [D] initial z values (code * delta units: codes) or null = 0
   double* zc_out;            // [D] codes of the epoch's result (snapshot under option II) or null

@@ -367,6 +367,18 @@ def run_lp_svrg(obj: Objective, cfg: OptimizerConfig, trace: Optional[np.ndarray
     return _run_algo(obj, cfg, Algorithm.LpSvrg, trace)
 
 
+def run_sgd(obj: Objective, cfg: OptimizerConfig) -> RunRecord:
+    """lpopt::run_sgd (optimizers.cpp:229-256): K3 with the fp64 iterate and
+    u = w - alpha*g (no snapshot gradient); K1 only for the boundary rows."""
+    return _run_algo(obj, cfg, Algorithm.Sgd, None)
+
+
+def run_lp_sgd(obj: Objective, cfg: OptimizerConfig, trace: Optional[np.ndarray] = None) -> RunRecord:
+    """lpopt::run_lp_sgd (optimizers.cpp:297-334): the iterate quantized at the
+    fixed scale cfg.delta after every step."""
+    return _run_algo(obj, cfg, Algorithm.LpSgd, trace)
+
+
 def _run_algo(obj: Objective, cfg: OptimizerConfig, algo: Algorithm, trace) -> RunRecord:
     if cfg.init is not None and np.asarray(cfg.init).size not in (0, obj.dim()):
         raise InvalidInputError("optimizer: init length does not match objective")
@@ -398,14 +410,12 @@ def _run_algo(obj: Objective, cfg: OptimizerConfig, algo: Algorithm, trace) -> R
 
 
 def run(obj: Objective, cfg: OptimizerConfig) -> RunRecord:
-    """lpopt::run (optimizers.cpp:629-639): Halp, Svrg and LpSvrg run on the
-    B200; Sgd, LpSgd and LmHalp are outside this build's scope."""
-    if cfg.algorithm == Algorithm.Halp:
-        return run_halp(obj, cfg)
-    if cfg.algorithm == Algorithm.Svrg:
-        return run_svrg(obj, cfg)
-    if cfg.algorithm == Algorithm.LpSvrg:
-        return run_lp_svrg(obj, cfg)
+    """lpopt::run (optimizers.cpp:629-639): Halp, Svrg, LpSvrg, Sgd and LpSgd
+    run on the B200; LmHalp is outside this build's scope."""
+    fns = {Algorithm.Halp: run_halp, Algorithm.Svrg: run_svrg, Algorithm.LpSvrg: run_lp_svrg,
+           Algorithm.Sgd: run_sgd, Algorithm.LpSgd: run_lp_sgd}
+    if cfg.algorithm in fns:
+        return fns[Algorithm(cfg.algorithm)](obj, cfg)
     raise UnsupportedError(f"algorithm {Algorithm(cfg.algorithm).name} is not on the B200 path")
 
 

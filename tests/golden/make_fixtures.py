@@ -2,7 +2,7 @@
 container only; /root/reference does not exist on the GPU box).
 
 Sources (reference outputs and known-answer tests, not source code):
-  proj/out/regression_floor/{halp-8,halp-16,svrg,lp-svrg-8,lp-svrg-16}_seed{1..5}.csv  golden traces
+  proj/out/regression_floor/{halp-8,halp-16,svrg,lp-svrg-8,lp-svrg-16,sgd,lp-sgd-8,lp-sgd-16}_seed{1..5}.csv  golden traces
   proj/out/regression_floor/manifest.json                        final values
   proj/specs/regression_floor.json                               their spec
   proj/tests/test_rng.cpp:14-31                                  RNG KATs
@@ -20,13 +20,13 @@ def traces():
     spec = json.load(open(f"{REF}/specs/regression_floor.json"))
     man = json.load(open(f"{REF}/out/regression_floor/manifest.json"))
     runs = {}
-    for name in ("halp-8", "halp-16", "svrg", "lp-svrg-8", "lp-svrg-16"):
+    for name in ("halp-8", "halp-16", "svrg", "lp-svrg-8", "lp-svrg-16", "sgd", "lp-sgd-8", "lp-sgd-16"):
         for seed in range(1, 6):
             fn = f"{REF}/out/regression_floor/{name}_seed{seed}.csv"
             rows = list(csv.DictReader(open(fn)))
             # keep the exact decimal strings (shortest round-trip, text.hpp:12-19)
             runs[f"{name}_seed{seed}"] = rows
-    finals = {f"{r['name']}_seed{r['seed']}": r for r in man["runs"] if r["name"] in ("halp-8", "halp-16", "svrg", "lp-svrg-8", "lp-svrg-16")}
+    finals = {f"{r['name']}_seed{r['seed']}": r for r in man["runs"] if r["name"] in ("halp-8", "halp-16", "svrg", "lp-svrg-8", "lp-svrg-16", "sgd", "lp-sgd-8", "lp-sgd-16")}
     json.dump({"source": "proj/out/regression_floor (lpopt run --spec specs/regression_floor.json)",
                "spec": spec, "traces": runs, "manifest": finals},
               open(os.path.join(OUT, "regression_floor.json"), "w"), indent=1)

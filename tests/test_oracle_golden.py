@@ -80,20 +80,27 @@ def test_golden_packet_width_is_sse2(oracle, obj):
     assert counts[2] == 12 and counts[2] > counts[1] and counts[2] > counts[4], counts
 
 
-@pytest.mark.parametrize("name,algo,kw,tol", [("svrg", 1, {}, 1e-9),
-                                              ("lp-svrg-8", 3, dict(delta=0.7, bits=8), 1e-15),
-                                              ("lp-svrg-16", 3, dict(delta=0.003, bits=16), 1e-15)])
+OPS = {0: 3, 1: 5, 2: 5, 3: 7}  # instr fp vector ops per inner step (objectives.cpp:249, optimizers.cpp, fixed_point.cpp)
+
+
+@pytest.mark.parametrize("name,algo,kw,tol", [("svrg", 1, dict(alpha=5e-3), 1e-9),
+                                              ("lp-svrg-8", 3, dict(alpha=5e-3, delta=0.7, bits=8), 1e-15),
+                                              ("lp-svrg-16", 3, dict(alpha=5e-3, delta=0.003, bits=16), 1e-15),
+                                              ("sgd", 0, dict(alpha=2.5e-6), 0.0),
+                                              ("lp-sgd-8", 2, dict(alpha=2.5e-6, delta=0.7, bits=8), 0.0),
+                                              ("lp-sgd-16", 2, dict(alpha=2.5e-6, delta=0.003, bits=16), 1e-15)])
 @pytest.mark.parametrize("seed", [1, 2, 3, 4, 5])
 def test_golden_svrg_family(oracle, obj, name, algo, kw, tol, seed):
-    """run_svrg / run_lp_svrg (optimizers.cpp:258-296, 336-385) restated,
-    against the golden traces svrg / lp-svrg-{8,16}_seed{1..5}.csv (spec rows
-    specs/regression_floor.json:8,11-12): every row within 1e-9 (SVRG) and
-    1e-15 (LP-SVRG, whose fixed-scale iterate makes it all but bit-exact)."""
-    cfg = oracle.OracleConfig(alpha=5e-3, epochs=25, inner_steps=2000, seed=seed, algorithm=algo, **kw)
+    """run_svrg / run_lp_svrg / run_sgd / run_lp_sgd (optimizers.cpp:229-385)
+    restated, against the golden traces {svrg, lp-svrg-{8,16}, sgd,
+    lp-sgd-{8,16}}_seed{1..5}.csv (spec rows specs/regression_floor.json:7-12):
+    every row within 1e-9 (SVRG), 1e-15 (LP-SVRG) and bit for bit (SGD,
+    LP-SGD-8; LP-SGD-16 to 1e-15)."""
+    cfg = oracle.OracleConfig(epochs=25, inner_steps=2000, seed=seed, algorithm=algo, **kw)
     rec = oracle.run(obj, cfg)
     gold = GOLD["traces"][f"{name}_seed{seed}"]
     assert len(rec.rows) == len(gold) == 26 and rec.status == "ok" and rec.steps_taken == 50000
-    assert rec.inner_fp_vector_ops == (5 if algo == 1 else 7) * 2000 * 25  # instr counters per step
+    assert rec.inner_fp_vector_ops == OPS[algo] * 2000 * 25
     for k, (a, b) in enumerate(zip(rec.rows, gold)):
         assert a["pass_"] == float(b["pass"])
         for f in ("loss", "grad_norm", "delta"):
