@@ -14,6 +14,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -131,9 +132,15 @@ uint64_t fnv1a(const double* v, int64_t len) {  // optimizers.cpp:218-227
 // Problems are created and destroyed per solve (run_prepared, sweeps, the e2e
 // path); keeping freed blocks in the pool makes that O(1) instead of a
 // cudaMalloc/cudaFree (and page-table work) per solve.
+std::mutex& host_state_mutex() {  // guards the per-device host-side caches below
+  static std::mutex m;
+  return m;
+}
+
 int pool_setup(int device) {
   static bool done[64] = {};
   if (device < 0 || device >= 64) return HALP_INVALID_INPUT;
+  std::lock_guard<std::mutex> lock(host_state_mutex());
   if (done[device]) return HALP_OK;
   cudaMemPool_t pool;
   if (cudaDeviceGetDefaultMemPool(&pool, device) != cudaSuccess) return HALP_CUDA_ERROR;
@@ -156,6 +163,7 @@ struct RngTables {
 int rng_tables(int device, int64_t D, const uint64_t** pow_tab, const uint64_t** jump_tab) {
   static RngTables per_dev[64];
   if (device < 0 || device >= 64) return fail(HALP_INVALID_INPUT, "device index out of range");
+  std::lock_guard<std::mutex> lock(host_state_mutex());
   RngTables& t = per_dev[device];
   const auto& jt = JumpTables::get();
   if (!t.pow_tab) {
