@@ -429,6 +429,38 @@ def run_prepared(obj: Objective, cfg: OptimizerConfig, data_seed: int = 0) -> Ru
         return e.partial
 
 
+# ---------------------------------------------------------------- clipping variants
+class ClipMode(enum.IntEnum):
+    """lpopt::ClipMode (optimizers.hpp:23): how the 16-bit variant of a narrow
+    bit-centered run keeps its dynamic range."""
+
+    Scale = 0
+    Clip = 1
+
+
+def clipping_variant_config(base: OptimizerConfig, mode: ClipMode) -> OptimizerConfig:
+    """optimizers.cpp:641-656: the same run at 16 bits; ClipMode.Scale also
+    rescales mu so the representable range (mu * span) is unchanged."""
+    import copy
+
+    if base.algorithm not in (Algorithm.Halp, Algorithm.LmHalp):
+        raise InvalidInputError("clipping variant applies to bit-centered runs only")
+    if base.bits >= 16:
+        raise InvalidInputError("clipping variant derives a 16-bit run; base must be narrower")
+    out = copy.deepcopy(base)
+    out.bits = 16
+    if mode == ClipMode.Scale:
+        span_base = math.ldexp(1.0, base.bits - 1) - 1.0
+        span16 = math.ldexp(1.0, 15) - 1.0
+        out.mu = base.mu * span_base / span16
+    return out
+
+
+def run_clipping_variant(obj: Objective, base: OptimizerConfig, mode: ClipMode) -> RunRecord:
+    """optimizers.cpp:658-661"""
+    return run(obj, clipping_variant_config(base, mode))
+
+
 # ---------------------------------------------------------------- traces
 def format_double(x: float) -> str:
     """lpopt::format_double (text.hpp:12-19): std::to_chars' shortest
