@@ -152,7 +152,7 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
-def fullgrad_sweep(H, cfg, device, reps, world, rank, nccl_id):
+def fullgrad_sweep(H, cfg, device, reps, world, rank, nccl_id, epoch_T=0):
     """K1 at a BASELINE full-gradient shape: average device ms per pass."""
     import torch
 
@@ -173,9 +173,29 @@ def fullgrad_sweep(H, cfg, device, reps, world, rank, nccl_id):
     ms = obj.bench_full_gradient(reps)
     es = 4 if cfg["dtype"] == "f32" else 2
     algo_bytes = rows * d * es + rows * ybytes
+    epoch = None
+    if cfg["dtype"] == "f32" and epoch_T:
+        # one full HALP epoch at C3: b = 16, T = N/8 (BASELINE); alpha, mu unspecified
+        # there -> 5e-5 (~0.2/|x|^2) and 1
+        c = H.OptimizerConfig(algorithm=H.Algorithm.Halp, alpha=5e-5, epochs=1, inner_steps=epoch_T, bits=16, mu=1.0,
+                              seed=0)
+        H.run_halp(obj, H.OptimizerConfig(algorithm=H.Algorithm.Halp, alpha=5e-5, epochs=1, inner_steps=1000, bits=16,
+                                          mu=1.0, seed=0))
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        rec = H.run_halp(obj, c)
+        e1.record()
+        torch.cuda.synchronize()
+        tim = obj.timing()
+        epoch = {"workload": "C3 HALP epoch: 4194304x4096 f32, b=16, T=N/8=524288, alpha=5e-5, mu=1 "
+                             "(full passes at the epoch start and the final boundary included)",
+                 "ms": e0.elapsed_time(e1), "inner_ms": tim["inner_ms"],
+                 "inner_steps_per_s": epoch_T / (tim["inner_ms"] / 1000.0),
+                 "loss_first_last": [rec.rows[0].loss, rec.rows[-1].loss]}
     del obj, X, y
     torch.cuda.empty_cache()
-    return ms, algo_bytes, pl
+    return ms, algo_bytes, pl, epoch
 
 
 GRID = dict(n=1000, d=64, alphas=17, mus=13, seeds=(1, 2, 3), epochs=10, T=2000)
@@ -251,6 +271,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-batch", action="store_true")
     ap.add_argument("--fg-reps", type=int, default=10)
+    ap.add_argument("--no-c3-epoch", action="store_true")
     args = ap.parse_args()
     rank, world, local = dist_env()
     if args.warmup < 3 and args.impl == "b200":
@@ -365,13 +386,16 @@ def main():
             nid = bytes(t.cpu().tolist())
         for name, cfg in (("C3", C3), ("C4", C4)):
             barrier()
-            ms, algo, pl = fullgrad_sweep(H, cfg, local, args.fg_reps, world, rank, nid)
+            ms, algo, pl, epoch = fullgrad_sweep(H, cfg, local, args.fg_reps, world, rank, nid,
+                                                 epoch_T=(cfg["n"] // 8) if name == "C3" and not args.no_c3_epoch else 0)
             ms = max_over_ranks(ms)
             tot_bytes = algo * world
             gbs = tot_bytes / (ms / 1000.0) / 1e9
             fullgrad[name] = {"shape": f"{cfg['n']}x{cfg['d']} {cfg['dtype']}", "ms_per_pass": ms,
                               "GB_per_s": gbs, "frac_of_hbm_peak": gbs / world / pk["hbm_gbs"],
                               "algorithmic_bytes_per_gpu": algo, "splits": pl["fg_splits"]}
+            if epoch is not None:
+                fullgrad[name]["halp_epoch"] = epoch
         c3 = fullgrad["C3"]
         traffic = None
         try:
