@@ -541,7 +541,9 @@ __global__ void __launch_bounds__(256, 1) k3_inner(InParams p) {
         for (int c = 0; c < 16; c += 2 * h) ev[c] = ev[c] + ev[c + h];
       const double s = ev[0];
       K3_MARK(11);
-      double pr = e / s;
+      // lanes without a class divide 1 by s: 0 / s would leave the division's
+      // fast path (the whole warp would wait on the slow one)
+      double pr = (act ? e : 1.0) / s;
       K3_MARK(12);
       if (hc == li) pr = pr - 1.0;
       p1A = __shfl_sync(0xffffffffu, pr, cA);
