@@ -88,10 +88,13 @@ typedef struct {
  * Inner loop (K3 cluster kernel):
  *   in_ctas      CTAs cooperating on one step (cluster size)
  *   in_threads   threads per CTA doing coordinate work (multiple of 32)
- *   in_per       coordinates per thread (contiguous flat index)          */
+ *   in_per       coordinates per thread (contiguous flat index)
+ *   in_levels    1: row dots combined across the cluster's warps directly;
+ *                2: per CTA first (its warps in order), then across CTAs  */
 typedef struct {
   int fg_threads, fg_vec, fg_splits;
   int in_ctas, in_threads, in_per;
+  int in_levels;
 } oq_plan;
 
 int oq_loss(const oq_objective* o, const double* w, const oq_plan* plan, double* out);

@@ -43,7 +43,8 @@ class _Objective(C.Structure):
 
 
 class _Plan(C.Structure):
-    _fields_ = [(k, C.c_int) for k in ("fg_threads", "fg_vec", "fg_splits", "in_ctas", "in_threads", "in_per")]
+    _fields_ = [(k, C.c_int) for k in ("fg_threads", "fg_vec", "fg_splits", "in_ctas", "in_threads", "in_per",
+                                       "in_levels")]
 
 
 class _Config(C.Structure):
@@ -263,6 +264,7 @@ class OraclePlan:
     in_ctas: int = 1
     in_threads: int = 32
     in_per: int = 1
+    in_levels: int = 1
 
 
 def _plan(p):
@@ -270,7 +272,7 @@ def _plan(p):
         return None
     if isinstance(p, dict):
         p = OraclePlan(**p)
-    return C.byref(_Plan(p.fg_threads, p.fg_vec, p.fg_splits, p.in_ctas, p.in_threads, p.in_per))
+    return C.byref(_Plan(p.fg_threads, p.fg_vec, p.fg_splits, p.in_ctas, p.in_threads, p.in_per, p.in_levels))
 
 
 @dataclass

@@ -60,7 +60,7 @@ class Timing(C.Structure):
 class Plan(C.Structure):
     _fields_ = [(k, C.c_int32) for k in ("fg_threads", "fg_vec", "fg_splits", "in_ctas", "in_threads", "in_per",
                                          "fg_rows_per_stage", "fg_stages")] + [
-        ("fg_split_begin", C.c_int64), ("fg_split_end", C.c_int64)
+        ("fg_split_begin", C.c_int64), ("fg_split_end", C.c_int64), ("in_levels", C.c_int32)
     ]
 
 

@@ -569,6 +569,7 @@ int halp_plan_for(int64_t n, int32_t d, int32_t C, int32_t dtype, int32_t world,
   out->in_ctas = kp.in.ctas;
   out->in_threads = kp.in.threads;
   out->in_per = kp.in.per;
+  out->in_levels = kp.in.levels > 1 ? kp.in.levels : 1;
   out->fg_rows_per_stage = kp.fg.fast ? kp.fg.rows : 2;
   out->fg_stages = kp.fg.fast ? kp.fg.stages : 4;
   out->fg_split_begin = sp.split_begin;
@@ -736,6 +737,7 @@ int halp_problem_plan(const halp_problem* p, halp_plan* out) {
   out->in_ctas = p->in.ctas;
   out->in_threads = p->in.threads;
   out->in_per = p->in.per;
+  out->in_levels = p->in.levels > 1 ? p->in.levels : 1;
   out->fg_rows_per_stage = p->fg.fast ? p->fg.rows : 2;
   out->fg_stages = p->fg.fast ? p->fg.stages : 4;
   out->fg_split_begin = p->sp.split_begin;
@@ -1069,6 +1071,7 @@ extern "C" int halp_batch_plan(const halp_batch* b, halp_plan* out) {
   out->in_threads = 32;
   const int M = (b->d + 31) / 32;
   out->in_per = M <= 1 ? 1 : M <= 2 ? 2 : M <= 4 ? 4 : 8;
+  out->in_levels = 1;
   out->fg_split_begin = 0;
   out->fg_split_end = b->splits;
   return HALP_OK;

@@ -92,7 +92,8 @@ struct InParams {
 };
 struct InLaunch {
   int dtype, ctas, threads, per, nslot_pow2;
-  int dry;  // 1: load + configure the kernel only (see FgLaunch::dry)
+  int dry;     // 1: load + configure the kernel only (see FgLaunch::dry)
+  int levels;  // 1: warp records exchanged across the cluster; 2: combined per CTA first (k_inner.cu)
 };
 cudaError_t launch_inner(const InLaunch& L, const InParams& p, cudaStream_t st);
 

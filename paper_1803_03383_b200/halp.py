@@ -272,7 +272,7 @@ class Objective:
 
     def oracle_plan(self) -> dict:
         p = self.plan()
-        return {k: p[k] for k in ("fg_threads", "fg_vec", "fg_splits", "in_ctas", "in_threads", "in_per")}
+        return {k: p[k] for k in ("fg_threads", "fg_vec", "fg_splits", "in_ctas", "in_threads", "in_per", "in_levels")}
 
     def timing(self) -> dict:
         t = A.Timing()
@@ -719,7 +719,7 @@ class BatchProblems:
 
     def oracle_plan(self) -> dict:
         p = self.plan()
-        return {k: p[k] for k in ("fg_threads", "fg_vec", "fg_splits", "in_ctas", "in_threads", "in_per")}
+        return {k: p[k] for k in ("fg_threads", "fg_vec", "fg_splits", "in_ctas", "in_threads", "in_per", "in_levels")}
 
     def run(self, cfgs) -> list:
         if len(cfgs) != self.nprob:
@@ -786,7 +786,7 @@ def plan_for(n: int, d: int, C_: int = 1, dtype: str = "f64", world: int = 1, ra
 
 def oracle_plan_for(n: int, d: int, C_: int = 1, dtype: str = "f64") -> dict:
     p = plan_for(n, d, C_, dtype)
-    return {k: p[k] for k in ("fg_threads", "fg_vec", "fg_splits", "in_ctas", "in_threads", "in_per")}
+    return {k: p[k] for k in ("fg_threads", "fg_vec", "fg_splits", "in_ctas", "in_threads", "in_per", "in_levels")}
 
 
 def rng_state_after(seed: int, stream: int, count: int) -> int:
