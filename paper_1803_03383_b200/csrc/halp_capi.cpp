@@ -695,7 +695,8 @@ int halp_problem_create(const halp_problem_desc* desc, halp_problem** out) {
     L.nsplit_local = (int)p->sp.local_splits();
     L.dry = 1;
     FgParams fp = fg_params(p, 0);
-    if (launch_fullgrad(L, fp, p->stream) != cudaSuccess) return bail(fail(HALP_CUDA_ERROR, "K1 preparation failed"));
+    const cudaError_t e1 = launch_fullgrad(L, fp, p->stream);
+    if (e1 != cudaSuccess) return bail(fail(HALP_CUDA_ERROR, std::string("K1 preparation failed: ") + cudaGetErrorString(e1)));
     InLaunch IL = p->in;
     IL.dry = 1;
     InParams ip{};
@@ -705,7 +706,8 @@ int halp_problem_create(const halp_problem_desc* desc, halp_problem** out) {
     ip.D = (int)p->D;
     for (int mode = 0; mode < 2; ++mode) {
       ip.mode = mode;
-      if (launch_inner(IL, ip, p->stream) != cudaSuccess) return bail(fail(HALP_CUDA_ERROR, "K3 preparation failed"));
+      const cudaError_t e3 = launch_inner(IL, ip, p->stream);
+      if (e3 != cudaSuccess) return bail(fail(HALP_CUDA_ERROR, std::string("K3 preparation failed: ") + cudaGetErrorString(e3)));
     }
   }
   // bf16 two-class sweeps may convert X with integer ops (k1_stream); that
