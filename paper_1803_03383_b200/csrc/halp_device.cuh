@@ -173,7 +173,10 @@ __device__ __forceinline__ double hlog(double x) {
     m = __dmul_rn(m, 0.5);
     e += 1;
   }
-  const double f = (m - 1.0) / (m + 1.0);
+  // (m - 1) / (m + 1) with a zero dividend (x a power of two) would take the
+  // IEEE division's slow path: divide a nonzero stand-in and select 0 instead
+  const double num = m - 1.0;
+  const double f = num == 0.0 ? 0.0 : (num == 0.0 ? 1.0 : num) / (m + 1.0);
   const double f2 = __dmul_rn(f, f);
   double p = 1.0 / 23.0;
   p = fma(p, f2, 1.0 / 21.0);

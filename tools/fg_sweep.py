@@ -21,6 +21,9 @@ else:
     n, d = 16777216, 1024
     X, y = H.generate("logistic", n, d, dtype="bf16", x_scale=d ** -0.5, seed=4)
     obj = H.Objective(H.Dataset(X, labels=y, num_classes=2), H.LossFamily.Softmax, 1e-5); b = n * d * 2 + n * 4
+if os.environ.get("FG_WRAND"):  # generic iterate instead of w = 0
+    import numpy as np
+    obj.full_gradient(np.random.default_rng(7).standard_normal(obj.dim()) * 0.5)
 obj.bench_full_gradient(2)
 ms = obj.bench_full_gradient(10 if w != "c1" else 200)
 p = obj.plan()
