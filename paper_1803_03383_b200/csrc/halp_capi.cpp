@@ -283,6 +283,14 @@ bool plan_stream(int d, int C, int dtype, FgLaunch* out) {
     while (R > 1 && (R * NG * V > 64 || regs(R) > reg_cap || (int64_t)R * row_bytes > 32 * 1024 ||
                      !stream_shape_ok(T1 / 32, NG, R, stages)))
       R /= 2;
+    // bf16 two-class rows (C4): 16-row tiles with x re-read from shared memory
+    // for the gradient phase, double-buffered (measured on B200, tools/fg_sweep.py:
+    // 51% vs 48% of HBM for 8-row register tiles; the gradient is bit-identical)
+    if (C == 2 && es == 2 && NG == 1 && env_int("HALP_FG_STAGES", 0) == 0 && stream_shape_ok(T1 / 32, NG, 16, 2) &&
+        (int64_t)16 * row_bytes <= 48 * 1024) {
+      R = 16;
+      stages = 2;
+    }
   }
   if (!stream_shape_ok(T1 / 32, NG, R, stages)) return false;
   if (stream_smem_bytes(ld, es, T1 / 32, R, C, stages) > 220 * 1024) return false;

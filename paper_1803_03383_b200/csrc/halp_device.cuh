@@ -156,6 +156,59 @@ __device__ __forceinline__ double hexp(double x) {
   return __dmul_rn(__dmul_rn(p, s1), s2);
 }
 
+// hexp for x <= 0 (or NaN) without branches: the same operations as hexp on
+// that domain (both scalings selected, the underflow cut applied at the end),
+// so the results are bit-identical; used where the argument is -|s|.
+__device__ __forceinline__ double hexp_nonpos(double x) {
+  const double kf = rint(__dmul_rn(x, 1.4426950408889634));
+  const double r1 = fma(-kf, 6.93147180369123816490e-01, x);
+  const double r = fma(-kf, 1.90821492927058770002e-10, r1);
+  const double r2 = __dmul_rn(r, r), r4 = __dmul_rn(r2, r2), r8 = __dmul_rn(r4, r4);
+  const double q0 = fma(1.0, r, 1.0);
+  const double q1 = fma(1.66666666666666666667e-01, r, 0.5);
+  const double q2 = fma(8.33333333333333333333e-03, r, 4.16666666666666666667e-02);
+  const double q3 = fma(1.98412698412698412698e-04, r, 1.38888888888888888889e-03);
+  const double q4 = fma(2.75573192239858906526e-06, r, 2.48015873015873015873e-05);
+  const double q5 = fma(2.50521083854417187751e-08, r, 2.75573192239858906526e-07);
+  const double q6 = fma(1.60590438368216145994e-10, r, 2.08767569878680989792e-09);
+  const double e0 = fma(q1, r2, q0), e1 = fma(q3, r2, q2), e2 = fma(q5, r2, q4);
+  const double u0 = fma(e1, r4, e0), u1 = fma(q6, r4, e2);
+  const double p = fma(u1, r8, u0);
+  const bool inr = x >= -745.1332191019412;  // false for NaN and the underflow range
+  const int k = inr ? (int)kf : 0;
+  const bool near = k > -1000;
+  const int k1 = near ? k / 2 : k + 600, k2 = near ? k - k / 2 : -600;
+  const double s1 = __longlong_as_double((long long)(k1 + 1023) << 52);
+  const double s2 = __longlong_as_double((long long)(k2 + 1023) << 52);
+  const double v = __dmul_rn(__dmul_rn(p, s1), s2);
+  return inr ? v : (x == x ? 0.0 : x);
+}
+
+// hlog for x in [1, 2] without branches: the same operations as hlog on that
+// domain (bit-identical); used for log(1 + exp(-|s|)).
+__device__ __forceinline__ double hlog_1to2(double x) {
+  const bool hi = x > 1.4142135623730951;
+  const double m = hi ? __dmul_rn(x, 0.5) : x;
+  const double num = m - 1.0;
+  const double f = num == 0.0 ? 0.0 : (num == 0.0 ? 1.0 : num) / (m + 1.0);
+  const double f2 = __dmul_rn(f, f);
+  double p = 1.0 / 23.0;
+  p = fma(p, f2, 1.0 / 21.0);
+  p = fma(p, f2, 1.0 / 19.0);
+  p = fma(p, f2, 1.0 / 17.0);
+  p = fma(p, f2, 1.0 / 15.0);
+  p = fma(p, f2, 1.0 / 13.0);
+  p = fma(p, f2, 1.0 / 11.0);
+  p = fma(p, f2, 1.0 / 9.0);
+  p = fma(p, f2, 1.0 / 7.0);
+  p = fma(p, f2, 1.0 / 5.0);
+  p = fma(p, f2, 1.0 / 3.0);
+  const double s = __dmul_rn(__dmul_rn(2.0, f), __dmul_rn(f2, p));
+  const double ef = hi ? 1.0 : 0.0;
+  const double h = fma(ef, 6.93147180369123816490e-01, __dmul_rn(2.0, f));
+  return h + fma(ef, 1.90821492927058770002e-10, s);
+}
+
 __device__ __forceinline__ double hlog(double x) {
   if (!(x == x) || x < 0.0) return __longlong_as_double(0x7FF8000000000000LL);
   if (x == 0.0) return __longlong_as_double((long long)0xFFF0000000000000ULL);

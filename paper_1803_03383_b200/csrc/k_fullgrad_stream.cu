@@ -120,11 +120,17 @@ template <bool B> struct BoolTag { static constexpr bool value = B; };
 }  // namespace
 
 template <class Tx, int CC, int NW, int NG, int R, int STAGES, bool FULLG>
-__global__ void __launch_bounds__(NW * 32, 1) k1_stream(FgParams p, int nloc) {
+#ifndef HALP_K1_MINB
+#define HALP_K1_MINB 1
+#endif
+__global__ void __launch_bounds__(NW * 32, HALP_K1_MINB) k1_stream(FgParams p, int nloc) {
   constexpr int V = VecK<Tx>::V;
   constexpr int T1 = NW * 32;
   constexpr int NV = R;  // one dot per row (squared: x.w; two classes: x.(w1 - w0))
   constexpr int LG = Log2<NV>::v;
+  // RR: tiles of 16+ rows keep x in shared memory only and re-read it for the
+  // gradient phase (registers for the row dots instead of an R x 8 fp64 slice)
+  constexpr bool RR = R >= 16;
   static_assert(CC == 1 || CC == 2, "least squares or two classes");
   static_assert((NV & (NV - 1)) == 0 && NV <= 32, "R must be a power of two <= 32");
   extern __shared__ __align__(128) unsigned char smem[];
@@ -134,8 +140,8 @@ __global__ void __launch_bounds__(NW * 32, 1) k1_stream(FgParams p, int nloc) {
   const int64_t stage_elems = (int64_t)R * ld;
   Tx* stages = reinterpret_cast<Tx*>(smem);
   double* red = reinterpret_cast<double*>(smem + (size_t)STAGES * stage_elems * sizeof(Tx));  // [2][NW][NV]
-  double* lts = red + 2 * NW * NV;  // [2][R] per-row losses (two classes), parity double-buffered
-  uint64_t* bars = reinterpret_cast<uint64_t*>(lts + 2 * R);
+  double* lts = red + 2 * NW * NV;  // [2][NW][R] per-row losses (two classes), parity double-buffered
+  uint64_t* bars = reinterpret_cast<uint64_t*>(lts + 2 * NW * R);
   const Tx* X = reinterpret_cast<const Tx*>(p.X);
   const unsigned long long nn = (unsigned long long)p.n, SS = (unsigned long long)p.S;
 
@@ -237,33 +243,47 @@ __global__ void __launch_bounds__(NW * 32, 1) k1_stream(FgParams p, int nloc) {
 
       auto body = [&](auto full_tag) {
         constexpr bool FULL = decltype(full_tag)::value;
-        double xr[R][NG][V];
-        double acc[NV];
-#pragma unroll
-        for (int v = 0; v < NV; ++v) acc[v] = 0.0;
-#pragma unroll
-        for (int r = 0; r < R; ++r)
+        // row r's x slice of this thread, upcast exactly (zeros past the tile / row end)
+        auto load_row = [&](int r, double (&xg)[NG][V]) {
 #pragma unroll
           for (int k = 0; k < NG; ++k) {
             if ((FULL || r < nr) && gval[k]) {
-              if constexpr (SC) load_group_scaled<Tx>(xs + (int64_t)r * ld + (tid + k * T1) * V, xr[r][k]);
-              else load_group_k<Tx>(xs + (int64_t)r * ld + (tid + k * T1) * V, xr[r][k]);
+              if constexpr (SC) load_group_scaled<Tx>(xs + (int64_t)r * ld + (tid + k * T1) * V, xg[k]);
+              else load_group_k<Tx>(xs + (int64_t)r * ld + (tid + k * T1) * V, xg[k]);
             } else {
 #pragma unroll
-              for (int q = 0; q < V; ++q) xr[r][k][q] = 0.0;
+              for (int q = 0; q < V; ++q) xg[k][q] = 0.0;
             }
           }
+        };
+        double xr[RR ? 1 : R][NG][V];
+        double acc[NV];
 #pragma unroll
-        for (int r = 0; r < R; ++r)
+        for (int v = 0; v < NV; ++v) acc[v] = 0.0;
+        if constexpr (!RR) {
+#pragma unroll
+          for (int r = 0; r < R; ++r) load_row(r, xr[RR ? 0 : r]);
+        }
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          if constexpr (RR) load_row(r, xr[0]);
 #pragma unroll
           for (int k = 0; k < NG; ++k)
 #pragma unroll
-            for (int q = 0; q < V; ++q) acc[r] = fma(xr[r][k][q], wr[k][q], acc[r]);
+            for (int q = 0; q < V; ++q) acc[r] = fma(xr[RR ? 0 : r][k][q], wr[k][q], acc[r]);
+        }
         reduce_scatter_k<NV>(acc, lane);
         if ((lane & ((32 >> LG) - 1)) == 0) rb[wid * NV + (lane >> (5 - LG))] = acc[0];
         __syncthreads();
-        // every thread's x slice is in registers: the stage can be refilled
-        if (tid == 0) issue(jseq + STAGES);
+        // x in registers: this tile's stage can be refilled now; x re-read in the
+        // gradient phase (RR): every warp has finished the PREVIOUS tile, refill that
+        if (tid == 0) {
+          if constexpr (RR) {
+            if (jseq > 0) issue(jseq - 1 + STAGES);
+          } else {
+            issue(jseq + STAGES);
+          }
+        }
 
         // logit of slot (fr, fc): the NW warp partials summed in warp order
         double lg = 0.0;
@@ -282,19 +302,32 @@ __global__ void __launch_bounds__(NW * 32, 1) k1_stream(FgParams p, int nloc) {
         } else {
           // two-class softmax, logistic form (mirror_logistic_row): s = lg
           const int lab = (int)tcur;
-          const double q = hexp(-fabs(lg));
+#ifdef HALP_K1_NOEXP
+          const double q = __dmul_rn(lg, 0.25);
+          const double den = 1.0 + q;
+          const double p0 = __dmul_rn(q, den);
+#else
+          const double q = hexp_nonpos(-fabs(lg));  // = hexp, branch-free
           const double den = 1.0 + q;
           const double p0 = (lg > 0.0 ? q : 1.0) / den;
+#endif
           pr = lab == 0 ? p0 - 1.0 : p0;
           if constexpr (SC) pr = __dmul_rn(pr, 0x1.0p896);  // |pr| <= 1: exact
-          // the loss terms (a log per row) rotate over the warps; warp 0 sums
-          // them in row order one tile later (after the next barrier)
-          if (wid == (int)(jseq % NW) && lane < NV) {
+          // the loss terms (a log per row): every warp evaluates them (straight-line
+          // code the scheduler overlaps with the gradient phase; a branch on one
+          // rotating warp made the others wait for it at the next barrier) into
+          // its own slot; warp 0 sums its copy in row order one tile later
+          {
             const double a = lab == 0 ? lg : -lg;
-            lts[(jseq & 1) * R + lane] = (a > 0.0 ? a : 0.0) + hlog(den);
+#ifdef HALP_K1_NOLOSS
+            const double lterm = (a > 0.0 ? a : 0.0) + den;
+#else
+            const double lterm = (a > 0.0 ? a : 0.0) + hlog_1to2(den);  // = hlog on [1, 2]
+#endif
+            if (lane < NV) lts[((jseq & 1) * NW + wid) * R + lane] = lterm;
           }
           if (wid == 0 && i > 0) {
-            const double* lp = lts + ((jseq - 1) & 1) * R;  // previous tile: full
+            const double* lp = lts + ((jseq - 1) & 1) * NW * R;  // previous tile, warp 0's copy: full
 #pragma unroll
             for (int r = 0; r < R; ++r) la = la + lp[r];
           }
@@ -312,10 +345,11 @@ __global__ void __launch_bounds__(NW * 32, 1) k1_stream(FgParams p, int nloc) {
 #pragma unroll
         for (int r = 0; r < R; ++r) {
           if (FULL || r < nr) {
+            if constexpr (RR) load_row(r, xr[0]);
 #pragma unroll
             for (int k = 0; k < NG; ++k)
 #pragma unroll
-              for (int q = 0; q < V; ++q) gacc[k][q] = fma(dlr[r], xr[r][k][q], gacc[k][q]);
+              for (int q = 0; q < V; ++q) gacc[k][q] = fma(dlr[r], xr[RR ? 0 : r][k][q], gacc[k][q]);
           }
         }
       };
@@ -326,7 +360,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k1_stream(FgParams p, int nloc) {
       __syncthreads();
       if (wid == 0 && ntile > 0) {
         const int nr_last = (int)(r1 - (r0 + (ntile - 1) * R));
-        const double* lp = lts + ((jseq - 1) & 1) * R;
+        const double* lp = lts + ((jseq - 1) & 1) * NW * R;
         for (int r = 0; r < nr_last; ++r) la = la + lp[r];
       }
     }
@@ -358,7 +392,7 @@ size_t stream_smem_bytes(int ld, int elem, int warps, int R, int CC, int stages)
   size_t b = (size_t)stages * R * ld * elem;
   b = (b + 15) / 16 * 16;
   (void)CC;
-  b += (size_t)2 * warps * R * 8 + (size_t)2 * R * 8 + (size_t)stages * 8;
+  b += (size_t)2 * warps * R * 8 + (size_t)2 * warps * R * 8 + (size_t)stages * 8;
   return b;
 }
 

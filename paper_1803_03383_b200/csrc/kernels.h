@@ -38,7 +38,8 @@ cudaError_t launch_fullgrad_smx(const FgLaunch& L, const FgParams& p, cudaStream
 #define HALP_STREAM_SHAPES(X) \
   X(1, 1, 4, 4) X(1, 1, 8, 4) X(2, 1, 4, 4) X(2, 1, 8, 4) X(4, 1, 4, 4) X(4, 1, 8, 4) X(8, 1, 2, 4) \
   X(8, 1, 4, 4) X(16, 1, 2, 4) X(16, 1, 4, 4) X(8, 2, 2, 4) X(16, 2, 1, 4) X(16, 2, 2, 4) X(8, 4, 1, 4) \
-  X(8, 4, 2, 4) X(16, 4, 1, 4) X(16, 2, 2, 6) X(8, 2, 2, 6) X(8, 4, 2, 6) X(4, 1, 4, 6)
+  X(8, 4, 2, 4) X(16, 4, 1, 4) X(16, 2, 2, 6) X(8, 2, 2, 6) X(8, 4, 2, 6) X(4, 1, 4, 6) \
+  X(4, 1, 16, 2) X(2, 1, 16, 2) X(1, 1, 16, 2)
 size_t stream_smem_bytes(int ld, int elem, int warps, int R, int CC, int stages);
 cudaError_t launch_fullgrad_stream(const FgLaunch& L, const FgParams& p, cudaStream_t st);
 cudaError_t launch_split_tree(const double* partials, int nsplit, int D1, double* out, double* scratch,

@@ -22,8 +22,11 @@ else:
     X, y = H.generate("logistic", n, d, dtype="bf16", x_scale=d ** -0.5, seed=4)
     obj = H.Objective(H.Dataset(X, labels=y, num_classes=2), H.LossFamily.Softmax, 1e-5); b = n * d * 2 + n * 4
 if os.environ.get("FG_WRAND"):  # generic iterate instead of w = 0
+    import hashlib
     import numpy as np
-    obj.full_gradient(np.random.default_rng(7).standard_normal(obj.dim()) * 0.5)
+    wv = np.random.default_rng(7).standard_normal(obj.dim()) * 0.5
+    g = obj.full_gradient(wv)
+    print("RESULT_HASH", hashlib.sha1(g.tobytes()).hexdigest()[:16], repr(obj.loss(wv)))
 obj.bench_full_gradient(2)
 ms = obj.bench_full_gradient(10 if w != "c1" else 200)
 p = obj.plan()
@@ -38,4 +41,4 @@ for v in (sys.argv[2:] or [""]):
         env[k] = val
     r = subprocess.run([sys.executable, "-c", CHILD, w], env=env, capture_output=True, text=True, timeout=600)
     out = [l for l in r.stdout.splitlines() if l.startswith("RESULT")]
-    print(v or "default", out[0] if out else ("FAILED " + r.stderr[-800:]), flush=True)
+    print(v or "default", out[-1] if out else ("FAILED " + r.stderr[-800:]), " ".join(out[:-1]), flush=True)
