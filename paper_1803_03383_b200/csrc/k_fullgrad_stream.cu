@@ -80,8 +80,10 @@ __device__ __forceinline__ void load_group_scaled(const Tx* p, double* out) {
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
     const uint32_t w = wds[q];
-    const uint32_t hlo = ((w << 16) & 0x80000000u) | ((w << 13) & 0x0FFFE000u);
-    const uint32_t hhi = (w & 0x80000000u) | ((w >> 3) & 0x0FFFE000u);
+    // arithmetic >> 3 puts the exponent field at bits 27..20 and copies the sign
+    // into bits 31..28; the mask keeps bit 31 and the 15 exponent/mantissa bits
+    const uint32_t hlo = (uint32_t)((int32_t)(w << 16) >> 3) & 0x8FFFE000u;
+    const uint32_t hhi = (uint32_t)((int32_t)w >> 3) & 0x8FFFE000u;
     out[2 * q] = __hiloint2double((int)hlo, 0);
     out[2 * q + 1] = __hiloint2double((int)hhi, 0);
   }
