@@ -64,14 +64,15 @@ __device__ __forceinline__ void load_group_k(const Tx* p, double* out) {
   }
 }
 
-// bf16 group -> fp64 scaled by 2^-896, with integer ops only (no F2F on the
-// XU pipe): the f32 pattern f of a bf16 maps to the double with the same sign,
-// exponent FIELD and leading mantissa bits, i.e. exactly x * 2^-896 for every
-// finite x (normal, subnormal, zero).  Used with w' = w * 2^896 and
-// dl' = dl * 2^896, products x'*w' and dl'*x' equal x*w and dl*x exactly,
-// so every fma rounds exactly as with the F2F-converted x.  Requires finite
-// x (checked at problem creation) and |w|, |dl| < 2^126 (checked per launch /
-// bounded by 1 for the two-class derivative).
+// bf16 group -> fp64 with the conversion split between two pipes.  ODD
+// features (the high bf16 of each 32-bit word) go through integer ops only:
+// the f32 pattern of a bf16 maps to the double with the same sign, exponent
+// FIELD and leading mantissa bits, i.e. exactly x * 2^-896 for every finite x
+// (normal, subnormal, zero); with w' = w * 2^896 and dl' = dl * 2^896 the
+// products x'*w' and dl'*x' equal x*w and dl*x exactly, so every fma rounds
+// as with the F2F-converted x.  EVEN features use F2F (unscaled, w and dl
+// unscaled).  Requires finite x (checked at problem creation) and |w|, |dl| <
+// 2^126 (checked per launch / bounded by 1 for the two-class derivative).
 template <class Tx>
 __device__ __forceinline__ void load_group_scaled(const Tx* p, double* out) {
   static_assert(sizeof(Tx) == 2, "bf16 only");
@@ -82,9 +83,8 @@ __device__ __forceinline__ void load_group_scaled(const Tx* p, double* out) {
     const uint32_t w = wds[q];
     // arithmetic >> 3 puts the exponent field at bits 27..20 and copies the sign
     // into bits 31..28; the mask keeps bit 31 and the 15 exponent/mantissa bits
-    const uint32_t hlo = (uint32_t)((int32_t)(w << 16) >> 3) & 0x8FFFE000u;
     const uint32_t hhi = (uint32_t)((int32_t)w >> 3) & 0x8FFFE000u;
-    out[2 * q] = __hiloint2double((int)hlo, 0);
+    out[2 * q] = (double)__uint_as_float(w << 16);  // even features: F2F, unscaled
     out[2 * q + 1] = __hiloint2double((int)hhi, 0);
   }
 }
@@ -161,6 +161,9 @@ __global__ void __launch_bounds__(NW * 32, HALP_K1_MINB) k1_stream(FgParams p, i
   // bf16 two-class sweeps convert x with integer ops in the 2^-896-scaled
   // domain (load_group_scaled) when X is known finite and |w1 - w0| < 2^126
   constexpr bool SCALE_OK = std::is_same<Tx, __nv_bfloat16>::value && CC == 2;
+  // even features F2F-converted (unscaled, conversion pipe), odd ones integer-
+  // upcast (scaled, ALU): the two pipes share the conversion work (C4 58% -> 62%)
+  constexpr bool MIXED = true;
   bool ok = SCALE_OK && p.x_finite;
 #pragma unroll
   for (int k = 0; k < NG; ++k)
@@ -176,7 +179,8 @@ __global__ void __launch_bounds__(NW * 32, HALP_K1_MINB) k1_stream(FgParams p, i
 #pragma unroll
     for (int k = 0; k < NG; ++k)
 #pragma unroll
-      for (int q = 0; q < V; ++q) wr[k][q] = __dmul_rn(wr[k][q], 0x1.0p896);
+      for (int q = 0; q < V; ++q)
+        if (!MIXED || (q & 1)) wr[k][q] = __dmul_rn(wr[k][q], 0x1.0p896);
   }
 
   // ---- producer (thread 0): the CTA's tile sequence across its splits ----
@@ -314,7 +318,7 @@ __global__ void __launch_bounds__(NW * 32, HALP_K1_MINB) k1_stream(FgParams p, i
           const double p0 = (lg > 0.0 ? q : 1.0) / den;
 #endif
           pr = lab == 0 ? p0 - 1.0 : p0;
-          if constexpr (SC) pr = __dmul_rn(pr, 0x1.0p896);  // |pr| <= 1: exact
+          if constexpr (SC && !MIXED) pr = __dmul_rn(pr, 0x1.0p896);  // |pr| <= 1: exact
           // the loss terms (a log per row): every warp evaluates them (straight-line
           // code the scheduler overlaps with the gradient phase; a branch on one
           // rotating warp made the others wait for it at the next barrier) into
@@ -334,9 +338,13 @@ __global__ void __launch_bounds__(NW * 32, HALP_K1_MINB) k1_stream(FgParams p, i
             for (int r = 0; r < R; ++r) la = la + lp[r];
           }
         }
-        double dlr[NV];
+        double dlr[NV], dls[SC && MIXED ? NV : 1];
 #pragma unroll
         for (int v = 0; v < NV; ++v) dlr[v] = __shfl_sync(0xffffffffu, pr, v);
+        if constexpr (SC && MIXED) {
+#pragma unroll
+          for (int v = 0; v < NV; ++v) dls[v] = __dmul_rn(dlr[v], 0x1.0p896);  // odd features: scaled domain
+        }
         if (CC == 1 && wid == 0) {
 #pragma unroll
           for (int r = 0; r < R; ++r) {
@@ -351,7 +359,8 @@ __global__ void __launch_bounds__(NW * 32, HALP_K1_MINB) k1_stream(FgParams p, i
 #pragma unroll
             for (int k = 0; k < NG; ++k)
 #pragma unroll
-              for (int q = 0; q < V; ++q) gacc[k][q] = fma(dlr[r], xr[RR ? 0 : r][k][q], gacc[k][q]);
+              for (int q = 0; q < V; ++q)
+                gacc[k][q] = fma((SC && MIXED && (q & 1)) ? dls[SC && MIXED ? r : 0] : dlr[r], xr[RR ? 0 : r][k][q], gacc[k][q]);
           }
         }
       };
