@@ -73,6 +73,23 @@ __device__ __forceinline__ void load_group_k(const Tx* p, double* out) {
 // as with the F2F-converted x.  EVEN features use F2F (unscaled, w and dl
 // unscaled).  Requires finite x (checked at problem creation) and |w|, |dl| <
 // 2^126 (checked per launch / bounded by 1 for the two-class derivative).
+#ifndef HALP_K1_OF
+#define HALP_K1_OF 0  // odd features of the first OF words of a group also via F2F
+#endif
+__device__ __forceinline__ bool k1_scaled_feature(int j) { return (j & 1) && (j >> 1) >= HALP_K1_OF; }
+
+// exact bf16 -> fp64 of the low / high half of a 32-bit word (F2F.F64.BF16 reads the half directly)
+__device__ __forceinline__ double bf16_lo_to_f64(uint32_t w) {
+  double r;
+  asm("{\n\t.reg .b16 l, h;\n\tmov.b32 {l, h}, %1;\n\tcvt.f64.bf16 %0, l;\n\t}" : "=d"(r) : "r"(w));
+  return r;
+}
+__device__ __forceinline__ double bf16_hi_to_f64(uint32_t w) {
+  double r;
+  asm("{\n\t.reg .b16 l, h;\n\tmov.b32 {l, h}, %1;\n\tcvt.f64.bf16 %0, h;\n\t}" : "=d"(r) : "r"(w));
+  return r;
+}
+
 template <class Tx>
 __device__ __forceinline__ void load_group_scaled(const Tx* p, double* out) {
   static_assert(sizeof(Tx) == 2, "bf16 only");
@@ -83,9 +100,13 @@ __device__ __forceinline__ void load_group_scaled(const Tx* p, double* out) {
     const uint32_t w = wds[q];
     // arithmetic >> 3 puts the exponent field at bits 27..20 and copies the sign
     // into bits 31..28; the mask keeps bit 31 and the 15 exponent/mantissa bits
-    const uint32_t hhi = (uint32_t)((int32_t)w >> 3) & 0x8FFFE000u;
-    out[2 * q] = (double)__uint_as_float(w << 16);  // even features: F2F, unscaled
-    out[2 * q + 1] = __hiloint2double((int)hhi, 0);
+    out[2 * q] = bf16_lo_to_f64(w);  // even features: one F2F.F64.BF16, unscaled
+    if (q < HALP_K1_OF) {
+      out[2 * q + 1] = bf16_hi_to_f64(w);
+    } else {
+      const uint32_t hhi = (uint32_t)((int32_t)w >> 3) & 0x8FFFE000u;
+      out[2 * q + 1] = __hiloint2double((int)hhi, 0);
+    }
   }
 }
 
@@ -180,7 +201,7 @@ __global__ void __launch_bounds__(NW * 32, HALP_K1_MINB) k1_stream(FgParams p, i
     for (int k = 0; k < NG; ++k)
 #pragma unroll
       for (int q = 0; q < V; ++q)
-        if (!MIXED || (q & 1)) wr[k][q] = __dmul_rn(wr[k][q], 0x1.0p896);
+        if (!MIXED || k1_scaled_feature(q)) wr[k][q] = __dmul_rn(wr[k][q], 0x1.0p896);
   }
 
   // ---- producer (thread 0): the CTA's tile sequence across its splits ----
@@ -360,7 +381,8 @@ __global__ void __launch_bounds__(NW * 32, HALP_K1_MINB) k1_stream(FgParams p, i
             for (int k = 0; k < NG; ++k)
 #pragma unroll
               for (int q = 0; q < V; ++q)
-                gacc[k][q] = fma((SC && MIXED && (q & 1)) ? dls[SC && MIXED ? r : 0] : dlr[r], xr[RR ? 0 : r][k][q], gacc[k][q]);
+                gacc[k][q] = fma((SC && MIXED && k1_scaled_feature(q)) ? dls[SC && MIXED ? r : 0] : dlr[r],
+                                 xr[RR ? 0 : r][k][q], gacc[k][q]);
           }
         }
       };
