@@ -76,7 +76,12 @@ __device__ __forceinline__ void load_group_k(const Tx* p, double* out) {
 #ifndef HALP_K1_OF
 #define HALP_K1_OF 0  // odd features of the first OF words of a group also via F2F
 #endif
-__device__ __forceinline__ bool k1_scaled_feature(int j) { return (j & 1) && (j >> 1) >= HALP_K1_OF; }
+#ifndef HALP_K1_EF
+#define HALP_K1_EF 4  // even features of the first EF words of a group via F2F (the rest integer-upcast)
+#endif
+__device__ __forceinline__ bool k1_scaled_feature(int j) {
+  return (j & 1) ? (j >> 1) >= HALP_K1_OF : (j >> 1) >= HALP_K1_EF;
+}
 
 // exact bf16 -> fp64 of the low / high half of a 32-bit word (F2F.F64.BF16 reads the half directly)
 __device__ __forceinline__ double bf16_lo_to_f64(uint32_t w) {
@@ -100,7 +105,12 @@ __device__ __forceinline__ void load_group_scaled(const Tx* p, double* out) {
     const uint32_t w = wds[q];
     // arithmetic >> 3 puts the exponent field at bits 27..20 and copies the sign
     // into bits 31..28; the mask keeps bit 31 and the 15 exponent/mantissa bits
-    out[2 * q] = bf16_lo_to_f64(w);  // even features: one F2F.F64.BF16, unscaled
+    if (q < HALP_K1_EF) {
+      out[2 * q] = bf16_lo_to_f64(w);  // even features: one F2F.F64.BF16, unscaled
+    } else {
+      const uint32_t hlo = (uint32_t)((int32_t)(w << 16) >> 3) & 0x8FFFE000u;
+      out[2 * q] = __hiloint2double((int)hlo, 0);
+    }
     if (q < HALP_K1_OF) {
       out[2 * q + 1] = bf16_hi_to_f64(w);
     } else {
@@ -158,7 +168,9 @@ __global__ void __launch_bounds__(NW * 32, HALP_K1_MINB) k1_stream(FgParams p, i
   static_assert((NV & (NV - 1)) == 0 && NV <= 32, "R must be a power of two <= 32");
   extern __shared__ __align__(128) unsigned char smem[];
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const int d = p.d, D = d * CC, ld = p.ld;
+  // FULLG: every group of the padded row is owned, so the row pitch is a
+  // compile-time constant (ld = ngroups * V) and tile offsets fold into immediates
+  const int d = p.d, D = d * CC, ld = FULLG ? NG * T1 * V : p.ld;
   const int ngroups = (d + V - 1) / V;
   const int64_t stage_elems = (int64_t)R * ld;
   Tx* stages = reinterpret_cast<Tx*>(smem);
