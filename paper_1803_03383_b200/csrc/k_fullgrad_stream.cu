@@ -152,11 +152,17 @@ template <bool B> struct BoolTag { static constexpr bool value = B; };
 
 }  // namespace
 
+// Minimum resident CTAs per SM the register allocator must allow.  The bf16 two-class
+// 16-row shape (C4: 4 warps) fits 168 registers with no spills, so 3 CTAs per SM
+// (12 warps) instead of 2 at 243 registers: 63% -> 69% of HBM on B200, bit-identical
+// (tools/gpu_minb3.sh).  Forcing 3 on the 256-thread fp32 shapes spills (C3 86% -> 32%).
+template <class Tx, int CC, int NW, int R>
+struct K1MinBlocks {
+  static constexpr int value = (sizeof(Tx) == 2 && CC == 2 && NW == 4 && R == 16) ? 3 : 1;
+};
+
 template <class Tx, int CC, int NW, int NG, int R, int STAGES, bool FULLG>
-#ifndef HALP_K1_MINB
-#define HALP_K1_MINB 1
-#endif
-__global__ void __launch_bounds__(NW * 32, HALP_K1_MINB) k1_stream(FgParams p, int nloc) {
+__global__ void __launch_bounds__(NW * 32, (K1MinBlocks<Tx, CC, NW, R>::value)) k1_stream(FgParams p, int nloc) {
   constexpr int V = VecK<Tx>::V;
   constexpr int T1 = NW * 32;
   constexpr int NV = R;  // one dot per row (squared: x.w; two classes: x.(w1 - w0))
