@@ -156,9 +156,12 @@ template <bool B> struct BoolTag { static constexpr bool value = B; };
 // 16-row shape (C4: 4 warps) fits 168 registers with no spills, so 3 CTAs per SM
 // (12 warps) instead of 2 at 243 registers: 63% -> 69% of HBM on B200, bit-identical
 // (tools/gpu_minb3.sh).  Forcing 3 on the 256-thread fp32 shapes spills (C3 86% -> 32%).
+#ifndef HALP_K1_MINB_BF16_2C
+#define HALP_K1_MINB_BF16_2C 3
+#endif
 template <class Tx, int CC, int NW, int R>
 struct K1MinBlocks {
-  static constexpr int value = (sizeof(Tx) == 2 && CC == 2 && NW == 4 && R == 16) ? 3 : 1;
+  static constexpr int value = (sizeof(Tx) == 2 && CC == 2 && NW == 4 && R == 16) ? HALP_K1_MINB_BF16_2C : 1;
 };
 
 template <class Tx, int CC, int NW, int NG, int R, int STAGES, bool FULLG>
