@@ -2,28 +2,36 @@
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
 
-Workload (BASELINE.json configs[1], "C2"): multiclass softmax logistic
-regression, N=60000, d=784, C=10, fp32 features uniform in [0,1) with 80% of
-entries zero, labels = argmax of a Gaussian teacher W plus Gumbel noise, L2
-1e-4, HALP b=8, alpha=0.01, T=N, mu=2.5 (unspecified in BASELINE; the
-paper's MNIST value).  Synthetic data (seeded, generated on the device by
-K6) stands in for MNIST, which is not in the container.
+Headline workload = BASELINE.json configs[2] ("C3"), the largest config
+that fits one GPU: least-squares regression, N = 4,194,304, d = 4096, fp32
+Gaussian x and w*, noise sd 0.1, HALP b = 16, T = N/8 = 524,288; alpha and
+mu are unspecified in BASELINE and recorded in `config` (alpha = 5e-5 ~
+0.2/|x|^2, mu = 1).  X is 68.7 GB (> the 126 MB L2).  The
+data is synthetic: the counter-based generator K6 (device) / oracle/datagen.c
+(host, byte-identical, tests/test_gpu_datagen.py).
 
-One step = one HALP epoch (K1 full-gradient + loss pass, centering, K4 sample
-indices, K3 T=60000-step inner loop, plus the reference's boundary
-measurement).  value = epochs/s over all GPUs: at N>1 every rank runs its own
-replica problem (the HALP epoch is sequential), so
-scaling is weak.  Extra keys: `fullgrad` (the K1 sweep on C3 = 4,194,304 x
-4096 fp32, 64 GiB, and C4 = 16,777,216 x 1024 bf16 as softmax C=2), whose K1
-numbers also fill `roofline`; `inner_loop` (K3 steps/s); `e2e` (the same
-epoch through the public API from pinned host buffers); `cpu_baseline` (the
-oracle restatement of the reference on the host cores, bounded sample).
+One step = one HALP epoch of lpopt::run_halp (optimizers.cpp:387-459): the
+full-gradient + loss pass at w~ (K1), centering (K2), sample indices (K4)
+and the T-step b-bit inner loop (K3).  `value` = epochs/s of the whole job.
+At N > 1 the same single problem runs on N GPUs: the full-gradient pass is
+row-sharded (one NCCL all-gather per epoch), the sequential inner loop is
+replicated -- total work fixed, so scaling is "strong".
 
---impl reference times the reference algorithm on the CPU: the reference
+Extra keys: `e2e` (the same epoch through the public API from pinned host
+buffers, X uploaded every step), `roofline` (K1 at C3 against measured
+HBM bandwidth, from the K1 time inside the timed region), `inner_loop` (K3,
+the latency-bound stage that dominates the epoch), `fullgrad` (K1 at C3 and
+C4), `c2` (the MNIST-shaped softmax epoch), `batch` (C5 via K5), `grid`,
+`cpu_baseline` (the oracle's reference-order restatement on the host cores,
+bounded sample, extrapolation stated).
+
+--impl reference times the reference algorithm on the CPU.  The reference
 (proj/, C++ + Eigen) cannot be built in this image (Eigen3 and vendor/ are
 absent), so its restatement oracle/liboracle.so in REF order
-(pinned to the reference's golden traces) runs one C2 epoch per step with
-the reference's blocked full gradient spread over all host threads.
+(pinned to the reference's golden traces) runs the same C3 workload on a
+bounded row / step sample per step, full gradient on all host threads (the
+reference's blocked scheme, objectives.cpp:289-301), sequential inner loop;
+its data comes from oracle/datagen.c.  That arm never loads libhalp_b200.so.
 """
 from __future__ import annotations
 
@@ -41,10 +49,27 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+C3 = dict(n=4194304, d=4096, dtype="f32", noise_sd=0.1, seed=3, bits=16, T=4194304 // 8, alpha=5e-5, mu=1.0, l2=0.0)
 C2 = dict(n=60000, d=784, C=10, density=0.2, l2=1e-4, bits=8, alpha=0.01, mu=2.5)
-C3 = dict(n=4194304, d=4096, dtype="f32")
-C5 = dict(nprob=512, n=4096, d=128, epochs=10, mu=3.0)  # per GPU; T = 2N (reference default)
 C4 = dict(n=16777216, d=1024, dtype="bf16")
+C5 = dict(nprob=512, n=4096, d=128, epochs=10, mu=3.0)  # per GPU; T = 2N (reference default)
+# CPU sample of the C3 epoch: rows / steps divisors (the epoch cost is linear in both)
+CPU_ROWS_DIV, CPU_STEPS_DIV = 64, 64
+
+METRIC, UNIT = "HALP epochs/sec", "epochs/s"
+
+
+def headline_config(world: int) -> dict:
+    """identical in both arms (the driver compares them)"""
+    return {
+        "workload": "C3: least squares N=4194304 d=4096 fp32 Gaussian x and w*, noise 0.1; HALP b=16, "
+                    "T=N/8=524288, alpha=5e-5, mu=1 (alpha, mu unspecified in BASELINE), option I, seed 0",
+        "N": C3["n"], "d": C3["d"], "bits": C3["bits"], "T": C3["T"], "alpha": C3["alpha"], "mu": C3["mu"],
+        "l2": C3["l2"], "x_dtype": "f32", "data_seed": C3["seed"],
+        "l2_cache": "inputs (68.7 GB) larger than L2 (126 MB)",
+        "parallelism": "single GPU" if world == 1 else
+        f"full-gradient rows sharded x{world} + one NCCL all-gather per epoch; inner loop replicated",
+    }
 
 
 def peaks():
@@ -95,110 +120,122 @@ def dist_env():
     return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
 
 
-def c2_data(H, seed, device):
-    X, lab = H.generate("softmax", C2["n"], C2["d"], num_classes=C2["C"], dtype="f32", density=C2["density"],
-                        seed=seed, device=device)
-    return X, lab
-
-
-def c2_config(H, epochs, seed):
-    return H.OptimizerConfig(algorithm=H.Algorithm.Halp, alpha=C2["alpha"], epochs=epochs, inner_steps=C2["n"],
-                             bits=C2["bits"], mu=C2["mu"], seed=seed)
-
-
-def cpu_c2_epoch(O, Xh, labh, threads, inner_steps, seed=0):
-    obj = O.OracleObjective(Xh, labels=labh, num_classes=C2["C"], l2=C2["l2"])
-    cfg = O.OracleConfig(alpha=C2["alpha"], epochs=1, inner_steps=inner_steps, bits=C2["bits"], mu=C2["mu"], seed=seed)
+# ----------------------------------------------------------------------------- CPU (oracle) legs
+def cpu_c3_sample(O, threads: int, rows_div: int = CPU_ROWS_DIV, steps_div: int = CPU_STEPS_DIV, data=None):
+    """One bounded sample of the C3 epoch on the host: the REF-order oracle's
+    run_halp (1 epoch) on the first N/rows_div rows of the C3 dataset with
+    T/steps_div inner steps; full gradient on `threads` threads.  The epoch
+    is one full-gradient + loss pass over N rows plus T sequential inner
+    steps, both linear in their count, so
+        epoch_s = (fullgrad_s / 2 passes) * rows_div + inner_s * steps_div
+    (a 1-epoch run makes 2 passes: the epoch start and the final boundary).
+    Returns (epoch_s, measured_s, data)."""
+    ns = C3["n"] // rows_div
+    if data is None:
+        X, y = O.generate("regression", C3["n"], C3["d"], dtype="f32", noise_sd=C3["noise_sd"], seed=C3["seed"],
+                          rows=(0, ns), threads=threads)
+        data = O.OracleObjective(X, y=y, l2=C3["l2"])
+    cfg = O.OracleConfig(alpha=C3["alpha"], epochs=1, inner_steps=C3["T"] // steps_div, bits=C3["bits"], mu=C3["mu"],
+                         seed=0)
     t = time.perf_counter()
-    rec = O.run_halp(obj, cfg, fullgrad_threads=threads)
-    return time.perf_counter() - t, rec
+    rec = O.run_halp(data, cfg, fullgrad_threads=threads)
+    measured = time.perf_counter() - t
+    epoch_s = rec.fullgrad_seconds / 2.0 * rows_div + rec.inner_seconds * steps_div
+    return epoch_s, measured, data
+
+
+def cpu_sample_text(threads):
+    return (f"REF-order oracle run_halp, 1 epoch on rows [0, N/{CPU_ROWS_DIV}) of the C3 dataset with "
+            f"T/{CPU_STEPS_DIV} = {C3['T'] // CPU_STEPS_DIV} inner steps, full gradient on {threads} threads "
+            f"(objectives.cpp:289-301 blocks), inner loop sequential; epoch = (fullgrad_s/2)*{CPU_ROWS_DIV} + "
+            f"inner_s*{CPU_STEPS_DIV}")
 
 
 def run_reference(args, rank, world):
-    """--impl reference: rank 0 only, the oracle restatement on all host threads."""
+    """--impl reference: rank 0 only; the oracle restatement on all host threads.
+    Imports nothing from the product package (no libhalp_b200.so)."""
     if rank != 0:
         return
-    import torch
-
-    import paper_1803_03383_b200 as H
     from oracle import oracle as O
 
     O.build()
     threads = os.cpu_count() or 1
-    # same bytes as the GPU arm's workload (generated by K6, copied to the host)
-    X, lab = c2_data(H, 0, 0)
-    Xh, labh = X.cpu().numpy(), lab.cpu().numpy()
-    del X, lab
-    torch.cuda.empty_cache()
+    data = None
     for _ in range(args.warmup):
-        cpu_c2_epoch(O, Xh, labh, threads, C2["n"] // 10)
-    times = []
+        _, _, data = cpu_c3_sample(O, threads, data=data)
+    eps, meas = [], []
     for _ in range(args.steps):
-        dt, rec = cpu_c2_epoch(O, Xh, labh, threads, C2["n"])
-        times.append(dt)
-    ms = 1000.0 * sum(times) / len(times)
+        e, m, data = cpu_c3_sample(O, threads, data=data)
+        eps.append(e)
+        meas.append(m)
+    ms = 1000.0 * sum(eps) / len(eps)
     v = 1000.0 / ms
     line = {
-        "impl": "reference", "metric": "HALP epochs/sec", "value": v, "unit": "epochs/s", "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (K6, seeded), MNIST-shaped",
-        "config": {"workload": "C2 softmax N=60000 d=784 C=10 b=8 alpha=0.01 T=60000 mu=2.5", "l2": C2["l2"]},
-        "cpu_baseline": {"value": v, "unit": "epochs/s", "cores": threads, "kind": "port",
-                         "sample": "1 full C2 epoch per step (full gradient on all host threads, sequential inner loop)"},
-        "e2e": {"value": v, "unit": "epochs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (oracle/datagen.c = K6 bytes, seeded)", "config": headline_config(world),
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "port", "sample": cpu_sample_text(threads),
+                         "measured_seconds_per_step": sum(meas) / len(meas)},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "note": "reference proj/ cannot be built here (Eigen3, vendor/ absent); oracle/liboracle.so REF order "
                 "restates it and reproduces its golden traces",
     }
     print(json.dumps(line), flush=True)
 
 
-def fullgrad_sweep(H, cfg, device, reps, world, rank, nccl_id, epoch_T=0):
-    """K1 at a BASELINE full-gradient shape: average device ms per pass."""
-    import torch
+# ----------------------------------------------------------------------------- GPU legs
+def c3_objective(H, device, world, rank, nccl_id):
+    X, y = H.generate("regression", C3["n"], C3["d"], dtype="f32", noise_sd=C3["noise_sd"], x_scale=1.0,
+                      seed=C3["seed"], device=device)
+    obj = H.Objective(H.Dataset(X, targets=y), H.LossFamily.Squared, C3["l2"], device=device, world_size=world,
+                      rank=rank, nccl_id=nccl_id)
+    return obj, X, y
 
-    n, d = cfg["n"], cfg["d"]
-    if cfg["dtype"] == "f32":
-        X, y = H.generate("regression", n, d, dtype="f32", noise_sd=0.1, x_scale=1.0, seed=3, device=device)
-        obj = H.Objective(H.Dataset(X, targets=y), H.LossFamily.Squared, 0.0, device=device, world_size=world,
-                          rank=rank, nccl_id=nccl_id)
-        ybytes = 8
-    else:
-        X, y = H.generate("logistic", n, d, dtype="bf16", x_scale=d ** -0.5, seed=4, device=device)
-        obj = H.Objective(H.Dataset(X, labels=y, num_classes=2), H.LossFamily.Softmax, 1e-5, device=device,
-                          world_size=world, rank=rank, nccl_id=nccl_id)
-        ybytes = 4
-    pl = obj.plan()
-    rows = int(n * (pl["fg_split_end"] - pl["fg_split_begin"]) // pl["fg_splits"])
-    # a generic iterate (w = 0 is a degenerate point: every logit 0), left resident for the timed passes
-    wgen = np.random.default_rng(7).standard_normal(obj.dim()) * (0.5 if cfg["dtype"] == "f32" else 1.0)
+
+def c3_config(H, epochs):
+    return H.OptimizerConfig(algorithm=H.Algorithm.Halp, alpha=C3["alpha"], epochs=epochs, inner_steps=C3["T"],
+                             bits=C3["bits"], mu=C3["mu"], seed=0)
+
+
+def fullgrad_c4(H, device, reps, world, rank, nccl_id):
+    """K1 at C4: binary logistic as softmax C=2, bf16 x ~ N(0, 1/d), l2 1e-5"""
+    n, d = C4["n"], C4["d"]
+    X, y = H.generate("logistic", n, d, dtype="bf16", x_scale=d ** -0.5, seed=4, device=device)
+    obj = H.Objective(H.Dataset(X, labels=y, num_classes=2), H.LossFamily.Softmax, 1e-5, device=device,
+                      world_size=world, rank=rank, nccl_id=nccl_id)
+    wgen = np.random.default_rng(7).standard_normal(obj.dim())
     obj.full_gradient(wgen)
     obj.bench_full_gradient(2)
     ms = obj.bench_full_gradient(reps)
-    es = 4 if cfg["dtype"] == "f32" else 2
-    algo_bytes = rows * d * es + rows * ybytes
-    epoch = None
-    if cfg["dtype"] == "f32" and epoch_T:
-        # one full HALP epoch at C3: b = 16, T = N/8 (BASELINE); alpha, mu unspecified
-        # there -> 5e-5 (~0.2/|x|^2) and 1 (SURVEY.md 8d)
-        c = H.OptimizerConfig(algorithm=H.Algorithm.Halp, alpha=5e-5, epochs=1, inner_steps=epoch_T, bits=16, mu=1.0,
-                              seed=0)
-        H.run_halp(obj, H.OptimizerConfig(algorithm=H.Algorithm.Halp, alpha=5e-5, epochs=1, inner_steps=1000, bits=16,
-                                          mu=1.0, seed=0))
-        torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        rec = H.run_halp(obj, c)
-        e1.record()
-        torch.cuda.synchronize()
-        tim = obj.timing()
-        epoch = {"workload": "C3 HALP epoch: 4194304x4096 f32, b=16, T=N/8=524288, alpha=5e-5, mu=1 "
-                             "(full passes at the epoch start and the final boundary included)",
-                 "ms": e0.elapsed_time(e1), "inner_ms": tim["inner_ms"],
-                 "inner_steps_per_s": epoch_T / (tim["inner_ms"] / 1000.0),
-                 "loss_first_last": [rec.rows[0].loss, rec.rows[-1].loss]}
-    del obj, X, y
-    torch.cuda.empty_cache()
-    return ms, algo_bytes, pl, epoch
+    pl = obj.plan()
+    rows = int(n * (pl["fg_split_end"] - pl["fg_split_begin"]) // pl["fg_splits"])
+    return ms, rows * d * 2 + rows * 4, pl
+
+
+def c2_epochs(H, device, rank, epochs):
+    """the MNIST-shaped softmax epoch (BASELINE C2), inputs resident"""
+    import torch
+
+    X, lab = H.generate("softmax", C2["n"], C2["d"], num_classes=C2["C"], dtype="f32", density=C2["density"],
+                        seed=rank, device=device)
+    obj = H.Objective(H.Dataset(X, labels=lab, num_classes=C2["C"]), H.LossFamily.Softmax, C2["l2"], device=device)
+    cfg = lambda k: H.OptimizerConfig(algorithm=H.Algorithm.Halp, alpha=C2["alpha"], epochs=k, inner_steps=C2["n"],
+                                      bits=C2["bits"], mu=C2["mu"], seed=rank)
+    H.run_halp(obj, cfg(1))
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    rec = H.run_halp(obj, cfg(epochs))
+    e1.record()
+    torch.cuda.synchronize()
+    tim = obj.timing()
+    ms = e0.elapsed_time(e1)
+    return {"workload": "C2: softmax N=60000 d=784 C=10 fp32 (80% zeros), l2=1e-4, HALP b=8, alpha=0.01, T=N, "
+                        "mu=2.5", "epochs_per_s": epochs / (ms / 1000.0), "ms_per_epoch": ms / epochs,
+            "inner_ns_per_step": 1e6 * tim["inner_ms"] / (epochs * C2["n"]),
+            "fullgrad_ms_per_pass": tim["fullgrad_ms"] / (epochs + 1),
+            "loss_first_last": [rec.rows[0].loss, rec.rows[-1].loss]}
 
 
 GRID = dict(n=1000, d=64, alphas=17, mus=13, seeds=(1, 2, 3), epochs=10, T=2000)
@@ -232,10 +269,10 @@ def grid_bench(H, device):
                         "least-squares problem, HALP b=8, T=2000, K=10; all runs in one K5 launch",
             "runs": runs, "wall_ms": 1000.0 * dt, "runs_per_s": runs / dt, "device_ms": res.device_ms,
             "best": {"alpha": res.best_config.alpha, "mu": res.best_config.mu,
-                     "grad_norm": res.points[res.best_index].mean_metric}}, (X.cpu().numpy(), y.cpu().numpy())
+                     "grad_norm": res.points[res.best_index].mean_metric}}
 
 
-def c5_batch(H, device, rank, reps=1):
+def c5_batch(H, device, rank, reps=2):
     """BASELINE C5: 512 independent least-squares HALP problems per GPU (4096 x 128
     fp32 Gaussian, per-problem seeds, alpha log-uniform [1e-4, 1e-2], b in {8, 16}
     alternating, T = 2N, K = 10, mu = 3 (unspecified in BASELINE; the golden value)),
@@ -269,15 +306,16 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--no-fullgrad", action="store_true")
+    ap.add_argument("--no-extras", action="store_true", help="headline + e2e + cpu only")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--no-batch", action="store_true")
     ap.add_argument("--fg-reps", type=int, default=10)
-    ap.add_argument("--no-c3-epoch", action="store_true")
     args = ap.parse_args()
     rank, world, local = dist_env()
-    if args.warmup < 3 and args.impl == "b200":
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if args.warmup < 3:
         args.warmup = 3
 
     import torch
@@ -289,12 +327,6 @@ def main():
 
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         pg = dist
-    if args.impl == "reference":
-        run_reference(args, rank, world)
-        if pg:
-            pg.barrier()
-            pg.destroy_process_group()
-        return
 
     import paper_1803_03383_b200 as H
 
@@ -313,125 +345,138 @@ def main():
         pg.all_reduce(t, op=pg.ReduceOp.MAX)
         return float(t.item())
 
-    # ---------------- headline: C2 HALP epochs, inputs resident in HBM ----------------
-    X, lab = c2_data(H, rank, local)
-    obj = H.Objective(H.Dataset(X, labels=lab, num_classes=C2["C"]), H.LossFamily.Softmax, C2["l2"], device=local)
-    H.run_halp(obj, c2_config(H, args.warmup, rank))
+    nccl_id = None
+    if world > 1:
+        import ctypes
+
+        nccl = ctypes.CDLL("libnccl.so.2")
+        idb = ctypes.create_string_buffer(128)
+        if rank == 0:
+            nccl.ncclGetUniqueId(idb)
+        t = torch.tensor(list(idb.raw), dtype=torch.uint8, device="cuda")
+        pg.broadcast(t, 0)
+        nccl_id = bytes(t.cpu().tolist())
+
+    # ---------------- headline: C3 HALP epochs, inputs resident in HBM ----------------
+    obj, X, y = c3_objective(H, local, world, rank, nccl_id)
+    H.run_halp(obj, c3_config(H, args.warmup))
     barrier()
     clk = Clocks(local)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record()
-    rec = H.run_halp(obj, c2_config(H, args.steps, rank))
+    rec = H.run_halp(obj, c3_config(H, args.steps))
     ev1.record()
     barrier()
     clocks = clk.stop()
     ms_total = max_over_ranks(ev0.elapsed_time(ev1))
     tim = obj.timing()
-    ms_step = ms_total / args.steps
-    value = world * args.steps / (ms_total / 1000.0)
-    inner_ms_epoch = tim["inner_ms"] / args.steps
-    steps_per_s = C2["n"] / (inner_ms_epoch / 1000.0)
-    gpu_launches = int(tim["kernel_launches"])
     plan = obj.plan()
-    final_loss = rec.rows[-1].loss
-    first_loss = rec.rows[0].loss
-    c2_fg_passes = args.steps + 1
+    ms_step = ms_total / args.steps
+    value = args.steps / (ms_total / 1000.0)
+    inner_ns = 1e6 * tim["inner_ms"] / (args.steps * C3["T"])
+    fg_passes = args.steps + 1
+    fg_ms = tim["fullgrad_ms"] / fg_passes  # K1 + split tree, CUDA events on the solver stream
+    rows_local = int(C3["n"] * (plan["fg_split_end"] - plan["fg_split_begin"]) // plan["fg_splits"])
+    algo_bytes = rows_local * C3["d"] * 4 + rows_local * 8
+    achieved = algo_bytes / (fg_ms / 1000.0) / 1e9
+    traffic = None
+    try:
+        tj = json.load(open(os.path.join(ROOT, "profiles", "k1_traffic.json")))["C3"]
+        traffic = tj["dram_read_bytes_per_launch"] + tj["dram_write_bytes_per_launch"]
+    except Exception:
+        pass
+    roofline = {"kernel": "k1_stream (+k1_tree_pass): the C3 full-gradient + loss pass (north star: >= 70% of HBM)",
+                "bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                "frac": achieved / pk["hbm_gbs"], "traffic": traffic,
+                "traffic_source": "profiles/k1_traffic.json (ncu dram__bytes_read+write per launch)",
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "_fallback" not in pk else "fallback 6650 GB/s",
+                "algorithmic_bytes_per_launch": algo_bytes, "launch_ms": fg_ms,
+                "bytes_model": "rows*d*4 (x, fp32) + rows*8 (y, fp64) per pass; rows = this rank's row shard",
+                "timed": f"K1 time inside the timed region ({fg_passes} passes, CUDA events on the solver stream)",
+                "note": "K1 is the HBM-bound kernel; the epoch's dominant kernel is K3 (latency-bound serial "
+                        "chain, see inner_loop)"}
+    inner = {"kernel": "k3_inner", "bound": "latency (one serial chain per step)", "ns_per_step": inner_ns,
+             "steps_per_s": 1e9 / inner_ns, "cycles_per_step_at_sm_clock": inner_ns * (clocks.get("sm_mhz") or 0) / 1e3,
+             "share_of_epoch": tim["inner_ms"] / ms_total if world == 1 else None,
+             "plan": {k: plan[k] for k in ("in_ctas", "in_threads", "in_per")}}
+    gpu_launches = int(tim["kernel_launches"])
+    loss_fl = [rec.rows[0].loss, rec.rows[-1].loss]
 
-    # ---------------- e2e: same epoch through the public API from pinned host buffers ----------------
+    # ---------------- e2e: the same epoch through the public API from pinned host buffers ----------------
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and world == 1:
         Xh = torch.empty(X.shape, dtype=X.dtype, pin_memory=True)
         Xh.copy_(X)
-        lh = torch.empty(lab.shape, dtype=lab.dtype, pin_memory=True)
-        lh.copy_(lab)
-        Xn, ln = Xh.numpy(), lh.numpy()
+        yh = y.cpu().numpy()
+        Xn = Xh.numpy()
+        del obj, X, y
+        torch.cuda.empty_cache()
         e_steps = max(1, min(args.steps, 3))
         barrier()
-        t0 = torch.cuda.Event(enable_timing=True)
-        t1 = torch.cuda.Event(enable_timing=True)
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         h2d = d2h = 0
         t0.record()
         for _ in range(e_steps):
-            o2 = H.Objective(H.Dataset(Xn, labels=ln, num_classes=C2["C"]), H.LossFamily.Softmax, C2["l2"],
-                             device=local)
-            r2 = H.run_halp(o2, c2_config(H, 1, rank))
+            o2 = H.Objective(H.Dataset(Xn, targets=yh), H.LossFamily.Squared, C3["l2"], device=local)
+            r2 = H.run_halp(o2, c3_config(H, 1))
             tt = o2.timing()
-            h2d += Xn.nbytes + ln.nbytes + tt["h2d_bytes"]
-            d2h += tt["d2h_bytes"]
+            h2d += tt["h2d_bytes"] + Xn.nbytes + yh.nbytes
+            d2h += tt["d2h_bytes"] + r2.final_iterate.nbytes
             del o2
         t1.record()
         barrier()
-        e_ms = max_over_ranks(t0.elapsed_time(t1))
-        e2e = {"value": world * e_steps / (e_ms / 1000.0), "unit": "epochs/s",
-               "h2d_bytes_per_step": int(h2d // e_steps), "d2h_bytes_per_step": int(d2h // e_steps),
-               "ms_per_step": e_ms / e_steps,
-               "path": "Objective(host numpy X, labels) -> run_halp(epochs=1) -> RunRecord, per step"}
-        del Xh, lh, r2
-    del obj, X, lab
+        e_ms = t0.elapsed_time(t1)
+        e2e = {"value": e_steps / (e_ms / 1000.0), "unit": UNIT, "h2d_bytes_per_step": int(h2d // e_steps),
+               "d2h_bytes_per_step": int(d2h // e_steps), "ms_per_step": e_ms / e_steps,
+               "path": "Objective(pinned host numpy X, y) -> run_halp(epochs=1) -> RunRecord per step "
+                       "(68.7 GB upload of X inside every step)"}
+        del Xh, Xn
+    else:
+        if world > 1:
+            e2e = {"value": None, "unit": UNIT, "h2d_bytes_per_step": None, "d2h_bytes_per_step": None,
+                   "note": "not measured at N>1: every rank needs the full 68.7 GB X pinned on one host "
+                           "(196 GB RAM)"}
+        del obj, X, y
     torch.cuda.empty_cache()
 
-    # ---------------- K1 full-gradient sweeps (roofline) ----------------
-    fullgrad = {}
-    roofline = None
-    if not args.no_fullgrad:
-        nid = None
-        if world > 1:
-            import ctypes
-
-            from paper_1803_03383_b200 import _capi  # noqa: F401
-
-            nccl = ctypes.CDLL("libnccl.so.2")
-            idb = ctypes.create_string_buffer(128)
-            if rank == 0:
-                nccl.ncclGetUniqueId(idb)
-            t = torch.tensor(list(idb.raw), dtype=torch.uint8, device="cuda")
-            pg.broadcast(t, 0)
-            nid = bytes(t.cpu().tolist())
-        for name, cfg in (("C3", C3), ("C4", C4)):
-            barrier()
-            ms, algo, pl, epoch = fullgrad_sweep(H, cfg, local, args.fg_reps, world, rank, nid,
-                                                 epoch_T=(cfg["n"] // 8) if name == "C3" and not args.no_c3_epoch else 0)
-            ms = max_over_ranks(ms)
-            tot_bytes = algo * world
-            gbs = tot_bytes / (ms / 1000.0) / 1e9
-            fullgrad[name] = {"shape": f"{cfg['n']}x{cfg['d']} {cfg['dtype']}", "ms_per_pass": ms,
-                              "GB_per_s": gbs, "frac_of_hbm_peak": gbs / world / pk["hbm_gbs"],
-                              "algorithmic_bytes_per_gpu": algo, "splits": pl["fg_splits"]}
-            if epoch is not None:
-                fullgrad[name]["halp_epoch"] = epoch
-        c3 = fullgrad["C3"]
-        traffic = None
-        try:
-            tj = json.load(open(os.path.join(ROOT, "profiles", "k1_traffic.json")))["C3"]
-            traffic = tj["dram_read_bytes_per_launch"] + tj["dram_write_bytes_per_launch"]
-        except Exception:
-            pass
-        roofline = {"kernel": "k1_stream (+k1_tree_pass), C3 full-gradient pass", "bound": "hbm",
-                    "achieved": c3["GB_per_s"] / world, "peak": pk["hbm_gbs"], "unit": "GB/s",
-                    "frac": c3["GB_per_s"] / world / pk["hbm_gbs"], "traffic": traffic,
-                    "traffic_source": "profiles/k1_traffic.json (ncu dram__bytes_read+write per launch)",
-                    "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "_fallback" not in pk else "fallback 6650 GB/s",
-                    "algorithmic_bytes_per_launch": c3["algorithmic_bytes_per_gpu"],
-                    "bytes_model": "N*d*4 (x, fp32) + N*8 (y, fp64) per pass"}
-
-    # ---------------- C5: batched independent problems (K5) ----------------
-    batch = None
-    if not args.no_batch:
+    extras = {}
+    if not args.no_extras:
+        # ---------------- K1 full-gradient sweeps (C3 via a fresh problem, C4) ----------------
+        barrier()
+        o3, X3, y3 = c3_objective(H, local, world, rank, nccl_id)
+        o3.full_gradient(np.random.default_rng(7).standard_normal(o3.dim()) * 0.5)
+        o3.bench_full_gradient(2)
+        ms3 = max_over_ranks(o3.bench_full_gradient(args.fg_reps))
+        gbs3 = algo_bytes * world / (ms3 / 1000.0) / 1e9
+        del o3, X3, y3
+        torch.cuda.empty_cache()
+        barrier()
+        ms4, b4, _ = fullgrad_c4(H, local, args.fg_reps, world, rank, nccl_id)
+        ms4 = max_over_ranks(ms4)
+        gbs4 = b4 * world / (ms4 / 1000.0) / 1e9
+        torch.cuda.empty_cache()
+        extras["fullgrad"] = {
+            "C3": {"shape": "4194304x4096 f32", "ms_per_pass": ms3, "GB_per_s": gbs3,
+                   "frac_of_hbm_peak": gbs3 / world / pk["hbm_gbs"], "algorithmic_bytes_per_gpu": algo_bytes,
+                   "includes": "K1 + split tree" + (" + NCCL all-gather + finalize" if world > 1 else "")},
+            "C4": {"shape": "16777216x1024 bf16 (softmax C=2)", "ms_per_pass": ms4, "GB_per_s": gbs4,
+                   "frac_of_hbm_peak": gbs4 / world / pk["hbm_gbs"], "algorithmic_bytes_per_gpu": b4}}
+        # ---------------- C2 epochs (MNIST-shaped softmax) ----------------
+        barrier()
+        extras["c2"] = c2_epochs(H, local, rank, 5)
+        torch.cuda.empty_cache()
+        # ---------------- C5: batched independent problems (K5) ----------------
         barrier()
         bms, ndiv, inner_steps = c5_batch(H, local, rank)
         bms = max_over_ranks(bms)
-        batch = {"workload": "C5: 512 least-squares problems/GPU, 4096x128 fp32, T=2N=8192, K=10, b 8/16, mu 3",
-                 "problems": C5["nprob"] * world, "ms_per_batch": bms,
-                 "problem_epochs_per_s": C5["nprob"] * world * C5["epochs"] / (bms / 1000.0),
-                 "inner_steps_per_s": inner_steps * world / (bms / 1000.0), "diverged": ndiv,
-                 "scaling": "weak (problems sharded, no collective)"}
+        extras["batch"] = {"workload": "C5: 512 least-squares problems/GPU, 4096x128 fp32, T=2N=8192, K=10, b 8/16, "
+                                       "mu 3", "problems": C5["nprob"] * world, "ms_per_batch": bms,
+                           "problem_epochs_per_s": C5["nprob"] * world * C5["epochs"] / (bms / 1000.0),
+                           "inner_steps_per_s": inner_steps * world / (bms / 1000.0), "diverged": ndiv,
+                           "scaling": "weak (problems sharded, no collective)"}
         torch.cuda.empty_cache()
-
-    # ---------------- batched grid search (rank 0 of every replica) ----------------
-    grid, grid_data = None, None
-    if not args.no_batch:
         barrier()
-        grid, grid_data = grid_bench(H, local)
+        extras["grid"] = grid_bench(H, local)
         torch.cuda.empty_cache()
 
     # ---------------- CPU baseline (rank 0, N=1 only) ----------------
@@ -440,46 +485,24 @@ def main():
         from oracle import oracle as O
 
         O.build()
-        Xc, lc = c2_data(H, 0, local)
-        Xh2, lh2 = Xc.cpu().numpy(), lc.cpu().numpy()
-        del Xc, lc
-        sample_T = C2["n"] // 4
-        dt, crec = cpu_c2_epoch(O, Xh2, lh2, 1, sample_T)
-        # per-epoch time = full passes (measured) + inner loop scaled to T = N
-        per_epoch = crec.fullgrad_seconds + crec.inner_seconds * (C2["n"] / sample_T)
-        cpu = {"value": 1.0 / per_epoch, "unit": "epochs/s", "cores": 1, "kind": "port",
-               "sample": f"1 C2 epoch with T={sample_T} (inner loop scaled x{C2['n'] // sample_T} to T=N); "
-                         "REF-order oracle, single thread like run_halp (optimizers.cpp:401)",
-               "measured_seconds": dt}
-        if grid_data is not None:
-            # the reference's grid runs its points one after another (harness.cpp:415-417):
-            # time 6 of the grid's runs on one core
-            gX, gy = grid_data
-            go = O.OracleObjective(gX, y=gy)
-            t0 = time.perf_counter()
-            for a_ in (1e-3, 1e-2):
-                for sd in GRID["seeds"]:
-                    O.run_halp(go, O.OracleConfig(alpha=a_, epochs=GRID["epochs"], inner_steps=GRID["T"], bits=8,
-                                                  mu=1.0, seed=sd))
-            cpu["grid_runs_per_s"] = 6 / (time.perf_counter() - t0)
+        threads = os.cpu_count() or 1
+        ep, meas, data = cpu_c3_sample(O, threads)
+        ep2, meas2, _ = cpu_c3_sample(O, threads, data=data)
+        cpu = {"value": 2.0 / (ep + ep2), "unit": UNIT, "cores": threads, "kind": "port",
+               "sample": cpu_sample_text(threads) + " (mean of 2 samples)", "measured_seconds": meas + meas2}
 
     if rank == 0:
         line = {
-            "metric": "HALP epochs/sec", "value": value, "unit": "epochs/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic (K6 device generator, seeded), MNIST-shaped",
-            "config": {"workload": "C2: softmax LR N=60000 d=784 C=10 fp32 (80% zeros), l2=1e-4, HALP b=8, "
-                                   "alpha=0.01, T=60000, mu=2.5", "epochs_timed": args.steps,
-                       "l2_cache": "inputs (188 MB) larger than L2 (126 MB)",
-                       "parallelism": "replicas" if world > 1 else "single GPU",
-                       "plan": {k: plan[k] for k in ("fg_threads", "fg_splits", "in_ctas", "in_threads", "in_per")}},
-            "inner_loop": {"steps_per_s": steps_per_s, "ns_per_step": 1e9 / steps_per_s,
-                           "share_of_epoch": tim["inner_ms"] / ms_total if world == 1 else None},
-            "c2_fullgrad_ms_per_pass": tim["fullgrad_ms"] / c2_fg_passes,
-            "loss_first_last": [first_loss, final_loss],
-            "fullgrad": fullgrad, "batch": batch, "grid": grid, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (K6 device generator, seeded; byte-identical host restatement in oracle/datagen.c)",
+            "config": headline_config(world),
+            "loss_first_last": loss_fl, "roofline": roofline, "inner_loop": inner, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": gpu_launches, "clocks": clocks,
+            "plan": {k: plan[k] for k in ("fg_threads", "fg_splits", "in_ctas", "in_threads", "in_per")},
         }
+        line.update(extras)
         print(json.dumps(line), flush=True)
     if pg:
         pg.barrier()

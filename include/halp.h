@@ -51,7 +51,10 @@ typedef enum { HALP_STATUS_OK = 0, HALP_STATUS_CONVERGED = 1, HALP_STATUS_DIVERG
  * X is row-major n x d (the reference stores fp64 column-major; any dtype
  * here is upcast exactly to fp64 inside the kernels).  mem says whether X,
  * y and labels are host or device (cuda:device) pointers; host data is
- * copied once at creation.  Multi-GPU (world_size > 1): every rank passes
+ * copied once at creation.  Device inputs (HALP_MEM_DEVICE) must be ready
+ * when halp_problem_create is called: the library reads them on its own
+ * non-blocking stream without waiting on the producer's stream (the Python
+ * mirror synchronizes torch's current stream first).  Multi-GPU (world_size > 1): every rank passes
  * the same full problem and a shared 128-byte ncclUniqueId; the
  * full-gradient pass is row-sharded across ranks with one NCCL all-gather
  * per epoch, the sequential inner loop is replicated. */

@@ -713,12 +713,19 @@ static void mirror_inner_dots(const double* x, const double* wa, const double* w
   const int D = d * C, T = pl->in_threads, m = pl->in_per, NC = pl->in_ctas;
   const int ngw = NC * (T / 32);
   double wsa[512], wsb[512];
-  for (int c = 0; c < C; ++c) {
-    double ca = 0.0, cb = 0.0;
-    int first = 1;
-    for (int gw = 0; gw < ngw; ++gw) {
+  int first[64];
+  for (int c = 0; c < C; ++c) { la[c] = 0.0; lb[c] = 0.0; first[c] = 1; }
+  for (int gw = 0; gw < ngw; ++gw) {
+    const int64_t k_lo = (int64_t)gw * 32 * m, k_hi0 = k_lo + 32 * (int64_t)m;
+    const int64_t k_hi = k_hi0 < D ? k_hi0 : D;
+    if (k_lo >= k_hi) {
+      /* warps past D hold no coordinate: +0 records (squared loss keeps them) */
+      if (C == 1) { wsa[gw] = 0.0; wsb[gw] = 0.0; }
+      continue;
+    }
+    const int c_lo = (int)(k_lo / d), c_hi = (int)((k_hi - 1) / d);
+    for (int c = c_lo; c <= c_hi; ++c) {
       double va[32], vb[32];
-      int any = 0;
       for (int l = 0; l < 32; ++l) {
         const int64_t tau = (int64_t)gw * 32 + l;
         double aa = 0.0, ab = 0.0;
@@ -727,36 +734,27 @@ static void mirror_inner_dots(const double* x, const double* wa, const double* w
           const int j = (int)(k % d);
           aa = fma(x[j], wa[k], aa);
           ab = fma(x[j], wb[k], ab);
-          any = 1;
         }
         va[l] = aa;
         vb[l] = ab;
       }
-      if (C == 1) {
-        /* squared loss: every warp's sum is kept, combined below */
-        wsa[gw] = warp_butterfly(va);
-        wsb[gw] = warp_butterfly(vb);
-        continue;
-      }
-      if (!any) continue;
       const double sa = warp_butterfly(va), sb = warp_butterfly(vb);
-      if (first) { ca = sa; cb = sb; first = 0; }
-      else { ca = ca + sa; cb = cb + sb; }
+      if (C == 1) { wsa[gw] = sa; wsb[gw] = sb; continue; }
+      if (first[c]) { la[c] = sa; lb[c] = sb; first[c] = 0; }
+      else { la[c] = la[c] + sa; lb[c] = lb[c] + sb; }
     }
-    if (C == 1) {
-      /* lane l sums warps l, l+32, ... sequentially from 0.0; lane butterfly */
-      double va[32], vb[32];
-      for (int l = 0; l < 32; ++l) {
-        double aa = 0.0, ab = 0.0;
-        for (int q = l; q < ngw; q += 32) { aa = aa + wsa[q]; ab = ab + wsb[q]; }
-        va[l] = aa;
-        vb[l] = ab;
-      }
-      ca = warp_butterfly(va);
-      cb = warp_butterfly(vb);
+  }
+  if (C == 1) {
+    /* lane l sums warps l, l+32, ... sequentially from 0.0; lane butterfly */
+    double va[32], vb[32];
+    for (int l = 0; l < 32; ++l) {
+      double aa = 0.0, ab = 0.0;
+      for (int q = l; q < ngw; q += 32) { aa = aa + wsa[q]; ab = ab + wsb[q]; }
+      va[l] = aa;
+      vb[l] = ab;
     }
-    la[c] = ca;
-    lb[c] = cb;
+    la[0] = warp_butterfly(va);
+    lb[0] = warp_butterfly(vb);
   }
 }
 
@@ -839,6 +837,18 @@ uint64_t oq_hash_vector(const double* v, int64_t len) {
   for (size_t i = 0; i < nb; ++i) {
     h ^= p[i];
     h *= 1099511628211ULL;
+  }
+  return h;
+}
+
+uint64_t oq_code_hash(const int64_t* codes, int64_t len) {
+  uint64_t h = 1469598103934665603ULL;
+  for (int64_t q = 0; q < len; ++q) {
+    uint64_t v = (uint64_t)codes[q];
+    for (int b = 0; b < 8; ++b, v >>= 8) {
+      h ^= v & 255u;
+      h *= 1099511628211ULL;
+    }
   }
   return h;
 }
@@ -971,7 +981,7 @@ int oq_run_halp(const oq_objective* o, const oq_config* cfg, const oq_plan* plan
   rec->fullgrad_seconds = 0.0;
   rec->inner_seconds = 0.0;
   recorder r = {cfg, rec, now_s(), 0.0, D};
-  int64_t steps = 0, traced = 0;
+  int64_t steps = 0, traced = 0, hashed = 0;
   int converged = 0;
   const int fgth = rec->fullgrad_threads > 0 ? rec->fullgrad_threads : 1;
   rc = OQ_OK;
@@ -1040,6 +1050,7 @@ int oq_run_halp(const oq_objective* o, const oq_config* cfg, const oq_plan* plan
         memcpy(rec->trace_codes + traced, code, sizeof(int64_t) * (size_t)D);
         traced += D;
       }
+      if (rec->step_hash && hashed < rec->step_hash_cap) rec->step_hash[hashed++] = oq_code_hash(code, D);
     }
     rec->inner_seconds += now_s() - ti0;
     rec->inner_fp_vector_ops += (uint64_t)(8 * T);

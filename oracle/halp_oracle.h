@@ -147,6 +147,12 @@ typedef struct {
   double   fullgrad_seconds;
   double   inner_seconds;
   int      fullgrad_threads;   /* threads for full_gradient (reference default 1) */
+  /* optional: one 64-bit hash of the codes after every inner step,
+   * [epoch][t] up to step_hash_cap entries (oq_code_hash).  Comparing the
+   * REF-order and MIRROR-order runs' hashes counts the steps whose rounding
+   * decisions depend on the reduction order. */
+  uint64_t* step_hash;
+  int64_t   step_hash_cap;
 } oq_record;
 
 int      oq_run_halp(const oq_objective* o, const oq_config* cfg, const oq_plan* plan, oq_record* rec);
@@ -155,6 +161,8 @@ int      oq_run_halp(const oq_objective* o, const oq_config* cfg, const oq_plan*
 int      oq_run(const oq_objective* o, const oq_config* cfg, const oq_plan* plan, oq_record* rec);
 int64_t  oq_resolve_inner_steps(const oq_config* cfg, int64_t n);
 uint64_t oq_hash_vector(const double* v, int64_t len);
+/* FNV-1a over the int64 code bytes of one inner step (test hook) */
+uint64_t oq_code_hash(const int64_t* codes, int64_t len);
 const char* oq_last_error(void);
 
 /* MIRROR-mode pieces of the multi-GPU full gradient: one rank's split
@@ -162,6 +170,23 @@ const char* oq_last_error(void);
 int oq_split_subtree(const oq_objective* o, const double* w, const oq_plan* plan, int64_t s0, int64_t s1,
                      double* out);
 int oq_finalize(const oq_objective* o, const double* w, const double* rank_sums, int G, double* g, double* loss);
+
+/* ---- K6 synthetic data, host restatement (oracle/datagen.c) ---- */
+typedef struct {
+  int32_t  kind;        /* 0 gaussian regression, 1 sparse-uniform softmax, 2 logistic labels */
+  int64_t  n;
+  int32_t  d;
+  int32_t  num_classes;
+  int32_t  dtype;       /* OQ_F64 / OQ_F32 / OQ_BF16 (raw uint16 bits) */
+  double   noise_sd;
+  double   x_scale;
+  double   density;
+  uint64_t seed;
+} oq_datagen_desc;
+/* rows [row0, row0 + nrows) of the dataset K6 generates for `g` (same bytes),
+ * written to X [nrows][d] and y / labels [nrows]; nthreads host threads */
+int oq_datagen(const oq_datagen_desc* g, int64_t row0, int64_t nrows, int nthreads, void* X, double* y,
+               int32_t* labels);
 
 /* mirror-mode exp/log (identical operation sequence to the device code) */
 double oq_mexp(double x);

@@ -29,7 +29,7 @@ STATUS = {0: "ok", 1: "converged", 2: "diverged"}
 
 def build(force: bool = False) -> str:
     if force or not os.path.exists(LIB_PATH) or os.path.getmtime(LIB_PATH) < max(
-        os.path.getmtime(os.path.join(HERE, f)) for f in ("halp_oracle.c", "halp_oracle.h")
+        os.path.getmtime(os.path.join(HERE, f)) for f in ("halp_oracle.c", "halp_oracle.h", "datagen.c")
     ):
         subprocess.run(["make", "-s", "-C", HERE, "-B" if force else "all"], check=True)
     return LIB_PATH
@@ -68,7 +68,14 @@ class _Record(C.Structure):
         ("final_iterate", C.c_void_p), ("status", C.c_int32), ("steps_taken", C.c_int64),
         ("inner_fp_vector_ops", C.c_uint64), ("trace_codes", C.c_void_p), ("trace_cap", C.c_int64),
         ("fullgrad_seconds", C.c_double), ("inner_seconds", C.c_double), ("fullgrad_threads", C.c_int),
+        ("step_hash", C.c_void_p), ("step_hash_cap", C.c_int64),
     ]
+
+
+class _Datagen(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("n", C.c_int64), ("d", C.c_int32), ("num_classes", C.c_int32),
+                ("dtype", C.c_int32), ("noise_sd", C.c_double), ("x_scale", C.c_double), ("density", C.c_double),
+                ("seed", C.c_uint64)]
 
 
 _lib = None
@@ -99,6 +106,10 @@ def lib():
         L.oq_component_gradient.argtypes = [C.POINTER(_Objective), C.c_int64, C.c_void_p, C.POINTER(_Plan), C.c_void_p]
         L.oq_run_halp.argtypes = [C.POINTER(_Objective), C.POINTER(_Config), C.POINTER(_Plan), C.POINTER(_Record)]
         L.oq_run.argtypes = [C.POINTER(_Objective), C.POINTER(_Config), C.POINTER(_Plan), C.POINTER(_Record)]
+        L.oq_datagen.argtypes = [C.POINTER(_Datagen), C.c_int64, C.c_int64, C.c_int, C.c_void_p, C.c_void_p,
+                                 C.c_void_p]
+        L.oq_code_hash.restype = C.c_uint64
+        L.oq_code_hash.argtypes = [C.c_void_p, C.c_int64]
         L.oq_hash_vector.restype = C.c_uint64
         L.oq_hash_vector.argtypes = [C.c_void_p, C.c_int64]
         L.oq_last_error.restype = C.c_char_p
@@ -304,15 +315,18 @@ class OracleRecord:
     steps_taken: int = 0
     inner_fp_vector_ops: int = 0
     trace: Optional[np.ndarray] = None
+    step_hash: Optional[np.ndarray] = None
     fullgrad_seconds: float = 0.0
     inner_seconds: float = 0.0
     rc: int = 0
 
 
 def run_halp(obj: OracleObjective, cfg: OracleConfig, plan=None, trace_steps: int = 0,
-             fullgrad_threads: int = 1, rows_cap: int = 0) -> OracleRecord:
-    """optimizers.cpp:387-459"""
-    return _run(obj, cfg, plan, trace_steps, fullgrad_threads, rows_cap, 4)
+             fullgrad_threads: int = 1, rows_cap: int = 0, hash_steps: int = 0) -> OracleRecord:
+    """optimizers.cpp:387-459.  hash_steps > 0: OracleRecord.step_hash holds
+    oq_code_hash of the codes after each of the first hash_steps inner steps
+    (over all epochs), for REF-vs-MIRROR rounding-decision comparisons."""
+    return _run(obj, cfg, plan, trace_steps, fullgrad_threads, rows_cap, 4, hash_steps)
 
 
 def run(obj: OracleObjective, cfg: OracleConfig, plan=None, trace_steps: int = 0, fullgrad_threads: int = 1,
@@ -321,7 +335,7 @@ def run(obj: OracleObjective, cfg: OracleConfig, plan=None, trace_steps: int = 0
     return _run(obj, cfg, plan, trace_steps, fullgrad_threads, rows_cap, int(cfg.algorithm))
 
 
-def _run(obj, cfg, plan, trace_steps, fullgrad_threads, rows_cap, algorithm) -> OracleRecord:
+def _run(obj, cfg, plan, trace_steps, fullgrad_threads, rows_cap, algorithm, hash_steps=0) -> OracleRecord:
     init = None
     if cfg.init is not None:
         init = np.ascontiguousarray(cfg.init, dtype=np.float64)
@@ -332,8 +346,10 @@ def _run(obj, cfg, plan, trace_steps, fullgrad_threads, rows_cap, algorithm) -> 
     rows = (_Row * cap)()
     fin = np.zeros(obj.dim, dtype=np.float64)
     tr = np.zeros(trace_steps * obj.dim, dtype=np.int64) if trace_steps else None
+    sh = np.zeros(hash_steps, dtype=np.uint64) if hash_steps else None
     rec = _Record(rows, cap, 0, fin.ctypes.data, 0, 0, 0, tr.ctypes.data if tr is not None else None,
-                  tr.size if tr is not None else 0, 0.0, 0.0, fullgrad_threads)
+                  tr.size if tr is not None else 0, 0.0, 0.0, fullgrad_threads,
+                  sh.ctypes.data if sh is not None else None, hash_steps)
     rc = lib().oq_run(C.byref(obj._s), C.byref(c), _plan(plan), C.byref(rec))
     if rc not in (0, 2):
         _check(rc)
@@ -352,7 +368,13 @@ def _run(obj, cfg, plan, trace_steps, fullgrad_threads, rows_cap, algorithm) -> 
     out.inner_seconds = rec.inner_seconds
     if tr is not None:
         out.trace = tr.reshape(-1, obj.dim)
+    out.step_hash = sh
     return out
+
+
+def code_hash(codes) -> int:
+    c = np.ascontiguousarray(codes, dtype=np.int64)
+    return lib().oq_code_hash(c.ctypes.data, c.size)
 
 
 def hash_vector(v) -> int:
@@ -366,3 +388,28 @@ def mexp(x: float) -> float:
 
 def mlog(x: float) -> float:
     return lib().oq_mlog(x)
+
+
+_KINDS = {"regression": 0, "softmax": 1, "logistic": 2}
+_DTYPES = {"f64": (F64, np.float64), "f32": (F32, np.float32), "bf16": (BF16, np.uint16)}
+
+
+def generate(kind: str, n: int, d: int, *, num_classes: int = 0, dtype: str = "f32", noise_sd: float = 0.0,
+             x_scale: float = 1.0, density: float = 1.0, seed: int = 0, rows=None, threads: int = 0):
+    """Host restatement of the K6 generator (oracle/datagen.c): the same bytes
+    as paper_1803_03383_b200.generate for the same arguments.  rows=(r0, r1)
+    generates only that row range of the n-row dataset (bf16 as uint16 bits).
+    Returns (X, y) for 'regression', (X, labels) otherwise."""
+    code, npdt = _DTYPES[dtype]
+    r0, r1 = rows if rows is not None else (0, n)
+    g = _Datagen(_KINDS[kind], n, d, num_classes, code, noise_sd, x_scale, density, seed)
+    X = np.empty((r1 - r0, d), dtype=npdt)
+    y = lab = None
+    if _KINDS[kind] == 0:
+        y = np.empty(r1 - r0, dtype=np.float64)
+    else:
+        lab = np.empty(r1 - r0, dtype=np.int32)
+    th = threads or (os.cpu_count() or 1)
+    _check(lib().oq_datagen(C.byref(g), r0, r1 - r0, th, X.ctypes.data, y.ctypes.data if y is not None else None,
+                            lab.ctypes.data if lab is not None else None))
+    return (X, y) if y is not None else (X, lab)

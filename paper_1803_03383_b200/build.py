@@ -55,8 +55,22 @@ def _run(cmd, log=None):
     return r
 
 
+def _flags_changed() -> bool:
+    """True when the compiler flags (incl. HALP_NVCC_DEFS variants) differ from
+    the ones the existing objects were built with (build/flags.stamp)."""
+    stamp = os.path.join(BUILD, "flags.stamp")
+    want = " ".join(NVCC_FLAGS) + "\n" + " ".join(CXX_FLAGS) + "\n"
+    have = open(stamp).read() if os.path.exists(stamp) else ""
+    if have != want:
+        with open(stamp, "w") as f:
+            f.write(want)
+        return True
+    return False
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(BUILD, exist_ok=True)
+    force = _flags_changed() or force
     hdrs = [os.path.join(CSRC, h) for h in HEADERS] + [os.path.join(ROOT, "include", "halp.h")]
     jobs = []
     objs = []

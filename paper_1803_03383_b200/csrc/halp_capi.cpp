@@ -128,6 +128,16 @@ uint64_t fnv1a(const double* v, int64_t len) {  // optimizers.cpp:218-227
   return h;
 }
 
+// Blocking copy ordered on `st`.  Every device buffer of a problem / batch is
+// produced and consumed on its own non-blocking stream, so copies must be
+// issued there too: a legacy-stream cudaMemcpy is not ordered against it
+// (and a pageable H2D cudaMemcpy may return before its DMA has landed).
+cudaError_t copy_sync(void* dst, const void* src, size_t bytes, cudaMemcpyKind kind, cudaStream_t st) {
+  cudaError_t e = cudaMemcpyAsync(dst, src, bytes, kind, st);
+  if (e != cudaSuccess) return e;
+  return cudaStreamSynchronize(st);
+}
+
 // ---- device memory: the device's stream-ordered pool, never trimmed ----
 // Problems are created and destroyed per solve (run_prepared, sweeps, the e2e
 // path); keeping freed blocks in the pool makes that O(1) instead of a
@@ -160,7 +170,7 @@ struct RngTables {
   const uint64_t* pow_tab = nullptr;
   std::vector<std::pair<int64_t, const uint64_t*>> jump;  // (D, table)
 };
-int rng_tables(int device, int64_t D, const uint64_t** pow_tab, const uint64_t** jump_tab) {
+int rng_tables(int device, int64_t D, const uint64_t** pow_tab, const uint64_t** jump_tab, cudaStream_t st) {
   static RngTables per_dev[64];
   if (device < 0 || device >= 64) return fail(HALP_INVALID_INPUT, "device index out of range");
   std::lock_guard<std::mutex> lock(host_state_mutex());
@@ -169,7 +179,7 @@ int rng_tables(int device, int64_t D, const uint64_t** pow_tab, const uint64_t**
   if (!t.pow_tab) {
     uint64_t* d = nullptr;
     CU(cudaMalloc(&d, sizeof(uint64_t) * jt.flat.size()));
-    CU(cudaMemcpy(d, jt.flat.data(), sizeof(uint64_t) * jt.flat.size(), cudaMemcpyHostToDevice));
+    CU(copy_sync(d, jt.flat.data(), sizeof(uint64_t) * jt.flat.size(), cudaMemcpyHostToDevice, st));
     t.pow_tab = d;
   }
   *pow_tab = t.pow_tab;
@@ -182,7 +192,7 @@ int rng_tables(int device, int64_t D, const uint64_t** pow_tab, const uint64_t**
   mat_tables(jt.power((uint64_t)D), tab.data());
   uint64_t* d = nullptr;
   CU(cudaMalloc(&d, sizeof(uint64_t) * 2048));
-  CU(cudaMemcpy(d, tab.data(), sizeof(uint64_t) * 2048, cudaMemcpyHostToDevice));
+  CU(copy_sync(d, tab.data(), sizeof(uint64_t) * 2048, cudaMemcpyHostToDevice, st));
   t.jump.emplace_back(D, d);
   *jump_tab = d;
   return HALP_OK;
@@ -215,7 +225,7 @@ struct halp_problem {
   int64_t* idx = nullptr;
   int64_t idx_cap = 0;
   long long* codes = nullptr;
-  int* blow = nullptr;
+  long long* blow = nullptr;
   const uint64_t *pow_tab = nullptr, *jump_tab = nullptr;  // resident per device (rng_tables)
   long long* trace_dev = nullptr;
   int64_t trace_dev_steps = 0;
@@ -402,10 +412,10 @@ int ensure_workspace(halp_problem* p) {
     CU(dalloc(&p->gathered, sizeof(double) * D1 * p->world, st));
     CU(dalloc(&p->stats, sizeof(double) * 4, st));
     CU(dalloc(&p->codes, sizeof(long long) * p->D, st));
-    CU(dalloc(&p->blow, sizeof(int), st));
+    CU(dalloc(&p->blow, sizeof(long long), st));
     CU(dalloc(&p->zb0, sizeof(double) * p->D, st));
     CU(dalloc(&p->zb1, sizeof(double) * p->D, st));
-    int rc = rng_tables(p->device, p->D, &p->pow_tab, &p->jump_tab);
+    int rc = rng_tables(p->device, p->D, &p->pow_tab, &p->jump_tab, p->stream);
     if (rc) return rc;
     CU(cudaEventCreate(&p->ev_fg.a));
     CU(cudaEventCreate(&p->ev_fg.b));
@@ -669,7 +679,7 @@ int halp_problem_create(const halp_problem_desc* desc, halp_problem** out) {
     const int32_t* lh = static_cast<const int32_t*>(desc->labels);
     if (dev_in) {
       lab.resize(p->n);
-      if (cudaMemcpy(lab.data(), desc->labels, sizeof(int32_t) * p->n, cudaMemcpyDeviceToHost) != cudaSuccess)
+      if (copy_sync(lab.data(), desc->labels, sizeof(int32_t) * p->n, cudaMemcpyDeviceToHost, p->stream) != cudaSuccess)
         return bail(fail(HALP_CUDA_ERROR, "copy of labels failed"));
       lh = lab.data();
     }
@@ -772,11 +782,11 @@ int halp_full_gradient(halp_problem* p, const double* w, double* g, double* loss
   if (!p || !w) return fail(HALP_INVALID_INPUT, "halp_full_gradient: null argument");
   CU(cudaSetDevice(p->device));
   p->timing = halp_timing{};
-  CU(cudaMemcpy(p->w, w, sizeof(double) * p->D, cudaMemcpyHostToDevice));
+  CU(copy_sync(p->w, w, sizeof(double) * p->D, cudaMemcpyHostToDevice, p->stream));
   double gn, delta, l;
   int rc = full_pass(p, &gn, &delta, &l, 1.0, 8, 1e-300);
   if (rc) return rc;
-  if (g) CU(cudaMemcpy(g, p->g, sizeof(double) * p->D, cudaMemcpyDeviceToHost));
+  if (g) CU(copy_sync(g, p->g, sizeof(double) * p->D, cudaMemcpyDeviceToHost, p->stream));
   if (loss) *loss = l;
   return HALP_OK;
 }
@@ -891,7 +901,7 @@ int halp_run(halp_problem* p, const halp_config* cfg, halp_record* rec) {
     double gn, delta, loss;
     rc = full_pass(p, &gn, &delta, &loss, mu, bits, cfg->delta_min);
     if (rc) return rc;
-    CU(cudaMemcpy(wh.data(), p->w, sizeof(double) * D, cudaMemcpyDeviceToHost));
+    CU(copy_sync(wh.data(), p->w, sizeof(double) * D, cudaMemcpyDeviceToHost, p->stream));
     p->timing.d2h_bytes += sizeof(double) * D;
     const double row_delta = halp ? delta : lp ? cfg->delta : 0.0;
     rc = r.boundary((double)steps / (double)n, wh.data(), loss, gn, row_delta, k == 0 || (halp && gn == 0.0));
@@ -921,7 +931,7 @@ int halp_run(halp_problem* p, const halp_config* cfg, halp_record* rec) {
     const uint64_t rdraws = halp ? (uint64_t)k * (uint64_t)D * (uint64_t)(T + 1) + (uint64_t)D
                                  : (uint64_t)D + (uint64_t)k * (uint64_t)D * (uint64_t)T;
     const uint64_t r0 = jt.jump(s_round, rdraws);
-    CU(cudaMemsetAsync(p->blow, 0xFF, sizeof(int), p->stream));
+    CU(cudaMemsetAsync(p->blow, 0xFF, sizeof(long long), p->stream));
     const double rcp = 1.0 / kdelta;
     InParams ip{p->X, p->ld, p->d, p->C, (int)D, p->loss, n, p->y, p->labels, p->l2, cfg->alpha, kdelta, hi, lo, maxc,
                 minc, std::isfinite(rcp) && rcp != 0.0 && env_int("HALP_IEEE_DIV", 0) == 0 ? rcp : 0.0, p->w, p->w2,
@@ -932,9 +942,9 @@ int halp_run(halp_problem* p, const halp_config* cfg, halp_record* rec) {
     ++p->timing.kernel_launches;
     ++p->timing.inner_launches;
     CU(cudaEventRecord(p->ev_in.b, p->stream));
-    int blow = -1;
-    CU(cudaMemcpyAsync(&blow, p->blow, sizeof(int), cudaMemcpyDeviceToHost, p->stream));
-    p->timing.d2h_bytes += sizeof(int);
+    long long blow = -1;
+    CU(cudaMemcpyAsync(&blow, p->blow, sizeof(long long), cudaMemcpyDeviceToHost, p->stream));
+    p->timing.d2h_bytes += sizeof(long long);
     CU(cudaStreamSynchronize(p->stream));
     float ms = 0;
     CU(cudaEventElapsedTime(&ms, p->ev_in.a, p->ev_in.b));
@@ -945,7 +955,7 @@ int halp_run(halp_problem* p, const halp_config* cfg, halp_record* rec) {
       const int64_t ns = std::min<int64_t>(tr_steps, (blow >= 0 ? blow : T));
       const int64_t cnt = std::min<int64_t>(ns * D, p->trace_cap - traced);
       std::vector<long long> tmp(cnt);
-      CU(cudaMemcpy(tmp.data(), p->trace_dev, sizeof(long long) * cnt, cudaMemcpyDeviceToHost));
+      CU(copy_sync(tmp.data(), p->trace_dev, sizeof(long long) * cnt, cudaMemcpyDeviceToHost, p->stream));
       for (int64_t q = 0; q < cnt; ++q) p->trace_host[traced + q] = tmp[q];
       traced += cnt;
     }
@@ -953,7 +963,7 @@ int halp_run(halp_problem* p, const halp_config* cfg, halp_record* rec) {
       // Recorder::blowup (optimizers.cpp:156-160; HALP :432-434, LP-SVRG :370-372)
       p->timing.inner_steps += blow + 1;
       std::vector<double> u(D);
-      CU(cudaMemcpy(u.data(), p->u_out, sizeof(double) * D, cudaMemcpyDeviceToHost));
+      CU(copy_sync(u.data(), p->u_out, sizeof(double) * D, cudaMemcpyDeviceToHost, p->stream));
       return r.boundary((double)(steps + blow + 1) / (double)n, u.data(), INFINITY, INFINITY, kdelta, true);
     }
     p->timing.inner_steps += T;
@@ -966,13 +976,13 @@ int halp_run(halp_problem* p, const halp_config* cfg, halp_record* rec) {
     double gn, delta, loss;
     rc = full_pass(p, &gn, &delta, &loss, mu, bits, cfg->delta_min);
     if (rc) return rc;
-    CU(cudaMemcpy(wh.data(), p->w, sizeof(double) * D, cudaMemcpyDeviceToHost));
+    CU(copy_sync(wh.data(), p->w, sizeof(double) * D, cudaMemcpyDeviceToHost, p->stream));
     p->timing.d2h_bytes += sizeof(double) * D;
     rc = r.boundary((double)steps / (double)n, wh.data(), loss, gn, halp ? delta : lp ? cfg->delta : 0.0, true);
     if (rc) return rc;
     if (halp && gn == 0.0) rec->status = HALP_STATUS_CONVERGED;
   } else {
-    CU(cudaMemcpy(wh.data(), p->w, sizeof(double) * D, cudaMemcpyDeviceToHost));
+    CU(copy_sync(wh.data(), p->w, sizeof(double) * D, cudaMemcpyDeviceToHost, p->stream));
   }
   if (rec->final_iterate) std::memcpy(rec->final_iterate, wh.data(), sizeof(double) * D);
   rec->steps_taken = steps;

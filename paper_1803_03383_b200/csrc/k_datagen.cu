@@ -14,6 +14,12 @@
 
 namespace halp {
 
+// Every value is produced by integer hashing and IEEE-exact float/double
+// operations (+ - * / sqrt and explicit fma, never contracted: -fmad=false)
+// plus the deterministic hexp/hlog, so the host restatement
+// oracle/datagen.c (oq_datagen) reproduces the bytes exactly: the reference
+// arm of bench.py and the tests regenerate any row range on the CPU without
+// touching this library.
 __device__ __forceinline__ uint64_t mix64(uint64_t x) {
   x += 0x9E3779B97F4A7C15ULL;
   x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ULL;
@@ -26,19 +32,49 @@ __device__ __forceinline__ uint64_t ctr(uint64_t seed, uint64_t stream, uint64_t
 __device__ __forceinline__ double unif64(uint64_t seed, uint64_t stream, uint64_t i) {
   return (double)(ctr(seed, stream, i) >> 11) * 0x1.0p-53;
 }
+// ln x for x in (0, 1]: x = m 2^e, m in [sqrt(1/2), sqrt(2)), atanh series in f = (m-1)/(m+1)
+__device__ __forceinline__ float det_logf(float x) {
+  const uint32_t b = __float_as_uint(x);
+  int e = (int)((b >> 23) & 255u) - 127;
+  float m = __uint_as_float((b & 0x7FFFFFu) | 0x3F800000u);
+  if (m > 1.41421356f) {
+    m = m * 0.5f;
+    e += 1;
+  }
+  const float f = (m - 1.0f) / (m + 1.0f);
+  const float f2 = f * f;
+  float q = 0.0909090909f;
+  q = q * f2 + 0.111111111f;
+  q = q * f2 + 0.142857143f;
+  q = q * f2 + 0.2f;
+  q = q * f2 + 0.333333333f;
+  const float tf = 2.0f * f;
+  const float lnm = tf + tf * (f2 * q);
+  const float ef = (float)e;
+  return ef * 0.693145752f + (ef * 1.42860677e-06f + lnm);
+}
+// cos(2 pi k / 2^24) for a 24-bit integer k: nearest quarter turn + a polynomial on [-pi/4, pi/4]
+__device__ __forceinline__ float det_cos2pi(uint32_t k) {
+  const uint32_t qu = (k + (1u << 21)) >> 22;
+  const int r = (int)k - (int)(qu << 22);
+  const float a = (float)r * 3.74507028e-07f;  // (pi/2) / 2^22
+  const float a2 = a * a;
+  const float c = 1.0f + a2 * (-0.5f + a2 * (0.0416666667f + a2 * (-0.00138888889f + a2 * 2.48015873e-05f)));
+  const float s = a + (a * a2) * (-0.166666667f + a2 * (0.00833333333f + a2 * (-0.000198412698f + a2 * 2.75573192e-06f)));
+  const uint32_t q = qu & 3u;
+  return q == 0 ? c : q == 1 ? -s : q == 2 ? -c : s;
+}
 __device__ __forceinline__ float unif32(uint64_t seed, uint64_t stream, uint64_t i) {
   return (float)(ctr(seed, stream, i) >> 40) * 0x1.0p-24f;
 }
+// Box-Muller from one 64-bit hash: 24 bits for the radius, 24 for the angle
 __device__ __forceinline__ float normal32(uint64_t seed, uint64_t stream, uint64_t i) {
   const uint64_t h = ctr(seed, stream, i);
   const float u1 = ((float)(h >> 40) + 0.5f) * 0x1.0p-24f;
-  const float u2 = (float)((h >> 16) & 0xFFFFFF) * 0x1.0p-24f;
-  return sqrtf(-2.0f * logf(u1)) * cospif(2.0f * u2);
+  return sqrtf(-2.0f * det_logf(u1)) * det_cos2pi((uint32_t)((h >> 16) & 0xFFFFFFu));
 }
 __device__ __forceinline__ double normal64(uint64_t seed, uint64_t stream, uint64_t i) {
-  const double u1 = unif64(seed, stream, 2 * i) + 0x1.0p-54;
-  const double u2 = unif64(seed, stream, 2 * i + 1);
-  return sqrt(-2.0 * log(u1)) * cospi(2.0 * u2);
+  return (double)normal32(seed, stream, i);
 }
 
 template <class Tx> __device__ __forceinline__ Tx from_f(float v);
@@ -89,7 +125,7 @@ __global__ void k_gen_y(GenParams p) {
         double bv = -1e300;
         for (int c = 0; c < C; ++c) {
           const double u = unif64(p.seed, 4, (uint64_t)i * C + c) + 0x1.0p-54;
-          const double v = acc[c] - log(-log(u));
+          const double v = acc[c] - hlog(-hlog(u));
           if (v > bv) {
             bv = v;
             best = c;
@@ -97,7 +133,7 @@ __global__ void k_gen_y(GenParams p) {
         }
         p.labels[i] = best;
       } else {
-        const double pr = 1.0 / (1.0 + exp(-acc[0]));
+        const double pr = 1.0 / (1.0 + hexp(-acc[0]));
         p.labels[i] = unif64(p.seed, 4, (uint64_t)i) < pr ? 1 : 0;
       }
     }

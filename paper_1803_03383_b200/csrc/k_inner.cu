@@ -443,7 +443,7 @@ __global__ void __launch_bounds__(256, 1) k3_inner(InParams p) {
     }
     if (last) {
       if (flagged()) {
-        if (rank == 0 && tid == 0) *p.blow_step = (int)(t - 1);
+        if (rank == 0 && tid == 0) *p.blow_step = (long long)(t - 1);
         if (CL) cluster_sync_all();  // nobody leaves while remote stores may target it
         return;
       }
@@ -583,7 +583,7 @@ __global__ void __launch_bounds__(256, 1) k3_inner(InParams p) {
           code[i] = (double)quantize_code(up[i], delta, p.hi, p.lo, p.maxc, p.minc, Ua[i]);
     }
     if (__any_sync(0xffffffffu, fl) && (KIND == 2 || flagged())) {
-      if (rank == 0 && tid == 0) *p.blow_step = (int)(t - 1);
+      if (rank == 0 && tid == 0) *p.blow_step = (long long)(t - 1);
       if (CL) cluster_sync_all();  // nobody leaves while remote stores may target it
       return;
     }

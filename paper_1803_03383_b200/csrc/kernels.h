@@ -81,7 +81,7 @@ struct InParams {
   long long* codes_out;      // [D] codes after the last step
   long long* trace;          // [trace_steps][D] or null
   int64_t trace_steps;
-  int* blow_step;            // -1 or failing step index
+  long long* blow_step;      // -1 or failing step index (64-bit: user T may exceed 2^31)
   double* u_out;             // [D] update vector of the failing step
   // algorithm: 0 HALP (wz = w~ + z, z = Q(u)), 1 LP-SVRG (fixed scale: the
   // iterate itself is quantized, wz = z), 2 SVRG (fp64 iterate in z, delta = 1,

@@ -196,6 +196,13 @@ class Objective:
                 lptr = lab.ctypes.data
             self._keep.append(lab)
             C_ = int(ds.num_classes)
+        if dev:
+            # HALP_MEM_DEVICE readiness contract (halp.h): the library reads X / y /
+            # labels on its own stream, so whatever produced them (and the
+            # conversions above) must have finished
+            import torch
+
+            torch.cuda.current_stream(X.device).synchronize()
         idbuf = None
         if nccl_id is not None:
             idbuf = C.create_string_buffer(bytes(nccl_id), 128)
@@ -680,6 +687,7 @@ class BatchProblems:
             X = X.contiguous()
             y = torch.as_tensor(y, dtype=torch.float64, device=X.device).contiguous()
             xptr, yptr = X.data_ptr(), y.data_ptr()
+            torch.cuda.current_stream(X.device).synchronize()  # readiness contract (halp.h)
         else:
             X = np.ascontiguousarray(X)
             y = np.ascontiguousarray(y, dtype=np.float64)
