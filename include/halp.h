@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define HALP_ABI_VERSION 3
+#define HALP_ABI_VERSION 4
 
 typedef enum {
   HALP_OK = 0,
@@ -72,7 +72,11 @@ typedef struct {
   int32_t        device;
   int32_t        world_size;   /* 1 => single GPU */
   int32_t        rank;
-  const void*    nccl_id;      /* 128 bytes (ncclUniqueId) when world_size > 1 */
+  const void*    nccl_id;      /* 128 bytes (ncclUniqueId) when world_size > 1 or collective == 1 */
+  int32_t        collective;   /* 0: NCCL iff world_size > 1; 1: always run the NCCL route (all-gather
+                                  of the rank sums + rank-tree finalize), also at world_size 1;
+                                  2: no NCCL, the caller moves the rank sums (test hook:
+                                  halp_rank_partial / halp_finalize_gathered only); ABI >= 4 */
 } halp_problem_desc;
 
 typedef struct halp_problem halp_problem;
@@ -166,9 +170,18 @@ int halp_set_trace(halp_problem* p, int64_t* codes, int64_t cap);
 
 int halp_last_timing(const halp_problem* p, halp_timing* out);
 
+/* The two halves of the sharded full gradient with the exchange done by the
+ * caller (problems created with collective == 2; test hook for the rank
+ * plumbing on one GPU): this rank's subtree root [D+1] (K1 over its splits
+ * + split tree) at host w, and the finalize over world_size gathered roots
+ * [world][D+1] -> g (D), loss. */
+int halp_rank_partial(halp_problem* p, const double* w, double* root);
+int halp_finalize_gathered(halp_problem* p, const double* w, const double* gathered, double* g, double* loss);
+
 /* Kernel-only timing helper for bench.py: runs `reps` full-gradient passes
- * at the device-resident iterate w (device pointer or NULL = zeros) and
- * returns the average device time per pass (ms). */
+ * at the device-resident iterate and returns the average device time per
+ * pass (ms): K1 + split tree, plus the NCCL all-gather and the finalize
+ * when the problem uses the collective (so multi-GPU GB/s include it). */
 int halp_bench_full_gradient(halp_problem* p, int reps, double* ms_per_pass);
 
 /* ---- batched independent problems (one persistent CTA per problem) ---- */

@@ -23,7 +23,7 @@ class ProblemDesc(C.Structure):
         ("X", C.c_void_p), ("dtype", C.c_int32), ("mem", C.c_int32), ("n", C.c_int64), ("d", C.c_int32),
         ("loss", C.c_int32), ("num_classes", C.c_int32), ("y", C.c_void_p), ("labels", C.c_void_p),
         ("l2", C.c_double), ("device", C.c_int32), ("world_size", C.c_int32), ("rank", C.c_int32),
-        ("nccl_id", C.c_void_p),
+        ("nccl_id", C.c_void_p), ("collective", C.c_int32),
     ]
 
 
@@ -83,7 +83,7 @@ SYMBOLS = [
     "halp_last_error", "halp_abi_version", "halp_problem_create", "halp_problem_destroy", "halp_problem_plan",
     "halp_run", "halp_full_gradient", "halp_set_trace", "halp_last_timing", "halp_bench_full_gradient",
     "halp_batch_create", "halp_batch_destroy", "halp_batch_run", "halp_datagen", "halp_shard_plan",
-    "halp_rng_state_after", "halp_plan_for", "halp_batch_plan",
+    "halp_rng_state_after", "halp_plan_for", "halp_batch_plan", "halp_rank_partial", "halp_finalize_gathered",
 ]
 
 _lib = None
@@ -118,6 +118,8 @@ def lib():
     L.halp_shard_plan.argtypes = [C.c_int64, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32] + [
         C.POINTER(C.c_int64)] * 5
     L.halp_plan_for.argtypes = [C.c_int64, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.POINTER(Plan)]
+    L.halp_rank_partial.argtypes = [P, C.c_void_p, C.c_void_p]
+    L.halp_finalize_gathered.argtypes = [P, C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(C.c_double)]
     L.halp_rng_state_after.restype = C.c_uint64
     L.halp_rng_state_after.argtypes = [C.c_uint64, C.c_uint64, C.c_uint64]
     _lib = L

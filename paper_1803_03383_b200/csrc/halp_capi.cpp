@@ -234,6 +234,7 @@ struct halp_problem {
   halp_timing timing{};
   int64_t create_h2d = 0;  // bytes uploaded by halp_problem_create
   int x_finite = 0;        // bf16 X checked finite (K1 integer-conversion path)
+  bool host_exchange = false;  // collective == 2: the caller moves the rank sums (test hook)
   Events ev_fg, ev_fin, ev_in, ev_smp;
 
   ~halp_problem() {
@@ -434,6 +435,21 @@ FgParams fg_params(const halp_problem* p, int pass) {
                   (int)p->sp.S, (int)p->sp.split_begin, pass * p->fg.ct, pass == 0, p->partials, p->x_finite};
 }
 
+// the exchange step of the row-sharded full gradient: every rank's subtree
+// root (D+1 doubles) all-gathered over NCCL, then the same rank tree on
+// every rank (k_finalize) -> identical g, |g|, delta, loss on all ranks
+int gather_finalize(halp_problem* p, double mu, int bits, double delta_min) {
+  const int64_t D1 = p->D + 1;
+  if (p->comm) {
+    ncclResult_t r = Nccl::get().allGather(p->rank_sum, p->gathered, (size_t)D1, ncclFloat64, p->comm, p->stream);
+    if (r != ncclSuccess) return fail(HALP_NCCL_ERROR, std::string("ncclAllGather: ") + Nccl::get().errStr(r));
+  }
+  FinParams fin{p->gathered, p->world, p->D, p->w, p->n, p->l2, mu, delta_min, bits, p->g, p->stats};
+  CU(launch_finalize(fin, p->stream));
+  ++p->timing.kernel_launches;
+  return HALP_OK;
+}
+
 // K1 + split tree (+ all-gather) + finalize at p->w; stats -> host
 int full_pass(halp_problem* p, double* gn, double* delta, double* loss, double mu, int bits, double delta_min) {
   const int64_t D1 = p->D + 1;
@@ -446,18 +462,13 @@ int full_pass(halp_problem* p, double* gn, double* delta, double* loss, double m
     CU(launch_fullgrad(L, fp, p->stream));
     ++p->timing.kernel_launches;
   }
-  CU(launch_split_tree(p->partials, nloc, (int)D1, p->world > 1 ? p->rank_sum : p->gathered, p->tree_scratch,
+  CU(launch_split_tree(p->partials, nloc, (int)D1, p->comm ? p->rank_sum : p->gathered, p->tree_scratch,
                         p->stream));
   ++p->timing.kernel_launches;
   CU(cudaEventRecord(p->ev_fg.b, p->stream));
   CU(cudaEventRecord(p->ev_fin.a, p->stream));
-  if (p->world > 1) {
-    ncclResult_t r = Nccl::get().allGather(p->rank_sum, p->gathered, (size_t)D1, ncclFloat64, p->comm, p->stream);
-    if (r != ncclSuccess) return fail(HALP_NCCL_ERROR, std::string("ncclAllGather: ") + Nccl::get().errStr(r));
-  }
-  FinParams fin{p->gathered, p->world, p->D, p->w, p->n, p->l2, mu, delta_min, bits, p->g, p->stats};
-  CU(launch_finalize(fin, p->stream));
-  ++p->timing.kernel_launches;
+  int rc = gather_finalize(p, mu, bits, delta_min);
+  if (rc) return rc;
   CU(cudaEventRecord(p->ev_fin.b, p->stream));
   double st[4];
   CU(cudaMemcpyAsync(st, p->stats, sizeof(double) * 3, cudaMemcpyDeviceToHost, p->stream));
@@ -695,8 +706,12 @@ int halp_problem_create(const halp_problem_desc* desc, halp_problem** out) {
   p->sp = shard_plan_for(p->n, p->d, C, p->dtype, world, p->rank);
   int rc = choose_plans(p);
   if (rc) return bail(rc);
-  if (world > 1) {
-    if (!desc->nccl_id) return bail(fail(HALP_INVALID_INPUT, "world_size > 1 needs an ncclUniqueId"));
+  if (desc->collective < 0 || desc->collective > 2)
+    return bail(fail(HALP_INVALID_INPUT, "halp_problem_create: collective must be 0, 1 or 2"));
+  if (desc->rank < 0 || desc->rank >= world) return bail(fail(HALP_INVALID_INPUT, "rank outside [0, world_size)"));
+  p->host_exchange = desc->collective == 2;
+  if (!p->host_exchange && (world > 1 || desc->collective == 1)) {
+    if (!desc->nccl_id) return bail(fail(HALP_INVALID_INPUT, "the NCCL route needs an ncclUniqueId"));
     if (!Nccl::get().load()) return bail(fail(HALP_NCCL_ERROR, "cannot load libnccl.so.2"));
     ncclUniqueId id;
     std::memcpy(&id, desc->nccl_id, sizeof id);
@@ -778,8 +793,41 @@ int halp_last_timing(const halp_problem* p, halp_timing* out) {
   return HALP_OK;
 }
 
+int halp_rank_partial(halp_problem* p, const double* w, double* root) {
+  if (!p || !w || !root) return fail(HALP_INVALID_INPUT, "halp_rank_partial: null argument");
+  CU(cudaSetDevice(p->device));
+  const int64_t D1 = p->D + 1;
+  const int nloc = (int)p->sp.local_splits();
+  CU(copy_sync(p->w, w, sizeof(double) * p->D, cudaMemcpyHostToDevice, p->stream));
+  for (int pass = 0; pass < p->fg_passes; ++pass) {
+    FgParams fp = fg_params(p, pass);
+    FgLaunch L = p->fg;
+    L.nsplit_local = nloc;
+    CU(launch_fullgrad(L, fp, p->stream));
+  }
+  CU(launch_split_tree(p->partials, nloc, (int)D1, p->rank_sum, p->tree_scratch, p->stream));
+  CU(copy_sync(root, p->rank_sum, sizeof(double) * D1, cudaMemcpyDeviceToHost, p->stream));
+  return HALP_OK;
+}
+
+int halp_finalize_gathered(halp_problem* p, const double* w, const double* gathered, double* g, double* loss) {
+  if (!p || !w || !gathered) return fail(HALP_INVALID_INPUT, "halp_finalize_gathered: null argument");
+  CU(cudaSetDevice(p->device));
+  const int64_t D1 = p->D + 1;
+  CU(copy_sync(p->w, w, sizeof(double) * p->D, cudaMemcpyHostToDevice, p->stream));
+  CU(copy_sync(p->gathered, gathered, sizeof(double) * D1 * p->world, cudaMemcpyHostToDevice, p->stream));
+  FinParams fin{p->gathered, p->world, p->D, p->w, p->n, p->l2, 1.0, 1e-300, 8, p->g, p->stats};
+  CU(launch_finalize(fin, p->stream));
+  double st[3];
+  CU(copy_sync(st, p->stats, sizeof st, cudaMemcpyDeviceToHost, p->stream));
+  if (g) CU(copy_sync(g, p->g, sizeof(double) * p->D, cudaMemcpyDeviceToHost, p->stream));
+  if (loss) *loss = st[2];
+  return HALP_OK;
+}
+
 int halp_full_gradient(halp_problem* p, const double* w, double* g, double* loss) {
   if (!p || !w) return fail(HALP_INVALID_INPUT, "halp_full_gradient: null argument");
+  if (p->host_exchange) return fail(HALP_INVALID_INPUT, "host-exchange problem: use halp_rank_partial / halp_finalize_gathered");
   CU(cudaSetDevice(p->device));
   p->timing = halp_timing{};
   CU(copy_sync(p->w, w, sizeof(double) * p->D, cudaMemcpyHostToDevice, p->stream));
@@ -792,7 +840,7 @@ int halp_full_gradient(halp_problem* p, const double* w, double* g, double* loss
 }
 
 int halp_bench_full_gradient(halp_problem* p, int reps, double* ms_per_pass) {
-  if (!p || reps < 1) return fail(HALP_INVALID_INPUT, "halp_bench_full_gradient: bad arguments");
+  if (!p || reps < 1 || p->host_exchange) return fail(HALP_INVALID_INPUT, "halp_bench_full_gradient: bad arguments");
   CU(cudaSetDevice(p->device));
   const int64_t D1 = p->D + 1;
   const int nloc = (int)p->sp.local_splits();
@@ -807,7 +855,12 @@ int halp_bench_full_gradient(halp_problem* p, int reps, double* ms_per_pass) {
       L.nsplit_local = nloc;
       CU(launch_fullgrad(L, fp, p->stream));
     }
-    CU(launch_split_tree(p->partials, nloc, (int)D1, p->rank_sum, p->tree_scratch, p->stream));
+    CU(launch_split_tree(p->partials, nloc, (int)D1, p->comm ? p->rank_sum : p->gathered, p->tree_scratch,
+                         p->stream));
+    if (p->comm) {  // the exchange step is part of a sharded pass
+      int rc = gather_finalize(p, 1.0, 8, 1e-300);
+      if (rc) return rc;
+    }
   }
   CU(cudaEventRecord(b, p->stream));
   CU(cudaEventSynchronize(b));
@@ -824,6 +877,7 @@ int halp_run(halp_problem* p, const halp_config* cfg, halp_record* rec) {
   // run_lp_svrg (:336-385): one epoch loop, K1 + K2 at the boundary, K4 + K3
   // inside; the three differ in the K3 mode and in how z / the scale start.
   if (!p || !cfg || !rec) return fail(HALP_INVALID_INPUT, "halp_run: null argument");
+  if (p->host_exchange) return fail(HALP_INVALID_INPUT, "host-exchange problem: use halp_rank_partial / halp_finalize_gathered");
   int rc = validate(p, cfg);
   if (rc) return rc;
   CU(cudaSetDevice(p->device));

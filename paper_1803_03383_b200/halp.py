@@ -146,10 +146,16 @@ def _x_dtype(X) -> int:
 
 
 class Objective:
-    """lpopt::Objective (objectives.hpp:59-91) backed by a device problem."""
+    """lpopt::Objective (objectives.hpp:59-91) backed by a device problem.
+
+    world_size / rank / nccl_id: multi-GPU problem (row-sharded full gradient,
+    one NCCL all-gather per epoch).  collective=True runs that NCCL route even
+    at world_size 1 (nccl_id required), so it can be exercised on one GPU;
+    collective="host" leaves the exchange to the caller (rank_partial /
+    finalize_gathered: the rank plumbing of G ranks checked on one GPU)."""
 
     def __init__(self, ds: Dataset, loss: LossFamily = LossFamily.Squared, l2: float = 0.0, device: int = 0,
-                 world_size: int = 1, rank: int = 0, nccl_id: Optional[bytes] = None):
+                 world_size: int = 1, rank: int = 0, nccl_id: Optional[bytes] = None, collective=False):
         self.ds = ds
         self._loss = LossFamily(loss)
         self._l2 = float(l2)
@@ -208,7 +214,8 @@ class Objective:
             idbuf = C.create_string_buffer(bytes(nccl_id), 128)
         desc = A.ProblemDesc(xptr, dtype, A.MEM_DEVICE if dev else A.MEM_HOST, int(X.shape[0]), int(X.shape[1]),
                              int(self._loss), C_, yptr, lptr, self._l2, device, world_size, rank,
-                             C.cast(idbuf, C.c_void_p) if idbuf is not None else None)
+                             C.cast(idbuf, C.c_void_p) if idbuf is not None else None,
+                             2 if collective == "host" else 1 if collective else 0)
         h = C.c_void_p()
         rc = A.lib().halp_problem_create(C.byref(desc), C.byref(h))
         if rc:
@@ -269,6 +276,26 @@ class Objective:
         if np.asarray(w).size != self.dim():
             raise InvalidInputError("loss: parameter length mismatch")
         return self._fullpass(w)[1]
+
+    def rank_partial(self, w) -> np.ndarray:
+        """this rank's subtree root of the sharded full gradient (D+1: gradient sums, loss sum)"""
+        w = np.ascontiguousarray(w, dtype=np.float64)
+        out = np.empty(self.dim() + 1, dtype=np.float64)
+        rc = A.lib().halp_rank_partial(self._h, w.ctypes.data, out.ctypes.data)
+        if rc:
+            _raise(rc)
+        return out
+
+    def finalize_gathered(self, w, gathered):
+        """(g, loss) from the all ranks' roots [world][D+1] (the exchange step's consumer)"""
+        w = np.ascontiguousarray(w, dtype=np.float64)
+        gat = np.ascontiguousarray(gathered, dtype=np.float64)
+        g = np.empty(self.dim(), dtype=np.float64)
+        loss = C.c_double()
+        rc = A.lib().halp_finalize_gathered(self._h, w.ctypes.data, gat.ctypes.data, g.ctypes.data, C.byref(loss))
+        if rc:
+            _raise(rc)
+        return g, loss.value
 
     def plan(self) -> dict:
         pl = A.Plan()

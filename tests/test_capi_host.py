@@ -29,7 +29,7 @@ def test_exports_every_declared_symbol(H):
     L = _capi.lib()
     for s in declared:
         assert getattr(L, s) is not None
-    assert L.halp_abi_version() == 3
+    assert L.halp_abi_version() == 4
 
 
 def test_no_cpu_fallback(H):

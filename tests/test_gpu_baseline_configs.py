@@ -49,11 +49,18 @@ def rows_equal(grows, orows):
 
 
 def rows_close(grows, orows, tol=1e-9):
+    """loss to tol relative; gradient norm and delta (= gn / (mu span)) to tol
+    relative to max(|value|, its first-row value): near the optimum the full
+    gradient is a sum of cancelling terms whose rounding error scales with the
+    terms, not with the (tiny) result -- REF and MIRROR sum in different
+    orders (a C5 problem at gn ~ 1e-7 from gn_0 ~ 10 differs by 3e-13 gn_0)."""
     assert len(grows) == len(orows)
     for a, b in zip(grows, orows):
-        for f in ("loss", "grad_norm", "delta"):
+        va, vb = a.loss, b["loss"]
+        assert abs(va - vb) <= tol * abs(vb), ("loss", a, b)
+        for f in ("grad_norm", "delta"):
             va, vb = getattr(a, f), b[f]
-            assert abs(va - vb) <= tol * abs(vb), (f, a, b)
+            assert abs(va - vb) <= tol * max(abs(vb), abs(orows[0][f])), (f, a, b)
 
 
 def mismatch_counts(ref_hash, mir_hash, T, K):
@@ -197,8 +204,9 @@ def test_c5_problems(H, oracle):
         rows_equal(recs[q].rows, mir.rows)
         assert np.array_equal(recs[q].final_iterate, mir.final_iterate), q
         assert recs[q].status == mir.status == "ok"
-        counts = mismatch_counts(ref.step_hash, mir.step_hash, T, K)
-        all_counts.append(counts)
-        rows_close(recs[q].rows, ref.rows)
-    log_counts("C5 (8 problems)", T=T, K=K, D=d, mismatched_steps_per_epoch=all_counts)
+        all_counts.append(mismatch_counts(ref.step_hash, mir.step_hash, T, K))
+    log_counts("C5 (8 problems)", T=T, K=K, D=d, mismatched_steps_per_epoch=all_counts,
+               loss_first_last=[[r.rows[0].loss, r.rows[-1].loss] for r in recs])
     assert all(c == [0] * K for c in all_counts)
+    for q, (mir, ref) in enumerate(res):
+        rows_close(recs[q].rows, ref.rows)
