@@ -234,6 +234,15 @@ int halp_shard_plan(int64_t n, int32_t d, int32_t C, int32_t dtype, int32_t worl
  * this shape (what halp_problem_plan reports after creation). */
 int halp_plan_for(int64_t n, int32_t d, int32_t C, int32_t dtype, int32_t world, int32_t rank, halp_plan* out);
 
+/* ---- the reference's own dataset generators (host, CPU-callable) ----
+ * make_regression (objectives.cpp:27-45): X [n][d] row-major fp64, y [n] */
+int halp_make_regression(int64_t n, int32_t d, double noise_sd, uint64_t seed, double* X, double* y);
+/* make_classification (objectives.cpp:46-76): X [n][d], labels [n] */
+int halp_make_classification(int64_t n, int32_t d, int32_t num_classes, double separation, uint64_t seed,
+                             double* X, int32_t* labels);
+/* `count` successive QuantRng(seed, stream).next_normal() draws (rng.hpp:57-62) */
+int halp_normals(uint64_t seed, uint64_t stream, int64_t count, double* out);
+
 /* xorshift64* stream state after `count` draws of (seed, stream) computed
  * by GF(2) jump-ahead (host), for tests of the counter-indexed RNG. */
 uint64_t halp_rng_state_after(uint64_t seed, uint64_t stream, uint64_t count);

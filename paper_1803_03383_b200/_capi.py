@@ -84,6 +84,7 @@ SYMBOLS = [
     "halp_run", "halp_full_gradient", "halp_set_trace", "halp_last_timing", "halp_bench_full_gradient",
     "halp_batch_create", "halp_batch_destroy", "halp_batch_run", "halp_datagen", "halp_shard_plan",
     "halp_rng_state_after", "halp_plan_for", "halp_batch_plan", "halp_rank_partial", "halp_finalize_gathered",
+    "halp_make_regression", "halp_make_classification", "halp_normals",
 ]
 
 _lib = None
@@ -120,6 +121,10 @@ def lib():
     L.halp_plan_for.argtypes = [C.c_int64, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.POINTER(Plan)]
     L.halp_rank_partial.argtypes = [P, C.c_void_p, C.c_void_p]
     L.halp_finalize_gathered.argtypes = [P, C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(C.c_double)]
+    L.halp_make_regression.argtypes = [C.c_int64, C.c_int32, C.c_double, C.c_uint64, C.c_void_p, C.c_void_p]
+    L.halp_make_classification.argtypes = [C.c_int64, C.c_int32, C.c_int32, C.c_double, C.c_uint64, C.c_void_p,
+                                           C.c_void_p]
+    L.halp_normals.argtypes = [C.c_uint64, C.c_uint64, C.c_int64, C.c_void_p]
     L.halp_rng_state_after.restype = C.c_uint64
     L.halp_rng_state_after.argtypes = [C.c_uint64, C.c_uint64, C.c_uint64]
     _lib = L

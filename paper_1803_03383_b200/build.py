@@ -26,7 +26,7 @@ CUDA = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 NVCC = os.path.join(CUDA, "bin", "nvcc")
 
 CU_SOURCES = ["k_fullgrad.cu", "k_fullgrad_smx.cu", "k_fullgrad_stream.cu", "k_inner.cu", "k_batch.cu", "k_datagen.cu"]
-CXX_SOURCES = ["halp_capi.cpp"]
+CXX_SOURCES = ["halp_capi.cpp", "halp_datasets.cpp"]
 HEADERS = ["halp_device.cuh", "kernels.h", "rng_jump.hpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-fmad=false", "-std=c++17", "-Xcompiler", "-fPIC",

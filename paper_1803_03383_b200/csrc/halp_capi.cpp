@@ -1069,12 +1069,17 @@ struct halp_batch {
   double l2 = 0.0;
   void* X = nullptr;
   double* y = nullptr;
-  uint64_t *pow_tab = nullptr, *jump_tab = nullptr;
+  const uint64_t *pow_tab = nullptr, *jump_tab = nullptr;  // resident per device (rng_tables)
   cudaStream_t stream = nullptr;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  void* arena = nullptr;  // per-run parameters + outputs (one pooled block, reused across runs)
+  size_t arena_bytes = 0;
   ~halp_batch() {
     cudaSetDevice(device);
-    for (void* q : {(void*)X, (void*)y, (void*)pow_tab, (void*)jump_tab})
-      if (q) cudaFree(q);
+    for (void* q : {(void*)X, (void*)y, arena})
+      if (q) cudaFreeAsync(q, stream);
+    if (e0) cudaEventDestroy(e0);
+    if (e1) cudaEventDestroy(e1);
     if (stream) cudaStreamDestroy(stream);
   }
 };
@@ -1090,7 +1095,9 @@ extern "C" int halp_batch_create(const halp_batch_desc* desc, halp_batch** out) 
   int ndev = 0;
   cudaError_t ce = cudaGetDeviceCount(&ndev);
   if (ce != cudaSuccess || ndev == 0) return fail(HALP_CUDA_ERROR, "no CUDA device (no CPU fallback)");
+  if (desc->device < 0 || desc->device >= ndev) return fail(HALP_INVALID_INPUT, "device index out of range");
   CU(cudaSetDevice(desc->device));
+  if (pool_setup(desc->device)) return fail(HALP_CUDA_ERROR, "cannot configure the device memory pool");
   auto* b = new halp_batch();
   b->device = desc->device;
   b->dtype = desc->dtype;
@@ -1110,25 +1117,24 @@ extern "C" int halp_batch_create(const halp_batch_desc* desc, halp_batch** out) 
   const size_t rows_total = (size_t)(b->shared ? 1 : b->nprob) * b->n;
   if (cudaStreamCreateWithFlags(&b->stream, cudaStreamNonBlocking) != cudaSuccess)
     return bail(fail(HALP_CUDA_ERROR, "cudaStreamCreate failed"));
-  if (cudaMalloc(&b->X, rows_total * b->ld * es) != cudaSuccess) return bail(fail(HALP_CUDA_ERROR, "cudaMalloc(X)"));
-  if (b->ld != b->d && cudaMemset(b->X, 0, rows_total * b->ld * es) != cudaSuccess)
+  if (cudaEventCreate(&b->e0) != cudaSuccess || cudaEventCreate(&b->e1) != cudaSuccess)
+    return bail(fail(HALP_CUDA_ERROR, "cudaEventCreate failed"));
+  cudaStream_t st = b->stream;
+  // everything on the batch's own stream (stream-ordered pool, async copies), one sync at the end
+  if (dalloc(&b->X, rows_total * b->ld * es, st) != cudaSuccess) return bail(fail(HALP_CUDA_ERROR, "cudaMallocAsync(X)"));
+  if (b->ld != b->d && cudaMemsetAsync(b->X, 0, rows_total * b->ld * es, st) != cudaSuccess)
     return bail(fail(HALP_CUDA_ERROR, "cudaMemset(X)"));
-  if (cudaMemcpy2D(b->X, (size_t)b->ld * es, desc->X, (size_t)b->d * es, (size_t)b->d * es, rows_total,
-                   dev_in ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice) != cudaSuccess)
+  if (cudaMemcpy2DAsync(b->X, (size_t)b->ld * es, desc->X, (size_t)b->d * es, (size_t)b->d * es, rows_total,
+                        dev_in ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st) != cudaSuccess)
     return bail(fail(HALP_CUDA_ERROR, "copy of X failed"));
-  if (cudaMalloc(&b->y, sizeof(double) * rows_total) != cudaSuccess) return bail(fail(HALP_CUDA_ERROR, "cudaMalloc(y)"));
-  if (cudaMemcpy(b->y, desc->y, sizeof(double) * rows_total, dev_in ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice) !=
-      cudaSuccess)
+  if (dalloc(&b->y, sizeof(double) * rows_total, st) != cudaSuccess) return bail(fail(HALP_CUDA_ERROR, "cudaMallocAsync(y)"));
+  if (cudaMemcpyAsync(b->y, desc->y, sizeof(double) * rows_total,
+                      dev_in ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st) != cudaSuccess)
     return bail(fail(HALP_CUDA_ERROR, "copy of y failed"));
-  const auto& jt = JumpTables::get();
-  if (cudaMalloc(&b->pow_tab, sizeof(uint64_t) * jt.flat.size()) != cudaSuccess ||
-      cudaMemcpy(b->pow_tab, jt.flat.data(), sizeof(uint64_t) * jt.flat.size(), cudaMemcpyHostToDevice) != cudaSuccess)
-    return bail(fail(HALP_CUDA_ERROR, "RNG tables"));
-  std::vector<uint64_t> tab(2048);
-  mat_tables(jt.power((uint64_t)b->d), tab.data());
-  if (cudaMalloc(&b->jump_tab, sizeof(uint64_t) * 2048) != cudaSuccess ||
-      cudaMemcpy(b->jump_tab, tab.data(), sizeof(uint64_t) * 2048, cudaMemcpyHostToDevice) != cudaSuccess)
-    return bail(fail(HALP_CUDA_ERROR, "RNG tables"));
+  int rc = rng_tables(b->device, b->d, &b->pow_tab, &b->jump_tab, st);
+  if (rc) return bail(rc);
+  // the caller may release its buffers when create returns
+  if (cudaStreamSynchronize(st) != cudaSuccess) return bail(fail(HALP_CUDA_ERROR, "upload of the batch failed"));
   *out = b;
   return HALP_OK;
 }
@@ -1142,9 +1148,8 @@ extern "C" int halp_batch_plan(const halp_batch* b, halp_plan* out) {
   out->fg_vec = 16 / elem_size(b->dtype);
   out->fg_splits = b->splits;
   out->in_ctas = 1;
-  out->in_threads = 32;
-  const int M = (b->d + 31) / 32;
-  out->in_per = M <= 1 ? 1 : M <= 2 ? 2 : M <= 4 ? 4 : 8;
+  out->in_threads = 128;  // k5_batch: 4 warps per problem, M = D/128 coordinates per thread
+  out->in_per = b->d <= 128 ? 1 : 2;
   out->in_levels = 1;
   out->fg_split_begin = 0;
   out->fg_split_end = b->splits;
@@ -1187,15 +1192,43 @@ extern "C" int halp_batch_run(halp_batch* b, const halp_config* cfgs, halp_recor
     }
     max_rows = std::max(max_rows, std::max(c.epochs, 0) + 2);
   }
-  // one device arena for the parameters and the outputs
-  std::vector<void*> bufs;
-  auto dev = [&](const void* src, size_t bytes) -> void* {
-    void* p = nullptr;
-    if (cudaMalloc(&p, std::max<size_t>(bytes, 8)) != cudaSuccess) return nullptr;
-    bufs.push_back(p);
-    if (src) cudaMemcpyAsync(p, src, bytes, cudaMemcpyHostToDevice, b->stream);
-    return p;
+  // one pooled device arena for the per-problem parameters and the outputs
+  // (kept by the batch and reused by the next run of the same or smaller size)
+  struct Part {
+    const void* src;
+    size_t bytes;
+    size_t off;
   };
+  std::vector<Part> parts;
+  size_t total = 0;
+  auto part = [&](const void* src, size_t bytes) -> size_t {
+    const size_t off = total;
+    parts.push_back(Part{src, bytes, off});
+    total += (std::max<size_t>(bytes, 8) + 255) / 256 * 256;
+    return off;
+  };
+  const size_t o_alpha = part(alpha.data(), 8 * P), o_mu = part(mu.data(), 8 * P), o_dmin = part(dmin.data(), 8 * P),
+               o_divl = part(divl.data(), 8 * P), o_mev = part(mev.data(), 8 * P), o_bits = part(bits.data(), 4 * P),
+               o_ep = part(epochs.data(), 4 * P), o_opt = part(option.data(), 4 * P), o_T = part(T.data(), 8 * P),
+               o_seed = part(seeds.data(), 16 * (size_t)P),
+               o_init = part(any_init ? init.data() : nullptr, any_init ? 8 * (size_t)P * D : 0);
+  const size_t in_bytes = total;
+  const size_t o_rows = part(nullptr, 8 * 5 * (size_t)P * max_rows), o_rh = part(nullptr, 8 * (size_t)P * max_rows),
+               o_rn = part(nullptr, 4 * (size_t)P), o_st = part(nullptr, 4 * (size_t)P), o_stp = part(nullptr, 8 * (size_t)P),
+               o_w = part(nullptr, 8 * (size_t)P * D);
+  if (total > b->arena_bytes) {
+    if (b->arena) CU(cudaFreeAsync(b->arena, b->stream));
+    b->arena = nullptr;
+    CU(dalloc(&b->arena, total, b->stream));
+    b->arena_bytes = total;
+  }
+  char* A = static_cast<char*>(b->arena);
+  {  // the inputs as one pinned-free staging copy
+    std::vector<char> stage(in_bytes);
+    for (const Part& q : parts)
+      if (q.src && q.off < in_bytes) std::memcpy(stage.data() + q.off, q.src, q.bytes);
+    CU(copy_sync(A, stage.data(), in_bytes, cudaMemcpyHostToDevice, b->stream));
+  }
   BatchParams bp{};
   bp.X = b->X;
   bp.ld = b->ld;
@@ -1206,61 +1239,47 @@ extern "C" int halp_batch_run(halp_batch* b, const halp_config* cfgs, halp_recor
   bp.x_rows_per_prob = b->shared ? 0 : b->n;
   bp.y = b->y;
   bp.l2 = b->l2;
-  bp.alpha = (const double*)dev(alpha.data(), 8 * P);
-  bp.mu = (const double*)dev(mu.data(), 8 * P);
-  bp.delta_min = (const double*)dev(dmin.data(), 8 * P);
-  bp.div_limit = (const double*)dev(divl.data(), 8 * P);
-  bp.metric_every = (const double*)dev(mev.data(), 8 * P);
-  bp.bits = (const int*)dev(bits.data(), 4 * P);
-  bp.epochs = (const int*)dev(epochs.data(), 4 * P);
-  bp.option = (const int*)dev(option.data(), 4 * P);
-  bp.T = (const int64_t*)dev(T.data(), 8 * P);
-  bp.seed = (const uint64_t*)dev(seeds.data(), 16 * P);
-  bp.init = any_init ? (const double*)dev(init.data(), 8 * (size_t)P * D) : nullptr;
+  bp.alpha = (const double*)(A + o_alpha);
+  bp.mu = (const double*)(A + o_mu);
+  bp.delta_min = (const double*)(A + o_dmin);
+  bp.div_limit = (const double*)(A + o_divl);
+  bp.metric_every = (const double*)(A + o_mev);
+  bp.bits = (const int*)(A + o_bits);
+  bp.epochs = (const int*)(A + o_ep);
+  bp.option = (const int*)(A + o_opt);
+  bp.T = (const int64_t*)(A + o_T);
+  bp.seed = (const uint64_t*)(A + o_seed);
+  bp.init = any_init ? (const double*)(A + o_init) : nullptr;
   bp.pow_tab = b->pow_tab;
   bp.jump_tab = b->jump_tab;
   bp.splits = b->splits;
   bp.max_rows = max_rows;
-  bp.rows = (double*)dev(nullptr, 8 * 5 * (size_t)P * max_rows);
-  bp.rhash = (uint64_t*)dev(nullptr, 8 * (size_t)P * max_rows);
-  bp.rows_n = (int*)dev(nullptr, 4 * P);
-  bp.status = (int*)dev(nullptr, 4 * P);
-  bp.steps = (int64_t*)dev(nullptr, 8 * P);
-  bp.w_out = (double*)dev(nullptr, 8 * (size_t)P * D);
-  auto cleanup = [&]() {
-    for (void* q : bufs) cudaFree(q);
-  };
-  for (void* q : bufs)
-    if (!q) {
-      cleanup();
-      return fail(HALP_CUDA_ERROR, "halp_batch_run: cudaMalloc failed");
-    }
-  cudaEvent_t e0, e1;
-  CU(cudaEventCreate(&e0));
-  CU(cudaEventCreate(&e1));
-  CU(cudaEventRecord(e0, b->stream));
-  cudaError_t le = launch_batch(bp, 128, b->stream);
-  CU(cudaEventRecord(e1, b->stream));
-  if (le != cudaSuccess) {
-    cleanup();
-    return fail(HALP_CUDA_ERROR, std::string("launch_batch: ") + cudaGetErrorString(le));
-  }
+  bp.rows = (double*)(A + o_rows);
+  bp.rhash = (uint64_t*)(A + o_rh);
+  bp.rows_n = (int*)(A + o_rn);
+  bp.status = (int*)(A + o_st);
+  bp.steps = (int64_t*)(A + o_stp);
+  bp.w_out = (double*)(A + o_w);
+  CU(cudaEventRecord(b->e0, b->stream));
+  CU(launch_batch(bp, 128, b->stream));
+  CU(cudaEventRecord(b->e1, b->stream));
   std::vector<double> rows(5 * (size_t)P * max_rows), wout((size_t)P * D);
   std::vector<uint64_t> rh((size_t)P * max_rows);
   std::vector<int> rn(P), st(P);
   std::vector<int64_t> stp(P);
-  CU(cudaMemcpyAsync(rows.data(), bp.rows, rows.size() * 8, cudaMemcpyDeviceToHost, b->stream));
-  CU(cudaMemcpyAsync(rh.data(), bp.rhash, rh.size() * 8, cudaMemcpyDeviceToHost, b->stream));
-  CU(cudaMemcpyAsync(rn.data(), bp.rows_n, 4 * P, cudaMemcpyDeviceToHost, b->stream));
-  CU(cudaMemcpyAsync(st.data(), bp.status, 4 * P, cudaMemcpyDeviceToHost, b->stream));
-  CU(cudaMemcpyAsync(stp.data(), bp.steps, 8 * P, cudaMemcpyDeviceToHost, b->stream));
-  CU(cudaMemcpyAsync(wout.data(), bp.w_out, wout.size() * 8, cudaMemcpyDeviceToHost, b->stream));
-  CU(cudaStreamSynchronize(b->stream));
+  {  // the outputs: one copy of the arena's output region
+    std::vector<char> res(total - in_bytes);
+    CU(copy_sync(res.data(), A + in_bytes, res.size(), cudaMemcpyDeviceToHost, b->stream));
+    auto R = [&](size_t off) { return res.data() + (off - in_bytes); };
+    std::memcpy(rows.data(), R(o_rows), rows.size() * 8);
+    std::memcpy(rh.data(), R(o_rh), rh.size() * 8);
+    std::memcpy(rn.data(), R(o_rn), 4 * (size_t)P);
+    std::memcpy(st.data(), R(o_st), 4 * (size_t)P);
+    std::memcpy(stp.data(), R(o_stp), 8 * (size_t)P);
+    std::memcpy(wout.data(), R(o_w), wout.size() * 8);
+  }
   float ms = 0;
-  cudaEventElapsedTime(&ms, e0, e1);
-  cudaEventDestroy(e0);
-  cudaEventDestroy(e1);
-  cleanup();
+  CU(cudaEventElapsedTime(&ms, b->e0, b->e1));
   if (device_ms) *device_ms = ms;
   int invalid = -1;
   for (int q = 0; q < P; ++q) {

@@ -17,14 +17,26 @@
 //     l, l+32, ... (K1 with fg_threads = 32, which is what the plan picks
 //     for d <= 128 fp32); gradient column = sequential fma over the split's rows.
 //   * finalize: k_finalize's 256-strided order for |g| and |w|.
-//   * inner loop: K3 with one CTA of one warp, M = D/32 coordinates per lane.
+//   * inner loop: K3's single-CTA order (KIND 0) with 128 threads, M = D/128
+//     coordinates per thread: thread partial, warp reduce-scatter butterfly,
+//     the 4 warp records combined by every warp (lane l reads warp l, lane
+//     butterfly) -- halp_batch_plan reports {1 CTA, 128 threads, M}.
 // Squared loss only (the C5 / sweep workloads); d*C <= 256.
+//
+// Inner-loop latency (the whole cost of a problem, one chain per step):
+//   * the sample stream does not depend on the iterate, so every thread runs
+//     it kP steps ahead and keeps the sampled rows (its M features + y) in a
+//     register ring: the HBM round trip of a row is off the serial chain;
+//   * all four warps work: one exchange through shared memory + one barrier
+//     per step (the blow-up flag of the previous step rides in the record);
+//   * the X^D jump table of the rounding stream lives in shared memory.
 #include "halp_device.cuh"
 #include "kernels.h"
 
 namespace halp {
 
-constexpr int kBatchMaxM = 8;     // D <= 256
+constexpr int kBatchMaxM = 2;     // D <= 256 over 128 threads
+constexpr int kP = 4;             // sample-row prefetch distance (steps)
 constexpr int kBatchMaxLev = 16;  // splits per warp <= 2^15
 
 template <class Tx> struct BVec;
@@ -53,6 +65,13 @@ __device__ __forceinline__ void load_group_g(const Tx* p, double* out) {
   }
 }
 
+template <class Tx>
+__device__ __forceinline__ Tx zero_raw() {
+  Tx z;
+  memset(&z, 0, sizeof z);
+  return z;
+}
+
 __device__ __forceinline__ uint64_t fnv1a_doubles(const double* v, int len) {
   uint64_t h = 1469598103934665603ULL;
   for (int k = 0; k < len; ++k) {
@@ -68,7 +87,7 @@ __device__ __forceinline__ uint64_t fnv1a_doubles(const double* v, int len) {
 
 // NG groups of V features per lane (NG*V*32 >= d)
 template <class Tx, int NG, int M>
-__global__ void __launch_bounds__(128, (M <= 4) ? 4 : 1) k5_batch(BatchParams p) {
+__global__ void __launch_bounds__(128, 4) k5_batch(BatchParams p) {
   constexpr int V = BVec<Tx>::V;
   const int prob = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -82,6 +101,8 @@ __global__ void __launch_bounds__(128, (M <= 4) ? 4 : 1) k5_batch(BatchParams p)
   __shared__ double w_s[264], g_s[264], wsum[4][257];  // iterate, g~, warp subtree roots (+loss)
   __shared__ double stats[4];
   __shared__ int sh_stop, sh_blew;
+  __shared__ uint64_t jt[2048];                 // X^D jump table of the rounding stream
+  __shared__ __align__(32) double rec[2][4][4];  // [parity][warp]: a-sum, b-sum, blow-up flag of step t-1
 
   const double alpha = p.alpha[prob], mu = p.mu[prob], dmin = p.delta_min[prob], divl = p.div_limit[prob];
   const int bits = p.bits[prob], epochs = p.epochs[prob], opt2 = p.option[prob];
@@ -105,9 +126,9 @@ __global__ void __launch_bounds__(128, (M <= 4) ? 4 : 1) k5_batch(BatchParams p)
 
   // RNG states (seeding as rng.hpp:29-32, done on the host: p.seed holds the
   // stream-0 / stream-1 initial states interleaved)
-  uint64_t s_sample = p.seed[2 * prob];   // stream 0 state (lane-uniform)
+  uint64_t s_sample = p.seed[2 * prob];   // stream 0 state (thread-uniform)
   const uint64_t s_round0 = p.seed[2 * prob + 1];
-  const uint64_t* jtD = p.jump_tab;       // X^D table (global, read-only)
+  for (int i = tid; i < 2048; i += 128) jt[i] = p.jump_tab[i];
 
   int nrow = 0;
   int status = 0;  // 0 ok, 1 converged, 2 diverged
@@ -229,14 +250,15 @@ __global__ void __launch_bounds__(128, (M <= 4) ? 4 : 1) k5_batch(BatchParams p)
     __syncthreads();
   };
 
-  // inner-loop state (warp 0): lane l owns coordinates [l*M, l*M + M)
-  double wt[M], gtl[M], code[M], snap[M], up[M];
+  // inner-loop state: thread tid owns coordinates [tid*M, tid*M + M)
+  double wt[M], gtl[M], l2w[M], code[M], snap[M], up[M];
   bool valid[M];
-  const int k0 = lane * M;
+  const int k0 = tid * M;
 #pragma unroll
   for (int i = 0; i < M; ++i) valid[i] = (k0 + i) < D;
-  uint64_t rs = 0;
-  if (wid == 0) rs = jump_count(s_round0, (uint64_t)(D + k0), p.pow_tab);  // after Q(0) of epoch 0
+  const bool vecx = (M * sizeof(Tx) == 8 || M * sizeof(Tx) == 16) && (ld % M == 0);
+  // rounding stream after Q(0) of epoch 0, at this thread's first draw
+  uint64_t rs = jump_count(s_round0, (uint64_t)(D + k0), p.pow_tab);
 
   bool converged = false;
   for (int k = 0; k < epochs && !converged; ++k) {
@@ -260,33 +282,67 @@ __global__ void __launch_bounds__(128, (M <= 4) ? 4 : 1) k5_batch(BatchParams p)
       converged = sh_stop == 1;
       break;
     }
-    if (wid == 0) {
-      const double rcp = 1.0 / delta;
-      const bool use_rcp = isfinite(rcp) && rcp != 0.0;
+    const double rcp = 1.0 / delta;
+    const bool fast_q = isfinite(rcp) && rcp != 0.0 && !wide;
 #pragma unroll
-      for (int i = 0; i < M; ++i) {
-        wt[i] = valid[i] ? w_s[k0 + i] : 0.0;
-        gtl[i] = valid[i] ? g_s[k0 + i] : 0.0;
-        code[i] = 0.0;
-        snap[i] = 0.0;
-        up[i] = 0.0;
+    for (int i = 0; i < M; ++i) {
+      wt[i] = valid[i] ? w_s[k0 + i] : 0.0;
+      gtl[i] = valid[i] ? g_s[k0 + i] : 0.0;
+      l2w[i] = __dmul_rn(l2, wt[i]);
+      code[i] = 0.0;
+      snap[i] = 0.0;
+      up[i] = 0.0;
+    }
+    int64_t t_pick = -1;
+    if (opt2) {
+      s_sample = xs_step(s_sample);
+      t_pick = (int64_t)index_of(s_sample, (uint64_t)T);
+    }
+    // sample-row ring: slot j holds the row of steps j, j + kP, ... (raw x + y)
+    Tx xr[kP][M];
+    double yr[kP];
+    auto issue = [&](Tx (&dst)[M], double& ydst) {
+      s_sample = xs_step(s_sample);
+      const int64_t row = (int64_t)index_of(s_sample, (uint64_t)n);
+      const Tx* xp = X + row * ld + k0;
+      if (vecx && M > 1) {
+        if constexpr (M * sizeof(Tx) == 16) {
+          const uint4 r = __ldg(reinterpret_cast<const uint4*>(xp));
+          const Tx* q = reinterpret_cast<const Tx*>(&r);
+#pragma unroll
+          for (int i = 0; i < M; ++i) dst[i] = q[i];
+        } else if constexpr (M * sizeof(Tx) == 8) {
+          const uint2 r = __ldg(reinterpret_cast<const uint2*>(xp));
+          const Tx* q = reinterpret_cast<const Tx*>(&r);
+#pragma unroll
+          for (int i = 0; i < M; ++i) dst[i] = q[i];
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < M; ++i) dst[i] = valid[i] ? __ldg(xp + i) : zero_raw<Tx>();
       }
-      int64_t t_pick = -1;
-      if (opt2) {
-        s_sample = xs_step(s_sample);
-        t_pick = (int64_t)index_of(s_sample, (uint64_t)T);
-      }
-      int blow = -1;
-      for (int64_t t = 0; t < T; ++t) {
+      ydst = __ldg(y + row);
+    };
+#pragma unroll
+    for (int j = 0; j < kP; ++j)
+      if (j < T) issue(xr[j], yr[j]);
+    int bad_prev = 0;
+    int64_t blow = -1;
+    for (int64_t t0 = 0; t0 < T && blow < 0; t0 += kP) {
+#pragma unroll
+      for (int j = 0; j < kP; ++j) {
+        const int64_t t = t0 + j;
+        if (t >= T) break;
+        const int par = (int)(t & 1);
+        double xc[M];
+#pragma unroll
+        for (int i = 0; i < M; ++i) xc[i] = to_d<Tx>(xr[j][i]);
+        const double yi = yr[j];
+        if (t + kP < T) issue(xr[j], yr[j]);  // the row of step t + kP
         if (t == t_pick) {
 #pragma unroll
           for (int i = 0; i < M; ++i) snap[i] = code[i];
         }
-        s_sample = xs_step(s_sample);
-        const int64_t row = (int64_t)index_of(s_sample, (uint64_t)n);
-        double xc[M];
-#pragma unroll
-        for (int i = 0; i < M; ++i) xc[i] = valid[i] ? to_d<Tx>(X[row * ld + k0 + i]) : 0.0;
         double a = 0.0, b = 0.0;
 #pragma unroll
         for (int i = 0; i < M; ++i) {
@@ -295,65 +351,97 @@ __global__ void __launch_bounds__(128, (M <= 4) ? 4 : 1) k5_batch(BatchParams p)
           a = fma(xc[i], wt[i] + z, a);
           b = fma(xc[i], wt[i], b);
         }
-        a = warp_allsum(a);
-        b = warp_allsum(b);
-        const double yi = y[row];
-        const double e1 = a - yi, e2 = b - yi;
+        // warp reduce-scatter: a on lanes 0..15, b on lanes 16..31 (K3 KIND 0)
+        const bool u16 = (lane & 16) != 0;
+        double v = (u16 ? b : a) + __shfl_xor_sync(0xffffffffu, u16 ? a : b, 16);
+        v = v + __shfl_xor_sync(0xffffffffu, v, 8);
+        v = v + __shfl_xor_sync(0xffffffffu, v, 4);
+        v = v + __shfl_xor_sync(0xffffffffu, v, 2);
+        v = v + __shfl_xor_sync(0xffffffffu, v, 1);
+        const double vp = __shfl_xor_sync(0xffffffffu, v, 16);
+        const int flag = __any_sync(0xffffffffu, bad_prev);
+        if (lane == 0)
+          *reinterpret_cast<double4*>(&rec[par][wid][0]) = make_double4(v, vp, flag ? 1.0 : 0.0, 0.0);
+        // rounding draws of this step, independent of the exchange
+        double U[M];
+        {
+          uint64_t sr = rs;
+#pragma unroll
+          for (int i = 0; i < M; ++i) {
+            sr = xs_step(sr);
+            U[i] = uniform_of(sr);
+          }
+          rs = jump_tab(rs, jt);
+        }
+        __syncthreads();
+        // lane l < 4 holds warp l's record; lane butterfly over the 4 records
+        double sa = 0.0, sb = 0.0, fl = 0.0;
+        if (lane < 4) {
+          const double4 r = *reinterpret_cast<const double4*>(&rec[par][lane][0]);
+          sa = sa + r.x;
+          sb = sb + r.y;
+          fl = r.z;
+        }
+        if (__any_sync(0xffffffffu, fl != 0.0)) {
+          blow = t - 1;  // step t-1's update was non-finite; up[] still holds it
+          break;
+        }
+        sa = sa + __shfl_xor_sync(0xffffffffu, sa, 2);
+        sb = sb + __shfl_xor_sync(0xffffffffu, sb, 2);
+        sa = sa + __shfl_xor_sync(0xffffffffu, sa, 1);
+        sb = sb + __shfl_xor_sync(0xffffffffu, sb, 1);
+        sa = __shfl_sync(0xffffffffu, sa, 0);
+        sb = __shfl_sync(0xffffffffu, sb, 0);
+        const double e1 = sa - yi, e2 = sb - yi;
         bool bad = false, slow_any = false;
         bool slow[M];
-        uint64_t s = rs;
 #pragma unroll
         for (int i = 0; i < M; ++i) {
-          s = xs_step(s);
-          const double U = uniform_of(s);
           const double z = __dmul_rn(code[i], delta);
           const double wz = wt[i] + z;
           const double g1 = __dmul_rn(e1, xc[i]) + __dmul_rn(l2, wz);
-          const double g2 = __dmul_rn(e2, xc[i]) + __dmul_rn(l2, wt[i]);
+          const double g2 = __dmul_rn(e2, xc[i]) + l2w[i];
           const double u = z - __dmul_rn(alpha, (g1 - g2) + gtl[i]);
           up[i] = u;
           bad |= valid[i] && !isfinite(u);
-          if (use_rcp && !wide) {
-            code[i] = quantize_fast(u, delta, rcp, hi, lo, U, slow[i]);
+          slow[i] = false;
+          if (fast_q) {
+            code[i] = quantize_fast(u, delta, rcp, hi, lo, U[i], slow[i]);
             slow_any |= valid[i] && slow[i];
           } else {
-            code[i] = (double)quantize_code(u, delta, hi, lo, maxc, minc, U);
+            code[i] = (double)quantize_code(u, delta, hi, lo, maxc, minc, U[i]);
           }
         }
         if (slow_any) {
-          s = rs;
 #pragma unroll
-          for (int i = 0; i < M; ++i) {
-            s = xs_step(s);
-            if (valid[i] && slow[i]) code[i] = (double)quantize_code(up[i], delta, hi, lo, maxc, minc, uniform_of(s));
-          }
+          for (int i = 0; i < M; ++i)
+            if (valid[i] && slow[i]) code[i] = (double)quantize_code(up[i], delta, hi, lo, maxc, minc, U[i]);
         }
-        rs = jump_tab(rs, jtD);
-        if (__any_sync(0xffffffffu, bad)) {
-          blow = (int)t;
-          break;
-        }
+        bad_prev = bad ? 1 : 0;
       }
-      if (blow >= 0) {
-        // Recorder::blowup: row (inf, inf, delta) hashed over u (optimizers.cpp:156-160)
+    }
+    // the last step's finiteness (no further exchange carries it)
+    if (blow < 0 && __syncthreads_or(bad_prev)) blow = T - 1;
+    if (blow >= 0) {
+      // Recorder::blowup: row (inf, inf, delta) hashed over u (optimizers.cpp:156-160)
+      __syncthreads();
 #pragma unroll
-        for (int i = 0; i < M; ++i)
-          if (valid[i]) g_s[k0 + i] = up[i];
-        __syncwarp();
-        if (lane == 0) {
-          boundary((double)(steps + blow + 1) / (double)n, g_s, INFINITY, INFINITY, delta, true);
-          status = 2;
-          sh_stop = 2;
-          sh_blew = 1;
-          for (int q = 0; q < D; ++q) p.w_out[(size_t)prob * D + q] = g_s[q];
-        }
-      } else {
-#pragma unroll
-        for (int i = 0; i < M; ++i)
-          if (valid[i]) w_s[k0 + i] = wt[i] + __dmul_rn(t_pick >= 0 ? snap[i] : code[i], delta);
-        // next epoch: skip its Q(0) draws
-        rs = jump_tab(rs, jtD);
+      for (int i = 0; i < M; ++i)
+        if (valid[i]) g_s[k0 + i] = up[i];
+      __syncthreads();
+      if (tid == 0) {
+        boundary((double)(steps + blow + 1) / (double)n, g_s, INFINITY, INFINITY, delta, true);
+        status = 2;
+        sh_stop = 2;
+        sh_blew = 1;
+        for (int q = 0; q < D; ++q) p.w_out[(size_t)prob * D + q] = g_s[q];
       }
+    } else {
+#pragma unroll
+      for (int i = 0; i < M; ++i)
+        if (valid[i]) w_s[k0 + i] = wt[i] + __dmul_rn(t_pick >= 0 ? snap[i] : code[i], delta);
+      // next epoch: skip its Q(0) draws
+      rs = jump_tab(rs, jt);
     }
     __syncthreads();
     if (sh_stop) break;
@@ -379,13 +467,8 @@ __global__ void __launch_bounds__(128, (M <= 4) ? 4 : 1) k5_batch(BatchParams p)
 
 template <class Tx, int NG>
 static cudaError_t launch_b_ng(const BatchParams& p, cudaStream_t st) {
-  const int M = (p.d + 31) / 32;
-  switch (M <= 1 ? 1 : M <= 2 ? 2 : M <= 4 ? 4 : 8) {
-    case 1: k5_batch<Tx, NG, 1><<<p.nprob, 128, 0, st>>>(p); break;
-    case 2: k5_batch<Tx, NG, 2><<<p.nprob, 128, 0, st>>>(p); break;
-    case 4: k5_batch<Tx, NG, 4><<<p.nprob, 128, 0, st>>>(p); break;
-    default: k5_batch<Tx, NG, 8><<<p.nprob, 128, 0, st>>>(p); break;
-  }
+  if (p.d <= 128) k5_batch<Tx, NG, 1><<<p.nprob, 128, 0, st>>>(p);
+  else k5_batch<Tx, NG, 2><<<p.nprob, 128, 0, st>>>(p);
   return cudaGetLastError();
 }
 
