@@ -11,4 +11,8 @@ from .halp import (  # noqa: F401
     oracle_plan_for, plan_for, resolve_inner_steps, rng_state_after, run, run_halp, run_lp_sgd, run_lp_svrg, run_prepared, run_sgd, run_svrg,
     shard_plan,
 )
-from . import theory  # noqa: F401,E402
+from . import harness  # noqa: F401,E402
+from .harness import (  # noqa: F401,E402
+    ExperimentSpec, build_dataset, conditioning_sweep, make_conditioned_regression, make_regression, run_experiment,
+    write_sweep_csv,
+)

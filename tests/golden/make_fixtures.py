@@ -3,7 +3,7 @@ container only; /root/reference does not exist on the GPU box).
 
 Sources (reference outputs and known-answer tests, not source code):
   proj/out/regression_floor/{halp-8,halp-16,svrg,lp-svrg-8,lp-svrg-16,sgd,lp-sgd-8,lp-sgd-16}_seed{1..5}.csv  golden traces
-  proj/out/regression_floor/manifest.json                        final values
+  proj/out/regression_floor/manifest.json                        final values (+ verbatim copy)
   proj/specs/regression_floor.json                               their spec
   proj/tests/test_rng.cpp:14-31                                  RNG KATs
 """
@@ -53,7 +53,15 @@ def rng_kats():
               open(os.path.join(OUT, "rng_kats.json"), "w"), indent=1)
 
 
+def manifest_copy():
+    """the reference's run_experiment manifest, byte for byte (harness.cpp:358-375)"""
+    src = open(f"{REF}/out/regression_floor/manifest.json").read()
+    with open(os.path.join(OUT, "regression_floor_manifest.json"), "w") as f:
+        f.write(src)
+
+
 if __name__ == "__main__":
     traces()
+    manifest_copy()
     rng_kats()
     print("fixtures written to", OUT)
