@@ -77,6 +77,11 @@ typedef struct {
                                   of the rank sums + rank-tree finalize), also at world_size 1;
                                   2: no NCCL, the caller moves the rank sums (test hook:
                                   halp_rank_partial / halp_finalize_gathered only); ABI >= 4 */
+  /* lpopt::QuantizedExamples (objectives.hpp): the dataset's LM-HALP codes,
+   * int64 [n][d] at one scale (halp_quantize_dataset), or NULL; ABI >= 4 */
+  const int64_t* qcodes;
+  int32_t        qbits;
+  double         qdelta;
 } halp_problem_desc;
 
 typedef struct halp_problem halp_problem;
@@ -100,8 +105,9 @@ typedef struct {
   int32_t       algorithm;            /* HALP_ALGO_*: lpopt::Algorithm numbering; ABI >= 3 */
 } halp_config;
 
-/* lpopt::Algorithm values halp_run accepts (optimizers.hpp:13-15; all but LmHalp) */
-enum { HALP_ALGO_SGD = 0, HALP_ALGO_SVRG = 1, HALP_ALGO_LP_SGD = 2, HALP_ALGO_LP_SVRG = 3, HALP_ALGO_HALP = 4 };
+/* lpopt::Algorithm values halp_run accepts (optimizers.hpp:13-15) */
+enum { HALP_ALGO_SGD = 0, HALP_ALGO_SVRG = 1, HALP_ALGO_LP_SGD = 2, HALP_ALGO_LP_SVRG = 3, HALP_ALGO_HALP = 4,
+       HALP_ALGO_LM_HALP = 5 /* needs qcodes; bits <= 16, d*C <= 4096, one GPU */ };
 
 /* lpopt::MetricRow (optimizers.hpp:49-58), HALP subset */
 typedef struct {
@@ -111,6 +117,8 @@ typedef struct {
   double   grad_norm;
   double   delta;
   uint64_t iterate_hash;
+  double   delta_inner;  /* LM-HALP inner-update scale (0 otherwise); ABI >= 4 */
+  double   delta_aux;    /* LM-HALP auxiliary scalar scale */
 } halp_row;
 
 /* lpopt::RunRecord (optimizers.hpp:60-67).  Caller-owned buffers. */
@@ -240,6 +248,9 @@ int halp_make_regression(int64_t n, int32_t d, double noise_sd, uint64_t seed, d
 /* make_classification (objectives.cpp:46-76): X [n][d], labels [n] */
 int halp_make_classification(int64_t n, int32_t d, int32_t num_classes, double separation, uint64_t seed,
                              double* X, int32_t* labels);
+/* quantize_dataset (objectives.cpp:110-133): codes [n][d] int64, *delta = data scale */
+int halp_quantize_dataset(const double* X, int64_t n, int32_t d, int32_t bits, uint64_t seed, int64_t* codes,
+                          double* delta);
 /* `count` successive QuantRng(seed, stream).next_normal() draws (rng.hpp:57-62) */
 int halp_normals(uint64_t seed, uint64_t stream, int64_t count, double* out);
 

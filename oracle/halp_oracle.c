@@ -895,6 +895,7 @@ typedef struct {
   oq_record* rec;
   double t0, next_pass;
   int D;
+  double delta_inner, delta_aux; /* LM-HALP rows only (set before rec_boundary) */
 } recorder;
 
 static int rec_due(const recorder* r, double pass, int forced) {
@@ -915,6 +916,8 @@ static int rec_boundary(recorder* r, double pass, const double* w, double loss, 
     row->grad_norm = gn;
     row->delta = delta;
     row->iterate_hash = oq_hash_vector(w, r->D);
+    row->delta_inner = r->delta_inner;
+    row->delta_aux = r->delta_aux;
     if (r->cfg->metric_every_passes > 0.0) r->next_pass = pass + r->cfg->metric_every_passes;
   }
   if (bad) {
@@ -980,7 +983,7 @@ int oq_run_halp(const oq_objective* o, const oq_config* cfg, const oq_plan* plan
   rec->inner_fp_vector_ops = 0;
   rec->fullgrad_seconds = 0.0;
   rec->inner_seconds = 0.0;
-  recorder r = {cfg, rec, now_s(), 0.0, D};
+  recorder r = {cfg, rec, now_s(), 0.0, D, 0.0, 0.0};
   int64_t steps = 0, traced = 0, hashed = 0;
   int converged = 0;
   const int fgth = rec->fullgrad_threads > 0 ? rec->fullgrad_threads : 1;
@@ -1152,7 +1155,7 @@ static int run_svrg_family(const oq_objective* o, const oq_config* cfg, const oq
   rec->inner_fp_vector_ops = 0;
   rec->fullgrad_seconds = 0.0;
   rec->inner_seconds = 0.0;
-  recorder r = {cfg, rec, now_s(), 0.0, D};
+  recorder r = {cfg, rec, now_s(), 0.0, D, 0.0, 0.0};
   int64_t steps = 0, traced = 0;
   const int fgth = rec->fullgrad_threads > 0 ? rec->fullgrad_threads : 1;
   for (int k = 0; k < cfg->epochs; ++k) {
@@ -1262,7 +1265,7 @@ static int run_sgd_family(const oq_objective* o, const oq_config* cfg, const oq_
   rec->inner_fp_vector_ops = 0;
   rec->fullgrad_seconds = 0.0;
   rec->inner_seconds = 0.0;
-  recorder r = {cfg, rec, now_s(), 0.0, D};
+  recorder r = {cfg, rec, now_s(), 0.0, D, 0.0, 0.0};
   int64_t steps = 0, traced = 0;
   const int fgth = rec->fullgrad_threads > 0 ? rec->fullgrad_threads : 1;
   for (int k = 0; k < cfg->epochs; ++k) {
@@ -1323,6 +1326,266 @@ int oq_run(const oq_objective* o, const oq_config* cfg, const oq_plan* plan, oq_
     case OQ_ALGO_HALP: return oq_run_halp(o, cfg, plan, rec);
     case OQ_ALGO_SVRG: return run_svrg_family(o, cfg, plan, rec, 0);
     case OQ_ALGO_LP_SVRG: return run_svrg_family(o, cfg, plan, rec, 1);
+    case OQ_ALGO_LM_HALP: set_err("lm_halp: dataset has no quantized examples"); return OQ_INVALID_INPUT;
     default: set_err("oracle: algorithm not restated"); return OQ_INVALID_INPUT;
   }
+}
+
+/* ======================================================================
+ * LM-HALP (optimizers.cpp:461-627): the integer inner loop of the paper's
+ * linear-model form.  REF = the reference's order (sequential epoch sweep,
+ * std::exp); MIRROR = the B200 kernels' (k_lm.cu: split tree over the
+ * device's splits with 128-thread row dots, deterministic exp).  The inner
+ * loop is integer arithmetic (exact in any order) apart from the link
+ * derivative.
+ * ====================================================================== */
+
+/* fixed_point.cpp data_scale (objectives.cpp:112-122) + quantize_dataset
+ * (:124-133): one LPRepr for the whole matrix, stream 2, row-major draws */
+int oq_quantize_dataset(const double* X, int64_t n, int d, int bits, uint64_t seed, int64_t* codes, double* delta) {
+  if (bits < 2 || bits > 64) { set_err("data_scale: bits must be in [2, 64]"); return OQ_INVALID_INPUT; }
+  double max_abs = 0.0;
+  for (int64_t k = 0; k < n * (int64_t)d; ++k) {
+    const double a = fabs(X[k]);
+    if (!(a <= max_abs)) max_abs = a; /* NaN propagates like Eigen's maxCoeff of cwiseAbs */
+  }
+  if (!isfinite(max_abs)) { set_err("data_scale: matrix has non-finite entries"); return OQ_INVALID_INPUT; }
+  const double span = ldexp(1.0, bits - 1) - 1.0;
+  const double dl = max_abs == 0.0 ? 1.0 : max_abs / span;
+  oq_rng rng;
+  oq_rng_init(&rng, seed, 2);
+  for (int64_t k = 0; k < n * (int64_t)d; ++k) {
+    const double u = oq_next_uniform(&rng);
+    codes[k] = oq_quantize_code(X[k], dl, bits, u, NULL);
+  }
+  *delta = dl;
+  return OQ_OK;
+}
+
+static int64_t lm_sat(int64_t c, int bits) {
+  const int64_t lo = min_code_for(bits), hi = max_code_for(bits);
+  return c < lo ? lo : c > hi ? hi : c;
+}
+/* sub_same_scale (fixed_point.cpp:150-165) */
+static int64_t lm_sub(int64_t a, int64_t b, int bits) {
+  int64_t s;
+  if (__builtin_sub_overflow(a, b, &s)) s = a > b ? INT64_MAX : INT64_MIN;
+  return lm_sat(s, bits);
+}
+/* requantize_shift (fixed_point.cpp:223-243) for one code */
+static int64_t lm_requant(int64_t c, int shift, int out_bits, double u) {
+  int64_t hi = c >> shift;
+  const int64_t low = c - (int64_t)((uint64_t)hi << shift);
+  if (low != 0 && u < ldexp((double)low, -shift)) ++hi;
+  return lm_sat(hi, out_bits);
+}
+
+/* squared: dl = l - y; softmax: the order of the mode (REF std::exp, MIRROR hexp) */
+static void lm_link_dl(const oq_objective* o, int64_t i, const double* l, double* dl, int mirror) {
+  const int C = o->C;
+  for (int c = 0; c < C; ++c) dl[c] = l[c];
+  if (o->loss == OQ_SQUARED) { dl[0] = l[0] - o->y[i]; return; }
+  if (mirror) mirror_softmax_dl(dl, C, o->labels[i]);
+  else ref_softmax_dl(dl, C, o->labels[i]);
+}
+static double lm_link_loss(const oq_objective* o, int64_t i, const double* l, int mirror) {
+  if (o->loss == OQ_SQUARED) {
+    const double r = l[0] - o->y[i];
+    return 0.5 * r * r;
+  }
+  return mirror ? mirror_softmax_loss(l, o->C, o->labels[i]) : ref_softmax_loss(l, o->C, o->labels[i]);
+}
+
+/* epoch_stats (optimizers.cpp:486-505): phi [n][C], g, loss; returns gn */
+static double lm_epoch_stats(const oq_objective* o, const oq_quantized* q, const double* wt, const oq_plan* plan,
+                             double* phi, double* g, double* loss_out) {
+  const int d = o->d, C = o->C, D = d * C;
+  const int64_t n = o->n;
+  double* x = (double*)malloc(sizeof(double) * (size_t)d);
+  double lg[64], dl[64];
+  if (!plan) {
+    for (int k = 0; k < D; ++k) g[k] = 0.0;
+    double acc = 0.0;
+    for (int64_t i = 0; i < n; ++i) {
+      for (int j = 0; j < d; ++j) x[j] = (double)q->codes[i * d + j] * q->delta;
+      ref_row_logits(x, wt, d, C, lg);
+      for (int c = 0; c < C; ++c) phi[i * C + c] = lg[c];
+      acc += lm_link_loss(o, i, lg, 0);
+      lm_link_dl(o, i, lg, dl, 0);
+      for (int c = 0; c < C; ++c)
+        for (int j = 0; j < d; ++j) g[(size_t)c * d + j] += x[j] * dl[c];
+    }
+    for (int k = 0; k < D; ++k) g[k] /= (double)n;
+    for (int k = 0; k < D; ++k) g[k] += o->l2 * wt[k];
+    *loss_out = acc / (double)n + 0.5 * o->l2 * ref_sqnorm(wt, D);
+    free(x);
+    return sqrt(ref_sqnorm(g, D));
+  }
+  /* MIRROR: splits of the device plan, sequential rows inside a split,
+   * 128-thread row dots (V = 1), gradient by fma, pairwise split tree */
+  const int S = plan->fg_splits;
+  double* part = (double*)calloc((size_t)S * D, sizeof(double));
+  double* lpart = (double*)calloc((size_t)S, sizeof(double));
+  for (int s = 0; s < S; ++s) {
+    const int64_t r0 = (int64_t)((__int128)n * s / S), r1 = (int64_t)((__int128)n * (s + 1) / S);
+    double* ps = part + (size_t)s * D;
+    double la = 0.0;
+    for (int64_t r = r0; r < r1; ++r) {
+      for (int j = 0; j < d; ++j) x[j] = (double)q->codes[r * d + j] * q->delta;
+      for (int c = 0; c < C; ++c) lg[c] = mirror_fg_dot(x, wt + (size_t)c * d, d, 128, 1);
+      for (int c = 0; c < C; ++c) phi[r * C + c] = lg[c];
+      la = la + lm_link_loss(o, r, lg, 1);
+      lm_link_dl(o, r, lg, dl, 1);
+      for (int c = 0; c < C; ++c)
+        for (int j = 0; j < d; ++j) ps[(size_t)c * d + j] = fma(dl[c], x[j], ps[(size_t)c * d + j]);
+    }
+    lpart[s] = la;
+  }
+  for (int k = 0; k < D; ++k) g[k] = tree_sum(part + k, D, S) / (double)n + o->l2 * wt[k];
+  double v[256];
+  for (int t = 0; t < 256; ++t) {
+    double a = 0.0;
+    for (int k = t; k < D; k += 256) a = fma(wt[k], wt[k], a);
+    v[t] = a;
+  }
+  double ws[8];
+  for (int wi = 0; wi < 8; ++wi) ws[wi] = warp_butterfly(v + wi * 32);
+  double sq = ws[0];
+  for (int wi = 1; wi < 8; ++wi) sq = sq + ws[wi];
+  *loss_out = tree_sum(lpart, 1, S) / (double)n + (0.5 * o->l2) * sq;
+  free(part);
+  free(lpart);
+  free(x);
+  return mirror_norm(g, D);
+}
+
+/* the scale chain of optimizers.cpp:509-521 (and :600-606); 0 = fine, else invalid */
+static int lm_scales(double gn, const oq_config* cfg, double delta_d, double* dm, double* di, double* daux, int check) {
+  *dm = *di = *daux = 0.0;
+  if (isfinite(gn) && gn > 0.0) {
+    double s = oq_halp_scale(gn, cfg->mu, cfg->bits);
+    if (s < cfg->delta_min) s = cfg->delta_min;
+    const double di0 = ldexp(s, -cfg->bits);
+    *daux = di0 / delta_d;
+    if (check && !(isfinite(*daux) && *daux > 0.0)) {
+      set_err("lm_halp: auxiliary scale left the double range");
+      return OQ_INVALID_INPUT;
+    }
+    *di = *daux * delta_d;
+    *dm = ldexp(*di, cfg->bits);
+  }
+  return OQ_OK;
+}
+
+int oq_run_lm_halp(const oq_objective* o, const oq_quantized* q, const oq_config* cfg, const oq_plan* plan,
+                   oq_record* rec) {
+  int rc = check_objective(o);
+  if (rc) return rc;
+  oq_config c2 = *cfg;
+  c2.algorithm = OQ_ALGO_HALP; /* the generic checks of validate_config (bit-centred) */
+  rc = validate_config(o, &c2);
+  if (rc) return rc;
+  if (cfg->bits > 32) { set_err("lm_halp: bits must be <= 32 (inner arithmetic is 2b wide)"); return OQ_INVALID_INPUT; }
+  if (cfg->option != 0) { set_err("lm_halp: only the last-iterate epoch update is defined"); return OQ_INVALID_INPUT; }
+  if (!q || !q->codes) { set_err("lm_halp: dataset has no quantized examples"); return OQ_INVALID_INPUT; }
+  if (q->bits != cfg->bits) { set_err("lm_halp: dataset quantized at a different width"); return OQ_INVALID_INPUT; }
+  const int d = o->d, C = o->C, D = d * C, b = cfg->bits;
+  const int64_t n = o->n;
+  const int64_t T = oq_resolve_inner_steps(cfg, n);
+  if (T < 1) { set_err("optimizer: epoch length must be >= 1"); return OQ_INVALID_INPUT; }
+  oq_rng sample, rounder;
+  oq_rng_init(&sample, cfg->seed, 0);
+  oq_rng_init(&rounder, cfg->seed, 1);
+  double* wt = (double*)calloc((size_t)D, sizeof(double));
+  if (cfg->init) memcpy(wt, cfg->init, sizeof(double) * (size_t)D);
+  double* phi = (double*)malloc(sizeof(double) * (size_t)(n * C));
+  double* g = (double*)malloc(sizeof(double) * (size_t)D);
+  int64_t* z = (int64_t*)calloc((size_t)D, sizeof(int64_t));
+  int64_t* h = (int64_t*)calloc((size_t)D, sizeof(int64_t));
+  rec->rows_n = 0;
+  rec->status = OQ_STATUS_OK;
+  rec->steps_taken = 0;
+  rec->inner_fp_vector_ops = 0;
+  rec->inner_lp_vector_ops = 0;
+  rec->fullgrad_seconds = 0.0;
+  rec->inner_seconds = 0.0;
+  recorder r = {cfg, rec, now_s(), 0.0, D, 0.0, 0.0};
+  int64_t steps = 0, traced = 0, hashed = 0;
+  int converged = 0;
+  rc = OQ_OK;
+  for (int k = 0; k < cfg->epochs && !converged; ++k) {
+    double loss = 0.0, dm, di, daux;
+    const double t0 = now_s();
+    const double gn = lm_epoch_stats(o, q, wt, plan, phi, g, &loss);
+    rec->fullgrad_seconds += now_s() - t0;
+    rc = lm_scales(gn, cfg, q->delta, &dm, &di, &daux, 1);
+    if (rc) goto done;
+    r.delta_inner = di;
+    r.delta_aux = daux;
+    rc = rec_boundary(&r, (double)steps / (double)n, wt, loss, gn, dm, k == 0 || gn == 0.0);
+    if (rc) goto done;
+    if (gn == 0.0) { rec->status = OQ_STATUS_CONVERGED; converged = 1; break; }
+    /* zcols = Q_m(0): D draws (class-major), codes 0 */
+    for (int kk = 0; kk < D; ++kk) { (void)oq_next_uniform(&rounder); z[kk] = 0; }
+    /* h_wide = widen_range(Q_i(alpha * g_c), b) */
+    for (int kk = 0; kk < D; ++kk) {
+      const double a = cfg->alpha * g[kk];
+      int err = 0;
+      h[kk] = oq_quantize_code(a, di, b, oq_next_uniform(&rounder), &err);
+      if (err) { set_err("quantize: input must be finite"); rc = OQ_INVALID_INPUT; goto done; }
+    }
+    const double sc = q->delta * dm; /* dot_lp: (double)acc * (delta_x * delta_z) */
+    const double ti0 = now_s();
+    double lg[64], ph[64], dl[64], dl0[64];
+    for (int64_t t = 0; t < T; ++t) {
+      const int64_t i = (int64_t)oq_next_index(&sample, (uint64_t)n);
+      const int64_t* xr = q->codes + i * d;
+      for (int c = 0; c < C; ++c) {
+        __int128 acc = 0;
+        for (int j = 0; j < d; ++j) acc += (__int128)xr[j] * (__int128)z[(size_t)c * d + j];
+        lg[c] = phi[i * C + c] + (double)acc * sc;
+        ph[c] = phi[i * C + c];
+      }
+      lm_link_dl(o, i, lg, dl, plan != NULL);
+      lm_link_dl(o, i, ph, dl0, plan != NULL);
+      for (int c = 0; c < C; ++c) {
+        const double beta = cfg->alpha * (dl[c] - dl0[c]);
+        int err = 0;
+        const int64_t gam = oq_quantize_code(beta, daux, b, oq_next_uniform(&rounder), &err);
+        if (err) { set_err("quantize: input must be finite"); rc = OQ_INVALID_INPUT; goto done; }
+        for (int j = 0; j < d; ++j) {
+          const size_t kk = (size_t)c * d + j;
+          const int64_t wz = z[kk] * ((int64_t)1 << b);          /* widen_shift */
+          const int64_t u1 = lm_sub(wz, xr[j] * gam, 2 * b);     /* - mul_scalar */
+          const int64_t u = lm_sub(u1, h[kk], 2 * b);            /* - h_wide */
+          z[kk] = lm_requant(u, b, b, oq_next_uniform(&rounder)); /* requantize_shift */
+        }
+      }
+      if (rec->trace_codes && traced + D <= rec->trace_cap) {
+        memcpy(rec->trace_codes + traced, z, sizeof(int64_t) * (size_t)D);
+        traced += D;
+      }
+      if (rec->step_hash && hashed < rec->step_hash_cap) rec->step_hash[hashed++] = oq_code_hash(z, D);
+    }
+    rec->inner_seconds += now_s() - ti0;
+    rec->inner_lp_vector_ops += (uint64_t)(6 * C) * (uint64_t)T;
+    for (int kk = 0; kk < D; ++kk) wt[kk] += (double)z[kk] * dm;
+    steps += T;
+  }
+  if (!converged) {
+    double loss = 0.0, dm, di, daux;
+    const double gn = lm_epoch_stats(o, q, wt, plan, phi, g, &loss);
+    lm_scales(gn, cfg, q->delta, &dm, &di, &daux, 0);
+    r.delta_inner = di;
+    r.delta_aux = daux;
+    rc = rec_boundary(&r, (double)steps / (double)n, wt, loss, gn, dm, 1);
+    if (rc) goto done;
+    if (gn == 0.0) rec->status = OQ_STATUS_CONVERGED;
+  }
+  memcpy(rec->final_iterate, wt, sizeof(double) * (size_t)D);
+  rec->steps_taken = steps;
+done:
+  if (rc == OQ_DIVERGED) rec->steps_taken = 0;
+  free(wt); free(phi); free(g); free(z); free(h);
+  return rc;
 }

@@ -122,11 +122,12 @@ typedef struct {
   int32_t  algorithm;            /* lpopt::Algorithm: 0 Sgd, 1 Svrg, 2 LpSgd, 3 LpSvrg, 4 Halp */
 } oq_config;
 
-enum { OQ_ALGO_SGD = 0, OQ_ALGO_SVRG = 1, OQ_ALGO_LP_SGD = 2, OQ_ALGO_LP_SVRG = 3, OQ_ALGO_HALP = 4 };
+enum { OQ_ALGO_SGD = 0, OQ_ALGO_SVRG = 1, OQ_ALGO_LP_SGD = 2, OQ_ALGO_LP_SVRG = 3, OQ_ALGO_HALP = 4, OQ_ALGO_LM_HALP = 5 };
 
 typedef struct {
   double   pass, seconds, loss, grad_norm, delta;
   uint64_t iterate_hash;
+  double   delta_inner, delta_aux;   /* LM-HALP scales (optimizers.hpp:56-57), 0 otherwise */
 } oq_row;
 
 enum { OQ_STATUS_OK = 0, OQ_STATUS_CONVERGED = 1, OQ_STATUS_DIVERGED = 2 };
@@ -153,6 +154,7 @@ typedef struct {
    * decisions depend on the reduction order. */
   uint64_t* step_hash;
   int64_t   step_hash_cap;
+  uint64_t  inner_lp_vector_ops;  /* LM-HALP's integer vector ops (instr counters) */
 } oq_record;
 
 int      oq_run_halp(const oq_objective* o, const oq_config* cfg, const oq_plan* plan, oq_record* rec);
@@ -164,6 +166,20 @@ uint64_t oq_hash_vector(const double* v, int64_t len);
 /* FNV-1a over the int64 code bytes of one inner step (test hook) */
 uint64_t oq_code_hash(const int64_t* codes, int64_t len);
 const char* oq_last_error(void);
+
+/* ---- LM-HALP: quantize_dataset (objectives.cpp:110-133, data_scale :112-122)
+ * and run_lm_halp (optimizers.cpp:461-627), non-bypass path ----
+ * codes [n][d] int64 out, *delta = the data scale (LPRepr delta) */
+int oq_quantize_dataset(const double* X, int64_t n, int d, int bits, uint64_t seed, int64_t* codes, double* delta);
+typedef struct {
+  const int64_t* codes;  /* [n][d] */
+  double         delta;
+  int            bits;
+} oq_quantized;
+/* MIRROR plan: only fg_splits is used (the device's split count); the LM
+ * stats pass uses 128-thread row dots.  Trace: z codes [epoch][t][D]. */
+int oq_run_lm_halp(const oq_objective* o, const oq_quantized* q, const oq_config* cfg, const oq_plan* plan,
+                   oq_record* rec);
 
 /* MIRROR-mode pieces of the multi-GPU full gradient: one rank's split
  * subtree root [D+1] and the finalize over G gathered rank sums */

@@ -58,7 +58,7 @@ class _Config(C.Structure):
 
 class _Row(C.Structure):
     _fields_ = [(k, C.c_double) for k in ("pass_", "seconds", "loss", "grad_norm", "delta")] + [
-        ("iterate_hash", C.c_uint64)
+        ("iterate_hash", C.c_uint64), ("delta_inner", C.c_double), ("delta_aux", C.c_double)
     ]
 
 
@@ -68,8 +68,12 @@ class _Record(C.Structure):
         ("final_iterate", C.c_void_p), ("status", C.c_int32), ("steps_taken", C.c_int64),
         ("inner_fp_vector_ops", C.c_uint64), ("trace_codes", C.c_void_p), ("trace_cap", C.c_int64),
         ("fullgrad_seconds", C.c_double), ("inner_seconds", C.c_double), ("fullgrad_threads", C.c_int),
-        ("step_hash", C.c_void_p), ("step_hash_cap", C.c_int64),
+        ("step_hash", C.c_void_p), ("step_hash_cap", C.c_int64), ("inner_lp_vector_ops", C.c_uint64),
     ]
+
+
+class _Quantized(C.Structure):
+    _fields_ = [("codes", C.c_void_p), ("delta", C.c_double), ("bits", C.c_int)]
 
 
 class _Datagen(C.Structure):
@@ -108,6 +112,10 @@ def lib():
         L.oq_run.argtypes = [C.POINTER(_Objective), C.POINTER(_Config), C.POINTER(_Plan), C.POINTER(_Record)]
         L.oq_datagen.argtypes = [C.POINTER(_Datagen), C.c_int64, C.c_int64, C.c_int, C.c_void_p, C.c_void_p,
                                  C.c_void_p]
+        L.oq_quantize_dataset.argtypes = [C.c_void_p, C.c_int64, C.c_int, C.c_int, C.c_uint64, C.c_void_p,
+                                          C.POINTER(C.c_double)]
+        L.oq_run_lm_halp.argtypes = [C.POINTER(_Objective), C.c_void_p, C.POINTER(_Config), C.POINTER(_Plan),
+                                     C.POINTER(_Record)]
         L.oq_code_hash.restype = C.c_uint64
         L.oq_code_hash.argtypes = [C.c_void_p, C.c_int64]
         L.oq_hash_vector.restype = C.c_uint64
@@ -314,6 +322,7 @@ class OracleRecord:
     status: str = "ok"
     steps_taken: int = 0
     inner_fp_vector_ops: int = 0
+    inner_lp_vector_ops: int = 0
     trace: Optional[np.ndarray] = None
     step_hash: Optional[np.ndarray] = None
     fullgrad_seconds: float = 0.0
@@ -335,7 +344,7 @@ def run(obj: OracleObjective, cfg: OracleConfig, plan=None, trace_steps: int = 0
     return _run(obj, cfg, plan, trace_steps, fullgrad_threads, rows_cap, int(cfg.algorithm))
 
 
-def _run(obj, cfg, plan, trace_steps, fullgrad_threads, rows_cap, algorithm, hash_steps=0) -> OracleRecord:
+def _run(obj, cfg, plan, trace_steps, fullgrad_threads, rows_cap, algorithm, hash_steps=0, quantized=None) -> OracleRecord:
     init = None
     if cfg.init is not None:
         init = np.ascontiguousarray(cfg.init, dtype=np.float64)
@@ -350,20 +359,28 @@ def _run(obj, cfg, plan, trace_steps, fullgrad_threads, rows_cap, algorithm, has
     rec = _Record(rows, cap, 0, fin.ctypes.data, 0, 0, 0, tr.ctypes.data if tr is not None else None,
                   tr.size if tr is not None else 0, 0.0, 0.0, fullgrad_threads,
                   sh.ctypes.data if sh is not None else None, hash_steps)
-    rc = lib().oq_run(C.byref(obj._s), C.byref(c), _plan(plan), C.byref(rec))
+    if algorithm == 5:
+        qs = None
+        if quantized is not None:
+            qs = _Quantized(quantized.codes.ctypes.data, quantized.delta, quantized.bits)
+        rc = lib().oq_run_lm_halp(C.byref(obj._s), C.byref(qs) if qs is not None else None, C.byref(c), _plan(plan),
+                                  C.byref(rec))
+    else:
+        rc = lib().oq_run(C.byref(obj._s), C.byref(c), _plan(plan), C.byref(rec))
     if rc not in (0, 2):
         _check(rc)
     out = OracleRecord()
     out.rc = rc
     out.rows = [
         dict(pass_=r.pass_, seconds=r.seconds, loss=r.loss, grad_norm=r.grad_norm, delta=r.delta,
-             iterate_hash=r.iterate_hash)
+             iterate_hash=r.iterate_hash, delta_inner=r.delta_inner, delta_aux=r.delta_aux)
         for r in rows[: rec.rows_n]
     ]
     out.final_iterate = fin
     out.status = STATUS[rec.status]
     out.steps_taken = rec.steps_taken
     out.inner_fp_vector_ops = rec.inner_fp_vector_ops
+    out.inner_lp_vector_ops = rec.inner_lp_vector_ops
     out.fullgrad_seconds = rec.fullgrad_seconds
     out.inner_seconds = rec.inner_seconds
     if tr is not None:
@@ -413,3 +430,29 @@ def generate(kind: str, n: int, d: int, *, num_classes: int = 0, dtype: str = "f
     _check(lib().oq_datagen(C.byref(g), r0, r1 - r0, th, X.ctypes.data, y.ctypes.data if y is not None else None,
                             lab.ctypes.data if lab is not None else None))
     return (X, y) if y is not None else (X, lab)
+
+
+@dataclass
+class OracleQuantized:
+    """lpopt::QuantizedExamples (objectives.hpp): int64 codes [n][d] at one scale"""
+
+    codes: np.ndarray
+    delta: float
+    bits: int
+
+
+def quantize_dataset(X, bits: int, seed: int) -> OracleQuantized:
+    """objectives.cpp:110-133 (data_scale + stream-2 stochastic rounding, row-major)"""
+    X = np.ascontiguousarray(X, dtype=np.float64)
+    codes = np.empty(X.shape, dtype=np.int64)
+    dl = C.c_double()
+    _check(lib().oq_quantize_dataset(X.ctypes.data, X.shape[0], X.shape[1], bits, seed, codes.ctypes.data,
+                                     C.byref(dl)))
+    return OracleQuantized(codes, dl.value, bits)
+
+
+def run_lm_halp(obj: OracleObjective, q: Optional[OracleQuantized], cfg: OracleConfig, plan=None,
+                trace_steps: int = 0, hash_steps: int = 0) -> OracleRecord:
+    """optimizers.cpp:461-627 (the non-bypass integer inner loop).  obj's X is
+    not read: every pass uses the dequantized codes of q."""
+    return _run(obj, cfg, plan, trace_steps, 1, 0, 5, hash_steps, q)

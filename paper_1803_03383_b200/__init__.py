@@ -9,6 +9,7 @@ from .halp import (  # noqa: F401
     GridAxis, GridOutcome, GridResult, MetricRow, Objective, OptimizerConfig, RunRecord, UnsupportedError, generate,
     format_double, grid_search, halp_scale, hash_vector, write_run_csv,
     oracle_plan_for, plan_for, resolve_inner_steps, rng_state_after, run, run_halp, run_lp_sgd, run_lp_svrg, run_prepared, run_sgd, run_svrg,
+    run_lm_halp, quantize_dataset, data_scale, QuantizedExamples,
     shard_plan,
 )
 from . import harness  # noqa: F401,E402

@@ -23,7 +23,8 @@ class ProblemDesc(C.Structure):
         ("X", C.c_void_p), ("dtype", C.c_int32), ("mem", C.c_int32), ("n", C.c_int64), ("d", C.c_int32),
         ("loss", C.c_int32), ("num_classes", C.c_int32), ("y", C.c_void_p), ("labels", C.c_void_p),
         ("l2", C.c_double), ("device", C.c_int32), ("world_size", C.c_int32), ("rank", C.c_int32),
-        ("nccl_id", C.c_void_p), ("collective", C.c_int32),
+        ("nccl_id", C.c_void_p), ("collective", C.c_int32), ("qcodes", C.c_void_p), ("qbits", C.c_int32),
+        ("qdelta", C.c_double),
     ]
 
 
@@ -38,7 +39,7 @@ class Config(C.Structure):
 
 class Row(C.Structure):
     _fields_ = [(k, C.c_double) for k in ("pass_", "seconds", "loss", "grad_norm", "delta")] + [
-        ("iterate_hash", C.c_uint64)
+        ("iterate_hash", C.c_uint64), ("delta_inner", C.c_double), ("delta_aux", C.c_double)
     ]
 
 
@@ -84,7 +85,7 @@ SYMBOLS = [
     "halp_run", "halp_full_gradient", "halp_set_trace", "halp_last_timing", "halp_bench_full_gradient",
     "halp_batch_create", "halp_batch_destroy", "halp_batch_run", "halp_datagen", "halp_shard_plan",
     "halp_rng_state_after", "halp_plan_for", "halp_batch_plan", "halp_rank_partial", "halp_finalize_gathered",
-    "halp_make_regression", "halp_make_classification", "halp_normals",
+    "halp_make_regression", "halp_make_classification", "halp_normals", "halp_quantize_dataset",
 ]
 
 _lib = None
@@ -125,6 +126,8 @@ def lib():
     L.halp_make_classification.argtypes = [C.c_int64, C.c_int32, C.c_int32, C.c_double, C.c_uint64, C.c_void_p,
                                            C.c_void_p]
     L.halp_normals.argtypes = [C.c_uint64, C.c_uint64, C.c_int64, C.c_void_p]
+    L.halp_quantize_dataset.argtypes = [C.c_void_p, C.c_int64, C.c_int32, C.c_int32, C.c_uint64, C.c_void_p,
+                                        C.POINTER(C.c_double)]
     L.halp_rng_state_after.restype = C.c_uint64
     L.halp_rng_state_after.argtypes = [C.c_uint64, C.c_uint64, C.c_uint64]
     _lib = L

@@ -25,7 +25,7 @@ LIB = os.path.join(HERE, "libhalp_b200.so")
 CUDA = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 NVCC = os.path.join(CUDA, "bin", "nvcc")
 
-CU_SOURCES = ["k_fullgrad.cu", "k_fullgrad_smx.cu", "k_fullgrad_stream.cu", "k_inner.cu", "k_batch.cu", "k_datagen.cu"]
+CU_SOURCES = ["k_fullgrad.cu", "k_fullgrad_smx.cu", "k_fullgrad_stream.cu", "k_inner.cu", "k_batch.cu", "k_datagen.cu", "k_lm.cu"]
 CXX_SOURCES = ["halp_capi.cpp", "halp_datasets.cpp"]
 HEADERS = ["halp_device.cuh", "kernels.h", "rng_jump.hpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

@@ -235,6 +235,13 @@ struct halp_problem {
   int64_t create_h2d = 0;  // bytes uploaded by halp_problem_create
   int x_finite = 0;        // bf16 X checked finite (K1 integer-conversion path)
   bool host_exchange = false;  // collective == 2: the caller moves the rank sums (test hook)
+  // LM-HALP: the quantized dataset (int8 / int16 codes), logits at w~ per row, h codes, error flag
+  void* q = nullptr;
+  int qbits = 0, qbytes = 0;
+  double qdelta = 0.0;
+  double* phi = nullptr;
+  long long* hdev = nullptr;
+  int* lm_bad = nullptr;
   Events ev_fg, ev_fin, ev_in, ev_smp;
 
   ~halp_problem() {
@@ -242,7 +249,8 @@ struct halp_problem {
     // stream-ordered frees back into the device pool (no device-wide sync)
     for (void* ptr : {(void*)w, (void*)w2, (void*)g, (void*)partials, (void*)rank_sum, (void*)gathered, (void*)stats,
                       (void*)u_out, (void*)idx, (void*)codes, (void*)blow, (void*)trace_dev, (void*)y,
-                      (void*)labels, (void*)tree_scratch, (void*)zb0, (void*)zb1})
+                      (void*)labels, (void*)tree_scratch, (void*)zb0, (void*)zb1, q, (void*)phi, (void*)hdev,
+                      (void*)lm_bad})
       if (ptr) cudaFreeAsync(ptr, stream);
     if (own_X && X) cudaFreeAsync(X, stream);
     if (comm) Nccl::get().commDestroy(comm);
@@ -492,7 +500,8 @@ struct Recorder {
   halp_record* rec;
   double t0, next_pass = 0.0;
   int D;
-  int boundary(double pass, const double* w, double loss, double gn, double delta, bool forced) {
+  int boundary(double pass, const double* w, double loss, double gn, double delta, bool forced, double delta_inner = 0.0,
+               double delta_aux = 0.0) {
     const bool bad =
         !(std::isfinite(loss) && std::isfinite(gn)) || loss > cfg->divergence_limit || gn > cfg->divergence_limit;
     const bool due = forced || cfg->metric_every_passes <= 0.0 || pass + 1e-9 >= next_pass;
@@ -505,6 +514,8 @@ struct Recorder {
       r.grad_norm = gn;
       r.delta = delta;
       r.iterate_hash = fnv1a(w, D);
+      r.delta_inner = delta_inner;
+      r.delta_aux = delta_aux;
       if (cfg->metric_every_passes > 0.0) next_pass = pass + cfg->metric_every_passes;
     }
     if (bad) {
@@ -547,20 +558,44 @@ int validate(const halp_problem* p, const halp_config* c) {
   if (!(std::isfinite(c->divergence_limit) && c->divergence_limit > 0.0))
     return fail(HALP_INVALID_INPUT, "optimizer: divergence_limit must be positive");
   if (!(std::isfinite(c->delta_min) && c->delta_min > 0.0)) return fail(HALP_INVALID_INPUT, "optimizer: delta_min must be positive");
-  if (c->algorithm < HALP_ALGO_SGD || c->algorithm > HALP_ALGO_HALP)
-    return fail(HALP_UNSUPPORTED, "optimizer: algorithm not on the B200 path (LmHalp is not)");
+  if (c->algorithm < HALP_ALGO_SGD || c->algorithm > HALP_ALGO_LM_HALP)
+    return fail(HALP_INVALID_INPUT, "unknown algorithm enum value");
   if (c->algorithm == HALP_ALGO_LP_SVRG || c->algorithm == HALP_ALGO_LP_SGD) {  // uses_fixed_scale
     if (c->bits < 2 || c->bits > 64) return fail(HALP_INVALID_INPUT, "optimizer: bits must be in [2, 64]");
     if (!(std::isfinite(c->delta) && c->delta > 0.0))
       return fail(HALP_INVALID_INPUT, "optimizer: delta must be positive for fixed-scale runs");
   }
-  if (c->algorithm == HALP_ALGO_HALP) {  // uses_bit_centering
+  if (c->algorithm == HALP_ALGO_HALP || c->algorithm == HALP_ALGO_LM_HALP) {  // uses_bit_centering
     if (c->bits < 2 || c->bits > 64) return fail(HALP_INVALID_INPUT, "optimizer: bits must be in [2, 64]");
     if (!(std::isfinite(c->mu) && c->mu > 0.0))
       return fail(HALP_INVALID_INPUT, "optimizer: mu must be positive for bit-centered runs");
   }
   if (c->option != 0 && c->option != 1) return fail(HALP_INVALID_INPUT, "optimizer: option must be 0 (I) or 1 (II)");
-  (void)p;
+  if (c->algorithm == HALP_ALGO_LM_HALP && p) {  // optimizers.cpp:77-96
+    if (c->bits > 32) return fail(HALP_INVALID_INPUT, "lm_halp: bits must be <= 32 (inner arithmetic is 2b wide)");
+    if (c->option != 0) return fail(HALP_INVALID_INPUT, "lm_halp: only the last-iterate epoch update is defined");
+    if (!p->qbits) return fail(HALP_INVALID_INPUT, "lm_halp: dataset has no quantized examples");
+    if (p->qbits != c->bits) return fail(HALP_INVALID_INPUT, "lm_halp: dataset quantized at a different width");
+    if (c->bits > 16) return fail(HALP_UNSUPPORTED, "lm_halp: the B200 inner loop supports bits <= 16");
+    if (p->D > kLmMaxD) return fail(HALP_UNSUPPORTED, "lm_halp: d * classes above 4096");
+    if (p->world > 1 || p->comm) return fail(HALP_UNSUPPORTED, "lm_halp: single-GPU problems only");
+  }
+  return HALP_OK;
+}
+
+// LM-HALP scale chain (optimizers.cpp:509-521; theory.cpp:93-102)
+int lm_scales(double gn, const halp_config* c, double delta_d, double* dm, double* di, double* daux, bool check) {
+  *dm = *di = *daux = 0.0;
+  if (std::isfinite(gn) && gn > 0.0) {
+    const double span = std::ldexp(1.0, c->bits - 1) - 1.0;
+    const double s = std::max(gn / (c->mu * span), c->delta_min);
+    const double di0 = std::ldexp(s, -c->bits);
+    *daux = di0 / delta_d;
+    if (check && !(std::isfinite(*daux) && *daux > 0.0))
+      return fail(HALP_INVALID_INPUT, "lm_halp: auxiliary scale left the double range");
+    *di = *daux * delta_d;
+    *dm = std::ldexp(*di, c->bits);
+  }
   return HALP_OK;
 }
 
@@ -702,6 +737,39 @@ int halp_problem_create(const halp_problem_desc* desc, halp_problem** out) {
                         dev_in ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, p->stream) != cudaSuccess)
       return bail(fail(HALP_CUDA_ERROR, "copy of labels failed"));
     if (!dev_in) p->create_h2d += (int64_t)p->n * 4;
+  }
+  if (desc->qcodes) {
+    // QuantizedExamples: one LPRepr, codes within its width (LPVector ctor, fixed_point.cpp:83-93)
+    if (desc->qbits < 2 || desc->qbits > 64 || !(std::isfinite(desc->qdelta) && desc->qdelta > 0.0))
+      return bail(fail(HALP_INVALID_INPUT, "LPRepr: delta must be positive and finite"));
+    p->qbits = desc->qbits;
+    p->qdelta = desc->qdelta;
+    if (desc->qbits <= 16) {  // wider codes: kept as metadata only (halp_run reports UNSUPPORTED)
+      const size_t cnt = (size_t)p->n * p->d;
+      std::vector<int64_t> qh;
+      const int64_t* src = desc->qcodes;
+      if (dev_in) {
+        qh.resize(cnt);
+        if (copy_sync(qh.data(), desc->qcodes, cnt * 8, cudaMemcpyDeviceToHost, p->stream) != cudaSuccess)
+          return bail(fail(HALP_CUDA_ERROR, "copy of the quantized codes failed"));
+        src = qh.data();
+      }
+      const int64_t lo = -(1LL << (desc->qbits - 1)), hi = (1LL << (desc->qbits - 1)) - 1;
+      p->qbytes = desc->qbits <= 8 ? 1 : 2;
+      std::vector<char> packed(cnt * p->qbytes);
+      for (size_t k = 0; k < cnt; ++k) {
+        if (src[k] < lo || src[k] > hi) return bail(fail(HALP_INVALID_INPUT, "LPVector: code outside representable range"));
+        if (p->qbytes == 1) reinterpret_cast<int8_t*>(packed.data())[k] = (int8_t)src[k];
+        else reinterpret_cast<int16_t*>(packed.data())[k] = (int16_t)src[k];
+      }
+      if (dalloc(&p->q, packed.size(), p->stream) != cudaSuccess ||
+          copy_sync(p->q, packed.data(), packed.size(), cudaMemcpyHostToDevice, p->stream) != cudaSuccess)
+        return bail(fail(HALP_CUDA_ERROR, "upload of the quantized codes failed"));
+      if (dalloc(&p->phi, sizeof(double) * (size_t)p->n * C, p->stream) != cudaSuccess ||
+          dalloc(&p->hdev, sizeof(long long) * (size_t)p->d * C, p->stream) != cudaSuccess ||
+          dalloc(&p->lm_bad, sizeof(int), p->stream) != cudaSuccess)
+        return bail(fail(HALP_CUDA_ERROR, "cudaMallocAsync(LM buffers)"));
+    }
   }
   p->sp = shard_plan_for(p->n, p->d, C, p->dtype, world, p->rank);
   int rc = choose_plans(p);
@@ -872,6 +940,152 @@ int halp_bench_full_gradient(halp_problem* p, int reps, double* ms_per_pass) {
   return HALP_OK;
 }
 
+// lpopt::run_lm_halp (optimizers.cpp:461-627, the integer inner loop): per
+// epoch K7 (k_lm_stats) + split tree + k_finalize -> g, |g|, loss and the
+// logits phi at w~; the scale chain and the h codes on the host; K4 sample
+// indices; K8 (k3_lm) the T integer steps.
+static int run_lm(halp_problem* p, const halp_config* cfg, halp_record* rec) {
+  const int64_t n = p->n, D = p->D;
+  const int d = p->d, C = p->C, b = cfg->bits;
+  const int64_t T = cfg->inner_steps > 0 ? cfg->inner_steps : (int64_t)cfg->full_grad_period * n;
+  if (T < 1) return fail(HALP_INVALID_INPUT, "optimizer: epoch length must be >= 1");
+  p->timing = halp_timing{};
+  if (p->idx_cap < T) {
+    if (p->idx) cudaFreeAsync(p->idx, p->stream);
+    CU(dalloc(&p->idx, sizeof(int64_t) * T, p->stream));
+    p->idx_cap = T;
+  }
+  const uint64_t* jtab = nullptr;
+  const uint64_t* ptab = nullptr;
+  {
+    int rc = rng_tables(p->device, (int64_t)C * (d + 1), &ptab, &jtab, p->stream);
+    if (rc) return rc;
+  }
+  const auto& jt = JumpTables::get();
+  const uint64_t s_sample = rng_seed_state(cfg->seed, 0);
+  const uint64_t s_round = rng_seed_state(cfg->seed, 1);
+  std::vector<double> wh(D, 0.0), gh(D);
+  if (cfg->init) std::memcpy(wh.data(), cfg->init, sizeof(double) * D);
+  CU(copy_sync(p->w, wh.data(), sizeof(double) * D, cudaMemcpyHostToDevice, p->stream));
+  p->timing.h2d_bytes += sizeof(double) * D;
+  int64_t tr_steps = p->trace_cap > 0 ? std::min<int64_t>(T, p->trace_cap / D) : 0, traced = 0;
+  if (tr_steps > p->trace_dev_steps) {
+    if (p->trace_dev) cudaFreeAsync(p->trace_dev, p->stream);
+    CU(dalloc(&p->trace_dev, sizeof(long long) * tr_steps * D, p->stream));
+    p->trace_dev_steps = tr_steps;
+  }
+  rec->rows_n = 0;
+  rec->status = HALP_STATUS_OK;
+  rec->steps_taken = 0;
+  rec->inner_fp_vector_ops = 0;
+  rec->inner_lp_vector_ops = 0;
+  Recorder r{cfg, rec, now_s(), 0.0, (int)D};
+  const int64_t D1 = D + 1;
+  const int nloc = (int)p->sp.local_splits();
+  // K7 + tree + finalize at p->w -> g (device), stats -> host
+  auto stats = [&](double* gn, double* loss) -> int {
+    CU(cudaEventRecord(p->ev_fg.a, p->stream));
+    LmStatsParams sp{p->q, n, d, C, p->loss, p->qdelta, p->y, p->labels, p->w, (int)p->sp.S, (int)p->sp.split_begin,
+                     p->partials, p->phi};
+    CU(launch_lm_stats(sp, nloc, p->qbytes, p->stream));
+    CU(launch_split_tree(p->partials, nloc, (int)D1, p->gathered, p->tree_scratch, p->stream));
+    CU(cudaEventRecord(p->ev_fg.b, p->stream));
+    FinParams fin{p->gathered, 1, (int)D, p->w, n, p->l2, 1.0, 1e-300, 8, p->g, p->stats};
+    CU(launch_finalize(fin, p->stream));
+    p->timing.kernel_launches += 3;
+    p->timing.fullgrad_launches += 1;
+    double st[3];
+    CU(copy_sync(st, p->stats, sizeof st, cudaMemcpyDeviceToHost, p->stream));
+    float ms = 0;
+    CU(cudaEventElapsedTime(&ms, p->ev_fg.a, p->ev_fg.b));
+    p->timing.fullgrad_ms += ms;
+    *gn = st[0];
+    *loss = st[2];
+    return HALP_OK;
+  };
+  const uint64_t per_step = (uint64_t)C * (uint64_t)(d + 1);
+  const uint64_t per_epoch = 2 * (uint64_t)D + (uint64_t)T * per_step;
+  const long long maxb = (1LL << (b - 1)) - 1, minb = -(1LL << (b - 1));
+  int64_t steps = 0;
+  bool converged = false;
+  for (int k = 0; k < cfg->epochs && !converged; ++k) {
+    double gn, loss, dm, di, daux;
+    int rc = stats(&gn, &loss);
+    if (rc) return rc;
+    CU(copy_sync(wh.data(), p->w, sizeof(double) * D, cudaMemcpyDeviceToHost, p->stream));
+    rc = lm_scales(gn, cfg, p->qdelta, &dm, &di, &daux, true);
+    if (rc) return rc;
+    rc = r.boundary((double)steps / (double)n, wh.data(), loss, gn, dm, k == 0 || gn == 0.0, di, daux);
+    if (rc) return rc;
+    if (gn == 0.0) {
+      rec->status = HALP_STATUS_CONVERGED;
+      converged = true;
+      break;
+    }
+    // h = Q_inner(alpha g~) (widen_range keeps the codes); its D draws follow Q_m(0)'s D
+    CU(copy_sync(gh.data(), p->g, sizeof(double) * D, cudaMemcpyDeviceToHost, p->stream));
+    std::vector<long long> hh(D);
+    uint64_t st = jt.jump(s_round, (uint64_t)k * per_epoch + (uint64_t)D);
+    for (int64_t q = 0; q < D; ++q) {
+      st = xs_step_host(st);
+      const double u = (double)((st * 0x2545F4914F6CDD1DULL) >> 11) * 0x1.0p-53;
+      const double a = cfg->alpha * gh[q];
+      if (!std::isfinite(a)) return fail(HALP_INVALID_INPUT, "quantize: input must be finite");
+      hh[q] = (long long)host_quantize_code(a, di, b, u);
+      (void)maxb;
+      (void)minb;
+    }
+    CU(cudaMemcpyAsync(p->hdev, hh.data(), sizeof(long long) * D, cudaMemcpyHostToDevice, p->stream));
+    const uint64_t sbase = jt.jump(s_sample, (uint64_t)k * (uint64_t)T);
+    CU(cudaEventRecord(p->ev_smp.a, p->stream));
+    CU(launch_samples(sbase, T, 0, (uint64_t)T, (uint64_t)n, p->pow_tab, p->idx, nullptr, p->stream));
+    CU(cudaEventRecord(p->ev_smp.b, p->stream));
+    CU(cudaMemsetAsync(p->lm_bad, 0, sizeof(int), p->stream));
+    LmInnerParams ip{p->q, d, C, p->loss, b, p->phi, p->y, p->labels, cfg->alpha, daux, dm, p->qdelta * dm,
+                     p->hdev, p->w, p->w2, p->idx, T, jt.jump(s_round, (uint64_t)k * per_epoch + 2 * (uint64_t)D),
+                     ptab, jtab, tr_steps > 0 ? p->trace_dev : nullptr, tr_steps, p->lm_bad};
+    CU(cudaEventRecord(p->ev_in.a, p->stream));
+    CU(launch_lm_inner(ip, p->qbytes, p->stream));
+    CU(cudaEventRecord(p->ev_in.b, p->stream));
+    p->timing.kernel_launches += 2;
+    p->timing.inner_launches += 1;
+    int bad = 0;
+    CU(copy_sync(&bad, p->lm_bad, sizeof(int), cudaMemcpyDeviceToHost, p->stream));
+    float ms = 0;
+    CU(cudaEventElapsedTime(&ms, p->ev_in.a, p->ev_in.b));
+    p->timing.inner_ms += ms;
+    CU(cudaEventElapsedTime(&ms, p->ev_smp.a, p->ev_smp.b));
+    p->timing.sample_ms += ms;
+    if (bad) return fail(HALP_INVALID_INPUT, "quantize: input must be finite");
+    if (tr_steps > 0 && p->trace_host && traced < p->trace_cap) {
+      const int64_t cnt = std::min<int64_t>(tr_steps * D, p->trace_cap - traced);
+      std::vector<long long> tmp(cnt);
+      CU(copy_sync(tmp.data(), p->trace_dev, sizeof(long long) * cnt, cudaMemcpyDeviceToHost, p->stream));
+      for (int64_t q = 0; q < cnt; ++q) p->trace_host[traced + q] = tmp[q];
+      traced += cnt;
+    }
+    p->timing.inner_steps += T;
+    std::swap(p->w, p->w2);
+    rec->inner_lp_vector_ops += (uint64_t)(6 * C) * (uint64_t)T;
+    steps += T;
+  }
+  if (!converged) {
+    double gn, loss, dm, di, daux;
+    int rc = stats(&gn, &loss);
+    if (rc) return rc;
+    CU(copy_sync(wh.data(), p->w, sizeof(double) * D, cudaMemcpyDeviceToHost, p->stream));
+    lm_scales(gn, cfg, p->qdelta, &dm, &di, &daux, false);
+    rc = r.boundary((double)steps / (double)n, wh.data(), loss, gn, dm, true, di, daux);
+    if (rc) return rc;
+    if (gn == 0.0) rec->status = HALP_STATUS_CONVERGED;
+  } else {
+    CU(copy_sync(wh.data(), p->w, sizeof(double) * D, cudaMemcpyDeviceToHost, p->stream));
+  }
+  if (rec->final_iterate) std::memcpy(rec->final_iterate, wh.data(), sizeof(double) * D);
+  rec->steps_taken = steps;
+  return HALP_OK;
+}
+
 int halp_run(halp_problem* p, const halp_config* cfg, halp_record* rec) {
   // lpopt::run_halp (optimizers.cpp:387-459), run_svrg (:258-296) and
   // run_lp_svrg (:336-385): one epoch loop, K1 + K2 at the boundary, K4 + K3
@@ -881,6 +1095,7 @@ int halp_run(halp_problem* p, const halp_config* cfg, halp_record* rec) {
   int rc = validate(p, cfg);
   if (rc) return rc;
   CU(cudaSetDevice(p->device));
+  if (cfg->algorithm == HALP_ALGO_LM_HALP) return run_lm(p, cfg, rec);
   const int algo = cfg->algorithm;
   const bool halp = algo == HALP_ALGO_HALP;
   const bool lp = algo == HALP_ALGO_LP_SVRG || algo == HALP_ALGO_LP_SGD;  // fixed-scale quantized iterate
@@ -1148,8 +1363,14 @@ extern "C" int halp_batch_plan(const halp_batch* b, halp_plan* out) {
   out->fg_vec = 16 / elem_size(b->dtype);
   out->fg_splits = b->splits;
   out->in_ctas = 1;
-  out->in_threads = 128;  // k5_batch: 4 warps per problem, M = D/128 coordinates per thread
-  out->in_per = b->d <= 128 ? 1 : 2;
+  if (batch_warps_per_problem(b->d) == 1) {  // k5_batch_w1: one warp, M = D/32 per lane
+    out->in_threads = 32;
+    const int M = (b->d + 31) / 32;
+    out->in_per = M <= 1 ? 1 : M <= 2 ? 2 : M <= 4 ? 4 : 8;
+  } else {  // k5_batch: 4 warps per problem, M = D/128 coordinates per thread
+    out->in_threads = 128;
+    out->in_per = b->d <= 128 ? 1 : 2;
+  }
   out->in_levels = 1;
   out->fg_split_begin = 0;
   out->fg_split_end = b->splits;

@@ -82,3 +82,40 @@ extern "C" int halp_normals(uint64_t seed, uint64_t stream, int64_t count, doubl
   for (int64_t k = 0; k < count; ++k) out[k] = rng.next_normal();
   return HALP_OK;
 }
+
+// fixed_point.cpp:30-50 quantize_code (host copy for the dataset quantizer)
+static int64_t q_code(double x, double delta, int bits, double u) {
+  const int64_t maxc = bits == 64 ? INT64_MAX : (int64_t)((1ULL << (bits - 1)) - 1);
+  const int64_t minc = bits == 64 ? INT64_MIN : -(int64_t)(1ULL << (bits - 1));
+  const double t = x / delta;
+  if (t >= (double)maxc) return maxc;
+  if (t <= (double)minc) return minc;
+  const double snapped = std::nearbyint(t);
+  if (snapped * delta == x) return (int64_t)snapped;
+  const double fl = std::floor(t);
+  const double frac = t - fl;
+  int64_t code = (int64_t)fl;
+  if (frac > 0.0 && u < frac) ++code;
+  return code;
+}
+
+// objectives.cpp:110-133 quantize_dataset: LPRepr(data_scale(X, bits), bits)
+// with data_scale = max|X| / (2^(bits-1) - 1) (1 for an all-zero X), one
+// stochastic rounding per element from QuantRng(seed, 2) in row order
+extern "C" int halp_quantize_dataset(const double* X, int64_t n, int32_t d, int32_t bits, uint64_t seed,
+                                     int64_t* codes, double* delta) {
+  if (!X || !codes || !delta || n < 0 || d < 0) return HALP_INVALID_INPUT;
+  if (bits < 2 || bits > 64) return HALP_INVALID_INPUT;
+  double max_abs = 0.0;
+  for (int64_t k = 0; k < n * (int64_t)d; ++k) {
+    const double a = std::fabs(X[k]);
+    if (!(a <= max_abs)) max_abs = a;
+  }
+  if (!std::isfinite(max_abs)) return HALP_INVALID_INPUT;
+  const double span = std::ldexp(1.0, bits - 1) - 1.0;
+  const double dl = max_abs == 0.0 ? 1.0 : max_abs / span;
+  QuantRng rng(seed, 2);
+  for (int64_t k = 0; k < n * (int64_t)d; ++k) codes[k] = q_code(X[k], dl, bits, rng.next_uniform());
+  *delta = dl;
+  return HALP_OK;
+}

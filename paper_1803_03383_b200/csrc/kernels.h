@@ -2,6 +2,7 @@
 #pragma once
 #include <cstddef>
 #include <cstdint>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 namespace halp {
@@ -98,6 +99,42 @@ struct InLaunch {
 };
 cudaError_t launch_inner(const InLaunch& L, const InParams& p, cudaStream_t st);
 
+// ---- LM-HALP (k_lm.cu): K7 epoch stats over the quantized rows, K8 integer inner loop ----
+constexpr int kLmMaxD = 4096;  // d*C over one 256-thread CTA, <= 16 coordinates per thread
+struct LmStatsParams {
+  const void* q;  // [n][d] codes (int8 for bits <= 8, int16 for bits <= 16)
+  int64_t n;
+  int d, C, loss;
+  double delta_x;  // data scale
+  const double* y;
+  const int32_t* labels;
+  const double* w;  // w~ [D]
+  int S, split0;
+  double* partials;  // [nsplit_local][D+1]
+  double* phi;       // [n][C] logits at w~
+};
+cudaError_t launch_lm_stats(const LmStatsParams& p, int nblocks, int code_bytes, cudaStream_t st);
+struct LmInnerParams {
+  const void* q;
+  int d, C, loss, bits;
+  const double* phi;
+  const double* y;
+  const int32_t* labels;
+  double alpha, daux, dm, sc;  // sc = delta_x * delta_m (dot_lp's scale)
+  const long long* h;          // [D] codes of Q_i(alpha g~) at delta_inner
+  const double* w;             // w~ [D]
+  double* w_out;               // w~ + to_real(z) after the epoch
+  const int64_t* idx;          // [T] sample indices
+  int64_t T;
+  uint64_t rstate0;            // rounding stream before the first draw of step 0
+  const uint64_t* pow_tab;
+  const uint64_t* jump_tab;    // X^(C(d+1))
+  long long* trace;            // [trace_steps][D] z codes or null
+  int64_t trace_steps;
+  int* bad;                    // 1 if a beta was non-finite (quantize: input must be finite)
+};
+cudaError_t launch_lm_inner(const LmInnerParams& p, int code_bytes, cudaStream_t st);
+
 // ---- K6 synthetic data ----
 struct GenParams {
   int kind;
@@ -142,5 +179,14 @@ struct BatchParams {
   double* w_out;         // [nprob][d] final iterate (the failing update on blow-up)
 };
 cudaError_t launch_batch(const BatchParams& p, int threads, cudaStream_t st);
+// K5 plan: 1 = one warp per problem (k5_batch_w1, M = D/32 per lane), 4 = four
+// warps (k5_batch, M = D/128 per thread); HALP_K5_WARPS overrides
+inline int batch_warps_per_problem(int d) {
+  const char* e = std::getenv("HALP_K5_WARPS");
+  if (e && std::atoi(e) == 4) return 4;
+  if (e && std::atoi(e) == 1) return 1;
+  (void)d;
+  return 1;
+}
 
 }  // namespace halp

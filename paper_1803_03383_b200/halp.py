@@ -115,6 +115,18 @@ def _raise(rc: int, partial: Optional[RunRecord] = None):
 
 
 @dataclass
+class QuantizedExamples:
+    """lpopt::QuantizedExamples (objectives.hpp): the rows of X quantized once
+    for LM-HALP -- int64 codes [n][d] at one scale `delta` and width `bits`,
+    drawn with `seed` on RNG stream 2 (objectives.cpp:110-133)."""
+
+    codes: np.ndarray
+    delta: float
+    bits: int
+    seed: int = 0
+
+
+@dataclass
 class Dataset:
     """lpopt::Dataset (objectives.hpp:23-33); X row-major n x d."""
 
@@ -122,6 +134,7 @@ class Dataset:
     targets: Optional[object] = None
     labels: Optional[object] = None
     num_classes: int = 0
+    quantized: Optional[QuantizedExamples] = None
 
     def n(self) -> int:
         return int(self.X.shape[0])
@@ -212,10 +225,17 @@ class Objective:
         idbuf = None
         if nccl_id is not None:
             idbuf = C.create_string_buffer(bytes(nccl_id), 128)
+        qptr, qbits, qdelta = None, 0, 0.0
+        if ds.quantized is not None:
+            qc = np.ascontiguousarray(ds.quantized.codes, dtype=np.int64)
+            if qc.shape != (int(X.shape[0]), int(X.shape[1])):
+                raise InvalidInputError("lm_halp: quantized rows do not match the dataset shape")
+            self._keep.append(qc)
+            qptr, qbits, qdelta = qc.ctypes.data, int(ds.quantized.bits), float(ds.quantized.delta)
         desc = A.ProblemDesc(xptr, dtype, A.MEM_DEVICE if dev else A.MEM_HOST, int(X.shape[0]), int(X.shape[1]),
                              int(self._loss), C_, yptr, lptr, self._l2, device, world_size, rank,
                              C.cast(idbuf, C.c_void_p) if idbuf is not None else None,
-                             2 if collective == "host" else 1 if collective else 0)
+                             2 if collective == "host" else 1 if collective else 0, qptr, qbits, qdelta)
         h = C.c_void_p()
         rc = A.lib().halp_problem_create(C.byref(desc), C.byref(h))
         if rc:
@@ -357,7 +377,8 @@ def _to_c_config(cfg: OptimizerConfig, keep: list) -> A.Config:
 
 def _record(rec: A.Record, rows, fin: np.ndarray) -> RunRecord:
     out = RunRecord()
-    out.rows = [MetricRow(r.pass_, r.seconds, r.loss, r.grad_norm, r.delta, r.iterate_hash) for r in rows[: rec.rows_n]]
+    out.rows = [MetricRow(r.pass_, r.seconds, r.loss, r.grad_norm, r.delta, r.iterate_hash, r.delta_inner, r.delta_aux)
+                for r in rows[: rec.rows_n]]
     out.final_iterate = fin
     out.status = _STATUS[rec.status]
     out.inner_fp_vector_ops = rec.inner_fp_vector_ops
@@ -413,6 +434,45 @@ def run_lp_sgd(obj: Objective, cfg: OptimizerConfig, trace: Optional[np.ndarray]
     return _run_algo(obj, cfg, Algorithm.LpSgd, trace)
 
 
+def run_lm_halp(obj: Objective, cfg: OptimizerConfig, trace: Optional[np.ndarray] = None) -> RunRecord:
+    """lpopt::run_lm_halp (optimizers.cpp:461-627): HALP's linear-model form
+    with an integer-only inner loop over the dataset's quantized rows
+    (obj.dataset().quantized, see quantize_dataset) -- K7 epoch stats + K8
+    integer inner loop (k_lm.cu).  `trace` receives the z codes per step."""
+    return _run_algo(obj, cfg, Algorithm.LmHalp, trace)
+
+
+def data_scale(X, bits: int) -> float:
+    """objectives.cpp:112-122: max|X| / (2^(bits-1) - 1), 1 for an all-zero X"""
+    if bits < 2 or bits > 64:
+        raise InvalidInputError("data_scale: bits must be in [2, 64]")
+    X = np.asarray(X, dtype=np.float64)
+    m = float(np.max(np.abs(X))) if X.size else 0.0
+    if not math.isfinite(m):
+        raise InvalidInputError("data_scale: matrix has non-finite entries")
+    return 1.0 if m == 0.0 else m / (math.ldexp(1.0, bits - 1) - 1.0)
+
+
+def quantize_dataset(ds: Dataset, bits: int, seed: int) -> None:
+    """objectives.cpp:124-133: quantize every row of ds.X once (stream 2 of
+    `seed`, row-major draws) and attach the codes as ds.quantized (host, the
+    library's restatement of the reference's quantize_code)."""
+    X = ds.X
+    if _is_torch_cuda(X):
+        X = X.double().cpu().numpy()
+    elif np.asarray(X).dtype == np.uint16:  # bf16 bits
+        X = (np.asarray(X, dtype=np.uint32) << 16).view(np.float32)
+    X = np.ascontiguousarray(X, dtype=np.float64)
+    data_scale(X, bits)  # the reference's checks and messages
+    codes = np.empty(X.shape, dtype=np.int64)
+    dl = C.c_double()
+    rc = A.lib().halp_quantize_dataset(X.ctypes.data, X.shape[0], X.shape[1], bits, int(seed) & (2**64 - 1),
+                                       codes.ctypes.data, C.byref(dl))
+    if rc:
+        raise InvalidInputError("quantize_dataset: invalid input")
+    ds.quantized = QuantizedExamples(codes, dl.value, int(bits), int(seed))
+
+
 def _run_algo(obj: Objective, cfg: OptimizerConfig, algo: Algorithm, trace) -> RunRecord:
     if cfg.init is not None and np.asarray(cfg.init).size not in (0, obj.dim()):
         raise InvalidInputError("optimizer: init length does not match objective")
@@ -444,20 +504,29 @@ def _run_algo(obj: Objective, cfg: OptimizerConfig, algo: Algorithm, trace) -> R
 
 
 def run(obj: Objective, cfg: OptimizerConfig) -> RunRecord:
-    """lpopt::run (optimizers.cpp:629-639): Halp, Svrg, LpSvrg, Sgd and LpSgd
-    run on the B200; LmHalp is outside this build's scope."""
+    """lpopt::run (optimizers.cpp:629-639): every algorithm of the reference
+    runs on the B200 (LmHalp needs the dataset's quantized rows)."""
     fns = {Algorithm.Halp: run_halp, Algorithm.Svrg: run_svrg, Algorithm.LpSvrg: run_lp_svrg,
-           Algorithm.Sgd: run_sgd, Algorithm.LpSgd: run_lp_sgd}
+           Algorithm.Sgd: run_sgd, Algorithm.LpSgd: run_lp_sgd, Algorithm.LmHalp: run_lm_halp}
     if cfg.algorithm in fns:
         return fns[Algorithm(cfg.algorithm)](obj, cfg)
     raise UnsupportedError(f"algorithm {Algorithm(cfg.algorithm).name} is not on the B200 path")
 
 
 def run_prepared(obj: Objective, cfg: OptimizerConfig, data_seed: int = 0) -> RunRecord:
-    """harness.cpp:296-312: a diverged run is returned, not raised.  data_seed
-    only feeds LM-HALP's dataset quantization (not on the B200 path)."""
-    del data_seed
+    """harness.cpp:296-312: a diverged run is returned, not raised; LM-HALP on a
+    dataset without codes of the config's width first quantizes a copy with
+    data_seed."""
     try:
+        if cfg.algorithm == Algorithm.LmHalp:
+            q = obj.ds.quantized
+            if q is None or q.bits != cfg.bits:
+                import copy as _copy
+
+                ds = _copy.copy(obj.ds)
+                quantize_dataset(ds, cfg.bits, data_seed)
+                prepared = Objective(ds, obj.loss_family(), obj.l2(), device=obj.device)
+                return run(prepared, cfg)
         return run(obj, cfg)
     except DivergenceError as e:
         return e.partial
