@@ -38,6 +38,14 @@ enum class LossFamily { Squared, Softmax };
 enum class Algorithm { Sgd, Svrg, LpSgd, LpSvrg, Halp, LmHalp };
 enum class EpochOption { LastIterate, SampledIterate };
 
+// lpopt::QuantizedExamples (objectives.hpp): LM-HALP's integer rows, one scale
+struct QuantizedExamples {
+  std::vector<std::int64_t> codes;  // row-major n x d
+  double delta = 0.0;
+  int bits = 0;
+  std::uint64_t seed = 0;
+};
+
 struct Dataset {
   std::vector<double> X;      // row-major n x d (the reference holds it column-major)
   long n = 0;
@@ -45,6 +53,8 @@ struct Dataset {
   std::vector<double> targets;
   std::vector<int> labels;
   int num_classes = 0;
+  bool has_quantized = false;  // std::optional<QuantizedExamples> quantized in the reference
+  QuantizedExamples quantized;
 };
 
 struct MetricRow {
@@ -119,6 +129,13 @@ class Objective {
     desc.l2 = l2;
     desc.device = device;
     desc.world_size = 1;
+    if (ds_.has_quantized) {
+      if ((long)ds_.quantized.codes.size() != ds_.n * (long)ds_.d)
+        throw InvalidInputError("lm_halp: quantized rows do not match the dataset shape");
+      desc.qcodes = ds_.quantized.codes.data();
+      desc.qbits = ds_.quantized.bits;
+      desc.qdelta = ds_.quantized.delta;
+    }
     const int rc = halp_problem_create(&desc, &h_);
     if (rc) detail::raise(rc);
     outputs_ = loss == LossFamily::Squared ? 1 : ds_.num_classes;
@@ -201,6 +218,8 @@ inline RunRecord run_algo(const Objective& obj, const OptimizerConfig& cfg, int 
       r.grad_norm = rows[i].grad_norm;
       r.delta = rows[i].delta;
       r.iterate_hash = rows[i].iterate_hash;
+      r.delta_inner = rows[i].delta_inner;
+      r.delta_aux = rows[i].delta_aux;
       out.rows.push_back(r);
     }
     out.status = rec.status == HALP_STATUS_CONVERGED ? "converged" : rec.status == HALP_STATUS_DIVERGED ? "diverged" : "ok";
@@ -240,7 +259,26 @@ inline RunRecord run_lp_sgd(const Objective& obj, const OptimizerConfig& cfg) {
   return detail::run_algo(obj, cfg, HALP_ALGO_LP_SGD);
 }
 
-// lpopt::run (optimizers.cpp:629-639): the branches this library runs on the B200
+// lpopt::run_lm_halp (optimizers.cpp:461-627): the integer inner loop over
+// obj.dataset().quantized (bits <= 16 and d * classes <= 4096 on the B200)
+inline RunRecord run_lm_halp(const Objective& obj, const OptimizerConfig& cfg) {
+  if (cfg.lm_bypass_aux_quant) throw UnsupportedError("lm_halp: the bypass test hook is not on the B200 path");
+  return detail::run_algo(obj, cfg, HALP_ALGO_LM_HALP);
+}
+
+// objectives.cpp:110-133 quantize_dataset: attaches the codes to ds
+inline void quantize_dataset(Dataset& ds, int bits, std::uint64_t seed) {
+  QuantizedExamples q;
+  q.codes.resize((size_t)ds.n * ds.d);
+  q.bits = bits;
+  q.seed = seed;
+  if (halp_quantize_dataset(ds.X.data(), ds.n, ds.d, bits, seed, q.codes.data(), &q.delta))
+    throw InvalidInputError("data_scale: bits must be in [2, 64] and the matrix finite");
+  ds.quantized = std::move(q);
+  ds.has_quantized = true;
+}
+
+// lpopt::run (optimizers.cpp:629-639)
 inline RunRecord run(const Objective& obj, const OptimizerConfig& cfg) {
   switch (cfg.algorithm) {
     case Algorithm::Halp: return run_halp(obj, cfg);
@@ -248,13 +286,22 @@ inline RunRecord run(const Objective& obj, const OptimizerConfig& cfg) {
     case Algorithm::LpSvrg: return run_lp_svrg(obj, cfg);
     case Algorithm::Sgd: return run_sgd(obj, cfg);
     case Algorithm::LpSgd: return run_lp_sgd(obj, cfg);
-    default: throw UnsupportedError("algorithm not on the B200 path (LmHalp)");
+    case Algorithm::LmHalp: return run_lm_halp(obj, cfg);
   }
+  throw InvalidInputError("unknown algorithm enum value");
 }
 
-// harness.cpp:296-312
-inline RunRecord run_prepared(const Objective& obj, const OptimizerConfig& cfg) {
+// harness.cpp:296-312 (LM-HALP on a dataset without codes of the run's width
+// quantizes a copy with data_seed first)
+inline RunRecord run_prepared(const Objective& obj, const OptimizerConfig& cfg, std::uint64_t data_seed = 0) {
   try {
+    if (cfg.algorithm == Algorithm::LmHalp &&
+        (!obj.dataset().has_quantized || obj.dataset().quantized.bits != cfg.bits)) {
+      Dataset ds = obj.dataset();
+      quantize_dataset(ds, cfg.bits, data_seed);
+      const Objective prepared(std::move(ds), obj.loss_family(), obj.l2());
+      return run(prepared, cfg);
+    }
     return run(obj, cfg);
   } catch (const DivergenceError& e) {
     return e.partial;

@@ -180,13 +180,14 @@ struct BatchParams {
 };
 cudaError_t launch_batch(const BatchParams& p, int threads, cudaStream_t st);
 // K5 plan: 1 = one warp per problem (k5_batch_w1, M = D/32 per lane), 4 = four
-// warps (k5_batch, M = D/128 per thread); HALP_K5_WARPS overrides
+// warps (k5_batch, M = D/128 per thread); HALP_K5_WARPS overrides.  Measured on
+// B200 (tools/gpu_r2_lm.sh): the 663-run 1000 x 64 grid 20.5 ms (1 warp) vs
+// 35.9 ms (4 warps); C5's 512 x (4096 x 128) 135 ms (1 warp) vs 84.6 ms (4 warps)
 inline int batch_warps_per_problem(int d) {
   const char* e = std::getenv("HALP_K5_WARPS");
   if (e && std::atoi(e) == 4) return 4;
   if (e && std::atoi(e) == 1) return 1;
-  (void)d;
-  return 1;
+  return d <= 64 ? 1 : 4;
 }
 
 }  // namespace halp

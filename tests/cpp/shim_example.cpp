@@ -35,6 +35,15 @@ int main(int argc, char** argv) {
     for (const auto& r : rec.rows)
       std::printf("%.17g %.17g %.17g %.17g %llu\n", r.pass, r.loss, r.grad_norm, r.delta,
                   (unsigned long long)r.iterate_hash);
+    // LM-HALP through run_prepared: the dataset is quantized on the fly
+    lpopt_b200::OptimizerConfig lm = cfg;
+    lm.algorithm = lpopt_b200::Algorithm::LmHalp;
+    lm.epochs = 2;
+    const auto lrec = lpopt_b200::run_prepared(obj, lm, 7);
+    if (lrec.rows.size() != 3 || !(lrec.rows.back().loss < lrec.rows.front().loss) || !(lrec.rows[0].delta_aux > 0.0))
+      return 4;
+    std::printf("lm %.17g %.17g %.17g\n", lrec.rows.back().loss, lrec.rows.back().delta_inner,
+                lrec.rows.back().delta_aux);
     // the reference's error behaviour: invalid configs throw InvalidInputError
     cfg.mu = 0.0;
     try {

@@ -38,7 +38,17 @@ def test_shim_matches_python_api(oracle, tmp_path):
         fh.write(np.int64(1000).tobytes() + np.int32(100).tobytes() + X.tobytes() + y.tobytes())
     out = subprocess.run([EXE, str(f)], capture_output=True, text=True)
     assert out.returncode == 0, out.stderr
-    cpp_rows = [line.split() for line in out.stdout.strip().splitlines()]
+    lines = out.stdout.strip().splitlines()
+    lm_line = [l.split() for l in lines if l.startswith("lm ")]
+    cpp_rows = [line.split() for line in lines if not line.startswith("lm ")]
+    # the C++ run_prepared(LmHalp, data_seed 7) equals the Python one
+    ds = H.Dataset(X, targets=y)
+    H.quantize_dataset(ds, 8, 7)
+    lrec = H.run_lm_halp(H.Objective(ds, H.LossFamily.Squared, 0.0),
+                         H.OptimizerConfig(algorithm=H.Algorithm.LmHalp, alpha=5e-3, epochs=2, inner_steps=2000,
+                                           bits=8, mu=3.0, seed=1))
+    assert len(lm_line) == 1 and float(lm_line[0][1]) == lrec.rows[-1].loss
+    assert float(lm_line[0][2]) == lrec.rows[-1].delta_inner and float(lm_line[0][3]) == lrec.rows[-1].delta_aux
     g = H.Objective(H.Dataset(X, targets=y), H.LossFamily.Squared, 0.0)
     rec = H.run_halp(g, H.OptimizerConfig(algorithm=H.Algorithm.Halp, alpha=5e-3, epochs=4, inner_steps=2000,
                                           bits=8, mu=3.0, seed=1))
