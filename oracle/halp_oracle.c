@@ -745,11 +745,24 @@ static void mirror_inner_dots(const double* x, const double* wa, const double* w
     }
   }
   if (C == 1) {
-    /* lane l sums warps l, l+32, ... sequentially from 0.0; lane butterfly */
+    /* in_levels 2: each CTA's warps summed in warp order first (one record
+     * per CTA); then lane l sums records l, l+32, ... sequentially from 0.0;
+     * lane butterfly */
+    int nrec = ngw;
+    if (pl->in_levels == 2) {
+      const int nw = T / 32;
+      for (int c = 0; c < NC; ++c) {
+        double sa = wsa[c * nw], sb = wsb[c * nw];
+        for (int q = 1; q < nw; ++q) { sa = sa + wsa[c * nw + q]; sb = sb + wsb[c * nw + q]; }
+        wsa[c] = sa;
+        wsb[c] = sb;
+      }
+      nrec = NC;
+    }
     double va[32], vb[32];
     for (int l = 0; l < 32; ++l) {
       double aa = 0.0, ab = 0.0;
-      for (int q = l; q < ngw; q += 32) { aa = aa + wsa[q]; ab = ab + wsb[q]; }
+      for (int q = l; q < nrec; q += 32) { aa = aa + wsa[q]; ab = ab + wsb[q]; }
       va[l] = aa;
       vb[l] = ab;
     }

@@ -260,6 +260,8 @@ struct halp_problem {
 
 namespace {
 
+constexpr int kDefaultInLevels = 1;  // measured on B200: see DESIGN.md 8
+
 struct KernelPlan {
   FgLaunch fg{};
   InLaunch in{};
@@ -393,6 +395,13 @@ int plan_for(int64_t n, int d, int C, int dtype, KernelPlan* kp) {
   if (T3 > 256) return fail(HALP_UNSUPPORTED, "inner loop: bad cluster plan");
   const int nslots = 2 * C + 1;
   kp->in = InLaunch{dtype, NC, T3, M, (int)std::max<int64_t>(4, next_pow2(nslots))};
+  // squared loss on a cluster: the CTA's warps pre-reduced in shared memory, one
+  // record per CTA in the DSMEM exchange (k_inner.cu LV2; HALP_IN_LEVELS overrides)
+  {
+    const int lv = (int)env_int("HALP_IN_LEVELS", 0);
+    const bool can = C == 1 && NC > 1 && T3 >= 64;
+    kp->in.levels = can ? (lv == 1 ? 1 : lv == 2 ? 2 : kDefaultInLevels) : 1;
+  }
   return HALP_OK;
 }
 

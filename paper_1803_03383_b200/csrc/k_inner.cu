@@ -143,14 +143,16 @@ struct K3Layout {
 // (arithmetic never produces it; NaN logits make receivers rescan for it).
 constexpr long long kFlagBits = 0x7FF4A1B2C3D4E5F6LL;
 
-template <class Tx, int M, bool CL, int KIND, bool BASE0>
+template <class Tx, int M, bool CL, int KIND, bool BASE0, bool LV2>
 __global__ void __launch_bounds__(256, 1) k3_inner(InParams p) {
+  static_assert(!LV2 || (KIND == 0 && CL), "two-level exchange: squared loss on a cluster");
   constexpr int NSLOT = K3Layout<KIND>::NSLOT;
   constexpr int FLAG = K3Layout<KIND>::FLAG;
   constexpr bool SQ = KIND == 0;
   __shared__ uint64_t jt[2048];
   __shared__ __align__(8) uint64_t mbar[2];
   __shared__ __align__(16) double gsc[2][8][32];  // softmax gathers: [parity][warp][lane]
+  __shared__ __align__(16) double ctar[2][8][2];  // LV2: this CTA's warp records [parity][warp]
   extern __shared__ __align__(16) double xbuf_dyn[];  // [2][NGW][NSLOT]
 
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, NW = blockDim.x >> 5;
@@ -158,6 +160,7 @@ __global__ void __launch_bounds__(256, 1) k3_inner(InParams p) {
   const int NC = CL ? (int)gridDim.x : 1;
   const int NGW = NC * NW;
   const int gw = (int)rank * NW + wid;
+  const int NREC = LV2 ? NC : NGW;  // records per exchange (LV2: one per CTA)
   const int d = p.d, C = p.C, D = p.D, ld = p.ld;
   const int64_t k0 = ((int64_t)rank * blockDim.x + tid) * M;
   const Tx* X = reinterpret_cast<const Tx*>(p.X);
@@ -165,7 +168,7 @@ __global__ void __launch_bounds__(256, 1) k3_inner(InParams p) {
   const int WC = 32 * M;  // coordinates per warp
   const int PAR_STRIDE = NGW * NSLOT;  // doubles between the two parity buffers
   auto XB = [&](int par_, int q_, int slot_) -> double& { return xbuf_dyn[par_ * PAR_STRIDE + q_ * NSLOT + slot_]; };
-  const uint32_t bytes_step = KIND == 0 ? (uint32_t)NGW * 16u
+  const uint32_t bytes_step = KIND == 0 ? (uint32_t)NREC * 16u
                               : KIND == 1 ? (uint32_t)NGW * 32u
                                           : (uint32_t)NGW * (uint32_t)(2 * C + 1) * 8u;
 
@@ -187,7 +190,7 @@ __global__ void __launch_bounds__(256, 1) k3_inner(InParams p) {
   if (CL && KIND == 0) {
     const int r0 = lane & 15;
     s0ok = lane < 16 && r0 < NC;
-    ra0 = mapa_u32(&XB(0, gw, 0), (uint32_t)(s0ok ? r0 : 0));
+    ra0 = mapa_u32(&XB(0, LV2 ? (int)rank : gw, 0), (uint32_t)(s0ok ? r0 : 0));
     rb0 = mapa_u32(&mbar[0], (uint32_t)(s0ok ? r0 : 0));
   } else if (CL && KIND == 1) {
     const int slot = 2 * (lane >> 4);
@@ -340,7 +343,24 @@ __global__ void __launch_bounds__(256, 1) k3_inner(InParams p) {
       v = v + __shfl_xor_sync(0xffffffffu, v, 1);
       double vp = __shfl_xor_sync(0xffffffffu, v, 16);
       if (flag) v = vp = fnan;
-      if (CL) {
+      if constexpr (LV2) {
+        // this CTA's warps summed in order by warp 0, one record per CTA to every CTA
+        if (lane == 0) *reinterpret_cast<double2*>(&ctar[par][wid][0]) = make_double2(v, vp);
+        asm volatile("bar.sync 1, %0;" ::"r"(NW * 32) : "memory");
+        if (wid == 0) {
+          double2 r = *reinterpret_cast<const double2*>(&ctar[par][0][0]);
+          bool fl2 = __double_as_longlong(r.x) == kFlagBits;
+          for (int q = 1; q < NW; ++q) {
+            const double2 rq = *reinterpret_cast<const double2*>(&ctar[par][q][0]);
+            fl2 |= __double_as_longlong(rq.x) == kFlagBits;
+            r.x = r.x + rq.x;
+            r.y = r.y + rq.y;
+          }
+          if (fl2) r.x = r.y = fnan;
+          const uint32_t xo = par ? xb_par_off : 0u, mo = par ? mb_par_off : 0u;
+          if (s0ok) st_async_v2f64(ra0 + xo, r.x, r.y, rb0 + mo);
+        }
+      } else if (CL) {
         const uint32_t xo = par ? xb_par_off : 0u, mo = par ? mb_par_off : 0u;
         if (s0ok) st_async_v2f64(ra0 + xo, v, vp, rb0 + mo);
       } else {
@@ -426,7 +446,7 @@ __global__ void __launch_bounds__(256, 1) k3_inner(InParams p) {
 #pragma unroll
       for (int j = 0; j < kMaxWarpsPerCluster / 32; ++j) {
         const int q = lane + 32 * j;
-        if (q < NGW) {
+        if (q < NREC) {
           if constexpr (KIND == 2) f |= xbp[q * NSLOT + FLAG] != 0.0;
           else f |= __double_as_longlong(xbp[q * NSLOT]) == kFlagBits;
         }
@@ -469,7 +489,7 @@ __global__ void __launch_bounds__(256, 1) k3_inner(InParams p) {
 #pragma unroll
       for (int j = 0; j < kMaxWarpsPerCluster / 32; ++j) {
         const int q = lane + 32 * j;
-        if (q < NGW) {
+        if (q < NREC) {
           const double2 v = *reinterpret_cast<const double2*>(xbp + q * NSLOT);
           sa = sa + v.x;
           sb = sb + v.y;
@@ -477,12 +497,12 @@ __global__ void __launch_bounds__(256, 1) k3_inner(InParams p) {
       }
       fl = isnan(sa) || isnan(sb);
       K3_MARK(8);
-      // lanes >= NGW hold +0.0: butterfly levels that only add zeros are skipped
-      for (int o = (NGW >= 32 ? 16 : NGW > 1 ? (1 << (31 - __clz(NGW - 1))) : 0); o >= 1; o >>= 1) {
+      // lanes >= NREC hold +0.0: butterfly levels that only add zeros are skipped
+      for (int o = (NREC >= 32 ? 16 : NREC > 1 ? (1 << (31 - __clz(NREC - 1))) : 0); o >= 1; o >>= 1) {
         sa = sa + __shfl_xor_sync(0xffffffffu, sa, o);
         sb = sb + __shfl_xor_sync(0xffffffffu, sb, o);
       }
-      if (NGW < 32) {
+      if (NREC < 32) {
         sa = __shfl_sync(0xffffffffu, sa, 0);
         sb = __shfl_sync(0xffffffffu, sb, 0);
       }
@@ -625,7 +645,7 @@ static cudaError_t launch_in_b(const InLaunch& L, const InParams& p, cudaStream_
   if (L.ctas * L.threads / 32 > kMaxWarpsPerCluster) return cudaErrorInvalidConfiguration;
   const size_t smem = sizeof(double) * 2 * (size_t)(L.ctas * L.threads / 32) * K3Layout<KIND>::NSLOT;
   if (L.ctas == 1) {
-    auto kern = k3_inner<Tx, M, false, KIND, BASE0>;
+    auto kern = k3_inner<Tx, M, false, KIND, BASE0, false>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     if (L.dry) return cudaSuccess;
@@ -633,7 +653,9 @@ static cudaError_t launch_in_b(const InLaunch& L, const InParams& p, cudaStream_
     return cudaGetLastError();
   }
   if (L.ctas > 16) return cudaErrorInvalidConfiguration;
-  auto kern = k3_inner<Tx, M, true, KIND, BASE0>;
+  auto kern = k3_inner<Tx, M, true, KIND, BASE0, false>;
+  if constexpr (KIND == 0)
+    if (L.levels == 2) kern = k3_inner<Tx, M, true, KIND, BASE0, true>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   if (e != cudaSuccess) return e;
   e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
