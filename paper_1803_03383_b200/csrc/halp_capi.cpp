@@ -716,10 +716,14 @@ int halp_problem_create(const halp_problem_desc* desc, halp_problem** out) {
     // padding columns must be zero: kernels process whole 16-byte groups
     if (p->ld != p->d && cudaMemsetAsync(p->X, 0, bytes, p->stream) != cudaSuccess)
       return bail(fail(HALP_CUDA_ERROR, "cudaMemset(X) failed"));
-    // async on the problem's stream (a DMA straight from pinned host memory)
-    if (cudaMemcpy2DAsync(p->X, (size_t)p->ld * es, desc->X, (size_t)p->d * es, (size_t)p->d * es, (size_t)p->n,
-                          dev_in ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, p->stream) != cudaSuccess)
-      return bail(fail(HALP_CUDA_ERROR, "copy of X to the device failed"));
+    // async on the problem's stream (a DMA straight from pinned host memory); a
+    // plain 1-D copy when the rows need no padding
+    const cudaMemcpyKind kind = dev_in ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    const cudaError_t ce2 =
+        p->ld == p->d ? cudaMemcpyAsync(p->X, desc->X, bytes, kind, p->stream)
+                      : cudaMemcpy2DAsync(p->X, (size_t)p->ld * es, desc->X, (size_t)p->d * es, (size_t)p->d * es,
+                                          (size_t)p->n, kind, p->stream);
+    if (ce2 != cudaSuccess) return bail(fail(HALP_CUDA_ERROR, "copy of X to the device failed"));
     if (!dev_in) p->create_h2d += (int64_t)p->n * p->d * es;
   }
   if (p->loss == HALP_SQUARED) {

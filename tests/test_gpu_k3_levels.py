@@ -19,25 +19,25 @@ def H():
     return H
 
 
-@pytest.mark.parametrize("nc,m", [(16, 2), (8, 2), (4, 4)])
+@pytest.mark.parametrize("nc,m", [(16, 2), (8, 4), (4, 4)])
 def test_two_level_bitexact(H, oracle, monkeypatch, nc, m):
     monkeypatch.setenv("HALP_IN_LEVELS", "2")
     monkeypatch.setenv("HALP_IN_NC", str(nc))
     monkeypatch.setenv("HALP_IN_M", str(m))
-    X, y = oracle.generate("regression", 4096, 1024, dtype="f32", noise_sd=0.1, seed=3)
+    X, y = oracle.generate("regression", 4096, 4096, dtype="f32", noise_sd=0.1, seed=3)
     g = H.Objective(H.Dataset(X, targets=y), H.LossFamily.Squared, 1e-5)
     plan = g.oracle_plan()
     assert plan["in_levels"] == 2 and plan["in_ctas"] == nc
     cfg = dict(alpha=2e-4, epochs=2, inner_steps=1500, bits=16, mu=1.0, seed=7)
-    steps = 500
-    tr = np.zeros(steps * 1024, dtype=np.int64)
+    steps = 300
+    tr = np.zeros(steps * 4096, dtype=np.int64)
     rec = H.run_halp(g, H.OptimizerConfig(algorithm=H.Algorithm.Halp, **cfg), trace=tr)
     o = oracle.OracleObjective(X, y=y, l2=1e-5)
     orec = oracle.run_halp(o, oracle.OracleConfig(**cfg), plan=plan, trace_steps=steps)
     assert [(r.loss, r.grad_norm, r.delta, r.iterate_hash) for r in rec.rows] == \
         [(r["loss"], r["grad_norm"], r["delta"], r["iterate_hash"]) for r in orec.rows]
     assert np.array_equal(rec.final_iterate, orec.final_iterate)
-    assert np.array_equal(tr.reshape(steps, 1024), orec.trace)
+    assert np.array_equal(tr.reshape(steps, 4096), orec.trace)
     # blow-up mid-epoch: same partial record as the oracle
     bad = dict(cfg, alpha=1e300)
     with pytest.raises(H.DivergenceError) as e:
