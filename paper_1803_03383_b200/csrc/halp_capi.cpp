@@ -95,7 +95,8 @@ ShardPlan make_shard_plan(int64_t n, int d, int C, int dtype, int world, int ran
   const double xbytes = (double)n * d * elem_size(dtype);
   const double budget = std::max(xbytes / 8.0, 2.0 * (1 << 20));
   int64_t S = 1;
-  while (S * 2 <= 4096 && S * 2 <= std::max<int64_t>(1, n / 2) && (double)(S * 2) * D1 * 8.0 <= budget) S *= 2;
+  const int64_t smax = std::max<int64_t>(1, env_int("HALP_FG_MAX_SPLITS", 4096));  // experiment knob
+  while (S * 2 <= smax && S * 2 <= std::max<int64_t>(1, n / 2) && (double)(S * 2) * D1 * 8.0 <= budget) S *= 2;
   if (S < world) S = next_pow2(world);
   sp.S = S;
   sp.split_begin = S / world * rank;

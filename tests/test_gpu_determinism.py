@@ -25,7 +25,7 @@ def sig(rec):
     return [(r.loss, r.grad_norm, r.delta, r.iterate_hash) for r in rec.rows], rec.final_iterate.tobytes()
 
 
-@pytest.mark.parametrize("plan", ["1:0:1", "4:2:1", "16:2:1", "16:2:2", "8:4:2"])
+@pytest.mark.parametrize("plan", ["0:0:1", "4:2:1", "16:2:1", "16:2:2", "8:4:2"])
 def test_k1_k3_repeatable(H, oracle, monkeypatch, plan):
     nc, m, lv = plan.split(":")
     monkeypatch.setenv("HALP_IN_NC", nc)
@@ -47,16 +47,25 @@ def test_k1_k3_repeatable(H, oracle, monkeypatch, plan):
     assert first[0] == [(r["loss"], r["grad_norm"], r["delta"], r["iterate_hash"]) for r in orec.rows]
 
 
-def test_softmax_cluster_and_blowup_repeatable(H, oracle):
-    X, lab = oracle.generate("softmax", 3000, 784, num_classes=10, dtype="f32", density=0.2, seed=1)
-    g = H.Objective(H.Dataset(X, labels=lab, num_classes=10), H.LossFamily.Softmax, 1e-4)
-    cfg = H.OptimizerConfig(algorithm=H.Algorithm.Halp, alpha=0.01, epochs=1, inner_steps=2000, bits=8, mu=2.5, seed=2)
-    bad = H.OptimizerConfig(algorithm=H.Algorithm.Halp, alpha=1e300, epochs=1, inner_steps=2000, bits=8, mu=2.5, seed=2)
+def test_softmax_cluster_and_blowup_repeatable(H, oracle, monkeypatch):
+    monkeypatch.setenv("HALP_IN_NC", "4")
+    monkeypatch.setenv("HALP_IN_M", "2")
+    rng = np.random.default_rng(5)
+    X = (rng.random((400, 300)) * 4.0).astype(np.float32)
+    lab = rng.integers(0, 3, 400).astype(np.int32)
+    g = H.Objective(H.Dataset(X, labels=lab, num_classes=3), H.LossFamily.Softmax, 1e-4)
+    cfg = H.OptimizerConfig(algorithm=H.Algorithm.Halp, alpha=0.01, epochs=2, inner_steps=500, bits=8, mu=2.0, seed=4)
+    bad = H.OptimizerConfig(algorithm=H.Algorithm.Halp, alpha=1.5e308, epochs=2, inner_steps=50, bits=8, mu=2.0,
+                            seed=4)
     first = sig(H.run_halp(g, cfg))
+    blow = None
     for i in range(REPS):
         assert sig(H.run_halp(g, cfg)) == first, i
-        with pytest.raises(H.DivergenceError):  # every CTA leaves through the blow-up path
+        with pytest.raises(H.DivergenceError) as e:  # every CTA leaves through the blow-up path
             H.run_halp(g, bad)
+        b = [(r.pass_, r.iterate_hash) for r in e.value.partial.rows]
+        blow = blow or b
+        assert b == blow, i
 
 
 def test_k1_bf16_two_class_repeatable(H, oracle):

@@ -39,7 +39,7 @@ def test_two_level_bitexact(H, oracle, monkeypatch, nc, m):
     assert np.array_equal(rec.final_iterate, orec.final_iterate)
     assert np.array_equal(tr.reshape(steps, 4096), orec.trace)
     # blow-up mid-epoch: same partial record as the oracle
-    bad = dict(cfg, alpha=1e300)
+    bad = dict(cfg, alpha=1e308)  # |alpha g~| overflows at step 0
     with pytest.raises(H.DivergenceError) as e:
         H.run_halp(g, H.OptimizerConfig(algorithm=H.Algorithm.Halp, **bad))
     orec = oracle.run_halp(o, oracle.OracleConfig(**bad), plan=plan)

@@ -130,5 +130,6 @@ def test_validation(H, oracle):
     with pytest.raises(H.InvalidInputError, match="bits must be in"):
         H.run(g, H.OptimizerConfig(algorithm=H.Algorithm.LpSvrg, delta=0.1, bits=1))
     H.run(g, H.OptimizerConfig(algorithm=H.Algorithm.Svrg, mu=0.0, bits=1))  # SVRG checks neither
-    with pytest.raises(H.UnsupportedError):
+    # LmHalp is bit-centred: validate_config rejects mu = 0 first (optimizers.cpp:69-75)
+    with pytest.raises(H.InvalidInputError, match="mu must be positive"):
         H.run(g, H.OptimizerConfig(algorithm=H.Algorithm.LmHalp))
