@@ -1381,6 +1381,10 @@ extern "C" int halp_batch_plan(const halp_batch* b, halp_plan* out) {
     out->in_threads = 32;
     const int M = (b->d + 31) / 32;
     out->in_per = M <= 1 ? 1 : M <= 2 ? 2 : M <= 4 ? 4 : 8;
+  } else if (batch_warps_per_problem(b->d) == 2) {  // k5_batch<.., 2>: M = D/64 per thread
+    out->in_threads = 64;
+    const int M = (b->d + 63) / 64;
+    out->in_per = M <= 1 ? 1 : M <= 2 ? 2 : 4;
   } else {  // k5_batch: 4 warps per problem, M = D/128 coordinates per thread
     out->in_threads = 128;
     out->in_per = b->d <= 128 ? 1 : 2;

@@ -35,7 +35,7 @@
 
 namespace halp {
 
-constexpr int kBatchMaxM = 2;     // D <= 256 over 128 threads
+constexpr int kBatchMaxM = 4;     // D <= 256 over 64 threads
 constexpr int kP = 4;             // sample-row prefetch distance (steps)
 constexpr int kBatchMaxLev = 16;  // splits per warp <= 2^15
 
@@ -86,8 +86,10 @@ __device__ __forceinline__ uint64_t fnv1a_doubles(const double* v, int len) {
 }
 
 // NG groups of V features per lane (NG*V*32 >= d)
-template <class Tx, int NG, int M>
-__global__ void __launch_bounds__(128, 4) k5_batch(BatchParams p) {
+template <class Tx, int NG, int M, int NWP>
+__global__ void __launch_bounds__(32 * NWP, 4) k5_batch(BatchParams p) {
+  static_assert(NWP == 2 || NWP == 4, "2 or 4 warps per problem");
+  constexpr int NTH = 32 * NWP;
   constexpr int V = BVec<Tx>::V;
   const int prob = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -117,7 +119,7 @@ __global__ void __launch_bounds__(128, 4) k5_batch(BatchParams p) {
   uint64_t* rhash = p.rhash + (size_t)prob * p.max_rows;
   const uint64_t t_start = globaltimer_ns();
 
-  for (int k = tid; k < 264; k += 128) w_s[k] = (k < D && p.init) ? p.init[(size_t)prob * D + k] : 0.0;
+  for (int k = tid; k < 264; k += NTH) w_s[k] = (k < D && p.init) ? p.init[(size_t)prob * D + k] : 0.0;
   if (tid == 0) {
     sh_stop = 0;
     sh_blew = 0;
@@ -128,7 +130,7 @@ __global__ void __launch_bounds__(128, 4) k5_batch(BatchParams p) {
   // stream-0 / stream-1 initial states interleaved)
   uint64_t s_sample = p.seed[2 * prob];   // stream 0 state (thread-uniform)
   const uint64_t s_round0 = p.seed[2 * prob + 1];
-  for (int i = tid; i < 2048; i += 128) jt[i] = p.jump_tab[i];
+  for (int i = tid; i < 2048; i += NTH) jt[i] = p.jump_tab[i];
 
   int nrow = 0;
   int status = 0;  // 0 ok, 1 converged, 2 diverged
@@ -156,8 +158,8 @@ __global__ void __launch_bounds__(128, 4) k5_batch(BatchParams p) {
 
   // ---- full gradient + loss in the K1 order; result -> g_s, stats ----
   auto full_pass = [&]() {
-    // warp w: splits [w*S/4, (w+1)*S/4), binary-counter tree
-    const int sw = S / 4;
+    // warp w: splits [w*S/NWP, (w+1)*S/NWP), binary-counter tree
+    const int sw = S / NWP;
     double stk[kBatchMaxLev][NG * V + 1];
     int cnt = 0;
     for (int si = 0; si < sw; ++si) {
@@ -211,11 +213,11 @@ __global__ void __launch_bounds__(128, 4) k5_batch(BatchParams p) {
       }
     if (lane == 0) wsum[wid][256] = stk[0][NG * V];
     __syncthreads();
-    // top of the tree: ((w0 + w1) + (w2 + w3)); g = sum/n + l2 w; norms (k_finalize order)
+    // top of the tree: ((w0 + w1) + (w2 + w3)) or (w0 + w1); g = sum/n + l2 w; norms (k_finalize order)
     double ag = 0.0, aw = 0.0;
-    for (int k = tid; k < 256; k += 128) {
+    for (int k = tid; k < 256; k += NTH) {
       if (k < D) {
-        const double tot = (wsum[0][k] + wsum[1][k]) + (wsum[2][k] + wsum[3][k]);
+        const double tot = NWP == 4 ? (wsum[0][k] + wsum[1][k]) + (wsum[2][k] + wsum[3][k]) : wsum[0][k] + wsum[1][k];
         const double g = tot / (double)n + __dmul_rn(l2, w_s[k]);
         g_s[k] = g;
       }
@@ -234,7 +236,8 @@ __global__ void __launch_bounds__(128, 4) k5_batch(BatchParams p) {
         sw2 = vw == 0 ? aw : sw2 + aw;
       }
       if (lane == 0) {
-        const double ltot = (wsum[0][256] + wsum[1][256]) + (wsum[2][256] + wsum[3][256]);
+        const double ltot = NWP == 4 ? (wsum[0][256] + wsum[1][256]) + (wsum[2][256] + wsum[3][256])
+                                     : wsum[0][256] + wsum[1][256];
         const double gn = sqrt(sg);
         double delta = 0.0;
         if (isfinite(gn) && gn > 0.0) {
@@ -374,9 +377,9 @@ __global__ void __launch_bounds__(128, 4) k5_batch(BatchParams p) {
           rs = jump_tab(rs, jt);
         }
         __syncthreads();
-        // lane l < 4 holds warp l's record; lane butterfly over the 4 records
+        // lane l < NWP holds warp l's record; lane butterfly over the NWP records
         double sa = 0.0, sb = 0.0, fl = 0.0;
-        if (lane < 4) {
+        if (lane < NWP) {
           const double4 r = *reinterpret_cast<const double4*>(&rec[par][lane][0]);
           sa = sa + r.x;
           sb = sb + r.y;
@@ -386,8 +389,10 @@ __global__ void __launch_bounds__(128, 4) k5_batch(BatchParams p) {
           blow = t - 1;  // step t-1's update was non-finite; up[] still holds it
           break;
         }
-        sa = sa + __shfl_xor_sync(0xffffffffu, sa, 2);
-        sb = sb + __shfl_xor_sync(0xffffffffu, sb, 2);
+        if (NWP == 4) {
+          sa = sa + __shfl_xor_sync(0xffffffffu, sa, 2);
+          sb = sb + __shfl_xor_sync(0xffffffffu, sb, 2);
+        }
         sa = sa + __shfl_xor_sync(0xffffffffu, sa, 1);
         sb = sb + __shfl_xor_sync(0xffffffffu, sb, 1);
         sa = __shfl_sync(0xffffffffu, sa, 0);
@@ -462,7 +467,7 @@ __global__ void __launch_bounds__(128, 4) k5_batch(BatchParams p) {
     p.steps[prob] = (status >= 2) ? 0 : steps;
   }
   if (!sh_blew)
-    for (int q = tid; q < D; q += 128) p.w_out[(size_t)prob * D + q] = w_s[q];
+    for (int q = tid; q < D; q += NTH) p.w_out[(size_t)prob * D + q] = w_s[q];
 }
 
 // ---------------------------------------------------------------------------
@@ -793,10 +798,15 @@ static cudaError_t launch_b_ng(const BatchParams& p, cudaStream_t st) {
     else if (M <= 2) k5_batch_w1<Tx, NG, 2><<<p.nprob, 32, 0, st>>>(p);
     else if (M <= 4) k5_batch_w1<Tx, NG, 4><<<p.nprob, 32, 0, st>>>(p);
     else k5_batch_w1<Tx, NG, 8><<<p.nprob, 32, 0, st>>>(p);
+  } else if (batch_warps_per_problem(p.d) == 2) {
+    const int M = (p.d + 63) / 64;
+    if (M <= 1) k5_batch<Tx, NG, 1, 2><<<p.nprob, 64, 0, st>>>(p);
+    else if (M <= 2) k5_batch<Tx, NG, 2, 2><<<p.nprob, 64, 0, st>>>(p);
+    else k5_batch<Tx, NG, 4, 2><<<p.nprob, 64, 0, st>>>(p);
   } else if (p.d <= 128) {
-    k5_batch<Tx, NG, 1><<<p.nprob, 128, 0, st>>>(p);
+    k5_batch<Tx, NG, 1, 4><<<p.nprob, 128, 0, st>>>(p);
   } else {
-    k5_batch<Tx, NG, 2><<<p.nprob, 128, 0, st>>>(p);
+    k5_batch<Tx, NG, 2, 4><<<p.nprob, 128, 0, st>>>(p);
   }
   return cudaGetLastError();
 }

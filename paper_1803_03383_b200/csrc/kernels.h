@@ -185,8 +185,7 @@ cudaError_t launch_batch(const BatchParams& p, int threads, cudaStream_t st);
 // 35.9 ms (4 warps); C5's 512 x (4096 x 128) 135 ms (1 warp) vs 84.6 ms (4 warps)
 inline int batch_warps_per_problem(int d) {
   const char* e = std::getenv("HALP_K5_WARPS");
-  if (e && std::atoi(e) == 4) return 4;
-  if (e && std::atoi(e) == 1) return 1;
+  if (e && (std::atoi(e) == 1 || std::atoi(e) == 2 || std::atoi(e) == 4)) return std::atoi(e);
   return d <= 64 ? 1 : 4;
 }
 

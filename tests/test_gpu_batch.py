@@ -27,8 +27,12 @@ def rows_equal(grows, orows):
         assert a.iterate_hash == b["iterate_hash"]
 
 
+@pytest.mark.parametrize("warps", ["", "1", "2", "4"])
 @pytest.mark.parametrize("dtype,d", [("f32", 128), ("f64", 100), ("f32", 64), ("f32", 256)])
-def test_batch_bitexact_vs_mirror(H, oracle, dtype, d):
+def test_batch_bitexact_vs_mirror(H, oracle, dtype, d, warps, monkeypatch):
+    """every K5 plan (1, 2 or 4 warps per problem; "" = the library's choice)"""
+    if warps:
+        monkeypatch.setenv("HALP_K5_WARPS", warps)
     P, n = 12, 512
     rng = np.random.default_rng(d)
     X = rng.standard_normal((P, n, d))

@@ -87,7 +87,7 @@ def test_k5_and_lm_repeatable(H, oracle):
     cfgs = [H.OptimizerConfig(algorithm=H.Algorithm.Halp, alpha=1e-3, epochs=2, inner_steps=300, bits=8, mu=3.0,
                               seed=p) for p in range(P)]
     cfgs[3].alpha = 1e300
-    for warps in ("1", "4"):
+    for warps in ("1", "2", "4"):
         import os
 
         os.environ["HALP_K5_WARPS"] = warps
