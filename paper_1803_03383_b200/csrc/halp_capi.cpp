@@ -243,6 +243,11 @@ struct halp_problem {
   double* phi = nullptr;
   long long* hdev = nullptr;
   int* lm_bad = nullptr;
+  // pinned bounce buffer for the small per-epoch copies (stats, iterates): a
+  // pageable copy would queue behind another problem's multi-GB upload on the
+  // copy engine and stall this solve (e2e streaming of consecutive problems)
+  double* pin = nullptr;
+  size_t pin_bytes = 0;
   Events ev_fg, ev_fin, ev_in, ev_smp;
 
   ~halp_problem() {
@@ -254,12 +259,26 @@ struct halp_problem {
                       (void*)lm_bad})
       if (ptr) cudaFreeAsync(ptr, stream);
     if (own_X && X) cudaFreeAsync(X, stream);
+    if (pin) cudaFreeHost(pin);
     if (comm) Nccl::get().commDestroy(comm);
     if (stream) cudaStreamDestroy(stream);
   }
 };
 
 namespace {
+
+// small copies through the problem's pinned buffer (see halp_problem::pin)
+cudaError_t p_d2h(halp_problem* p, void* dst, const void* src, size_t bytes) {
+  if (!p->pin || bytes > p->pin_bytes) return copy_sync(dst, src, bytes, cudaMemcpyDeviceToHost, p->stream);
+  cudaError_t e = copy_sync(p->pin, src, bytes, cudaMemcpyDeviceToHost, p->stream);
+  if (e == cudaSuccess) std::memcpy(dst, p->pin, bytes);
+  return e;
+}
+cudaError_t p_h2d(halp_problem* p, void* dst, const void* src, size_t bytes) {
+  if (!p->pin || bytes > p->pin_bytes) return copy_sync(dst, src, bytes, cudaMemcpyHostToDevice, p->stream);
+  std::memcpy(p->pin, src, bytes);
+  return copy_sync(dst, p->pin, bytes, cudaMemcpyHostToDevice, p->stream);
+}
 
 constexpr int kDefaultInLevels = 1;  // measured on B200: see DESIGN.md 8
 
@@ -434,6 +453,8 @@ int ensure_workspace(halp_problem* p) {
     CU(dalloc(&p->blow, sizeof(long long), st));
     CU(dalloc(&p->zb0, sizeof(double) * p->D, st));
     CU(dalloc(&p->zb1, sizeof(double) * p->D, st));
+    p->pin_bytes = sizeof(double) * (size_t)std::max<int64_t>(p->D + 8, 64);
+    CU(cudaMallocHost(reinterpret_cast<void**>(&p->pin), p->pin_bytes));
     int rc = rng_tables(p->device, p->D, &p->pow_tab, &p->jump_tab, p->stream);
     if (rc) return rc;
     CU(cudaEventCreate(&p->ev_fg.a));
@@ -489,9 +510,8 @@ int full_pass(halp_problem* p, double* gn, double* delta, double* loss, double m
   if (rc) return rc;
   CU(cudaEventRecord(p->ev_fin.b, p->stream));
   double st[4];
-  CU(cudaMemcpyAsync(st, p->stats, sizeof(double) * 3, cudaMemcpyDeviceToHost, p->stream));
+  CU(p_d2h(p, st, p->stats, sizeof(double) * 3));
   p->timing.d2h_bytes += sizeof(double) * 3;
-  CU(cudaStreamSynchronize(p->stream));
   float ms = 0;
   CU(cudaEventElapsedTime(&ms, p->ev_fg.a, p->ev_fg.b));
   p->timing.fullgrad_ms += ms;
@@ -720,10 +740,17 @@ int halp_problem_create(const halp_problem_desc* desc, halp_problem** out) {
     // async on the problem's stream (a DMA straight from pinned host memory); a
     // plain 1-D copy when the rows need no padding
     const cudaMemcpyKind kind = dev_in ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
-    const cudaError_t ce2 =
-        p->ld == p->d ? cudaMemcpyAsync(p->X, desc->X, bytes, kind, p->stream)
-                      : cudaMemcpy2DAsync(p->X, (size_t)p->ld * es, desc->X, (size_t)p->d * es, (size_t)p->d * es,
-                                          (size_t)p->n, kind, p->stream);
+    // (in 256 MiB pieces, so other problems' copies interleave on the copy engine)
+    cudaError_t ce2 = cudaSuccess;
+    if (p->ld == p->d) {
+      constexpr size_t kChunk = (size_t)256 << 20;
+      for (size_t off = 0; off < bytes && ce2 == cudaSuccess; off += kChunk)
+        ce2 = cudaMemcpyAsync(static_cast<char*>(p->X) + off, static_cast<const char*>(desc->X) + off,
+                              std::min(kChunk, bytes - off), kind, p->stream);
+    } else {
+      ce2 = cudaMemcpy2DAsync(p->X, (size_t)p->ld * es, desc->X, (size_t)p->d * es, (size_t)p->d * es, (size_t)p->n,
+                              kind, p->stream);
+    }
     if (ce2 != cudaSuccess) return bail(fail(HALP_CUDA_ERROR, "copy of X to the device failed"));
     if (!dev_in) p->create_h2d += (int64_t)p->n * p->d * es;
   }
@@ -880,7 +907,7 @@ int halp_rank_partial(halp_problem* p, const double* w, double* root) {
   CU(cudaSetDevice(p->device));
   const int64_t D1 = p->D + 1;
   const int nloc = (int)p->sp.local_splits();
-  CU(copy_sync(p->w, w, sizeof(double) * p->D, cudaMemcpyHostToDevice, p->stream));
+  CU(p_h2d(p, p->w, w, sizeof(double) * p->D));
   for (int pass = 0; pass < p->fg_passes; ++pass) {
     FgParams fp = fg_params(p, pass);
     FgLaunch L = p->fg;
@@ -896,13 +923,13 @@ int halp_finalize_gathered(halp_problem* p, const double* w, const double* gathe
   if (!p || !w || !gathered) return fail(HALP_INVALID_INPUT, "halp_finalize_gathered: null argument");
   CU(cudaSetDevice(p->device));
   const int64_t D1 = p->D + 1;
-  CU(copy_sync(p->w, w, sizeof(double) * p->D, cudaMemcpyHostToDevice, p->stream));
+  CU(p_h2d(p, p->w, w, sizeof(double) * p->D));
   CU(copy_sync(p->gathered, gathered, sizeof(double) * D1 * p->world, cudaMemcpyHostToDevice, p->stream));
   FinParams fin{p->gathered, p->world, p->D, p->w, p->n, p->l2, 1.0, 1e-300, 8, p->g, p->stats};
   CU(launch_finalize(fin, p->stream));
   double st[3];
-  CU(copy_sync(st, p->stats, sizeof st, cudaMemcpyDeviceToHost, p->stream));
-  if (g) CU(copy_sync(g, p->g, sizeof(double) * p->D, cudaMemcpyDeviceToHost, p->stream));
+  CU(p_d2h(p, st, p->stats, sizeof st));
+  if (g) CU(p_d2h(p, g, p->g, sizeof(double) * p->D));
   if (loss) *loss = st[2];
   return HALP_OK;
 }
@@ -912,11 +939,11 @@ int halp_full_gradient(halp_problem* p, const double* w, double* g, double* loss
   if (p->host_exchange) return fail(HALP_INVALID_INPUT, "host-exchange problem: use halp_rank_partial / halp_finalize_gathered");
   CU(cudaSetDevice(p->device));
   p->timing = halp_timing{};
-  CU(copy_sync(p->w, w, sizeof(double) * p->D, cudaMemcpyHostToDevice, p->stream));
+  CU(p_h2d(p, p->w, w, sizeof(double) * p->D));
   double gn, delta, l;
   int rc = full_pass(p, &gn, &delta, &l, 1.0, 8, 1e-300);
   if (rc) return rc;
-  if (g) CU(copy_sync(g, p->g, sizeof(double) * p->D, cudaMemcpyDeviceToHost, p->stream));
+  if (g) CU(p_d2h(p, g, p->g, sizeof(double) * p->D));
   if (loss) *loss = l;
   return HALP_OK;
 }
@@ -980,7 +1007,7 @@ static int run_lm(halp_problem* p, const halp_config* cfg, halp_record* rec) {
   const uint64_t s_round = rng_seed_state(cfg->seed, 1);
   std::vector<double> wh(D, 0.0), gh(D);
   if (cfg->init) std::memcpy(wh.data(), cfg->init, sizeof(double) * D);
-  CU(copy_sync(p->w, wh.data(), sizeof(double) * D, cudaMemcpyHostToDevice, p->stream));
+  CU(p_h2d(p, p->w, wh.data(), sizeof(double) * D));
   p->timing.h2d_bytes += sizeof(double) * D;
   int64_t tr_steps = p->trace_cap > 0 ? std::min<int64_t>(T, p->trace_cap / D) : 0, traced = 0;
   if (tr_steps > p->trace_dev_steps) {
@@ -1009,7 +1036,7 @@ static int run_lm(halp_problem* p, const halp_config* cfg, halp_record* rec) {
     p->timing.kernel_launches += 3;
     p->timing.fullgrad_launches += 1;
     double st[3];
-    CU(copy_sync(st, p->stats, sizeof st, cudaMemcpyDeviceToHost, p->stream));
+    CU(p_d2h(p, st, p->stats, sizeof st));
     float ms = 0;
     CU(cudaEventElapsedTime(&ms, p->ev_fg.a, p->ev_fg.b));
     p->timing.fullgrad_ms += ms;
@@ -1026,7 +1053,7 @@ static int run_lm(halp_problem* p, const halp_config* cfg, halp_record* rec) {
     double gn, loss, dm, di, daux;
     int rc = stats(&gn, &loss);
     if (rc) return rc;
-    CU(copy_sync(wh.data(), p->w, sizeof(double) * D, cudaMemcpyDeviceToHost, p->stream));
+    CU(p_d2h(p, wh.data(), p->w, sizeof(double) * D));
     rc = lm_scales(gn, cfg, p->qdelta, &dm, &di, &daux, true);
     if (rc) return rc;
     rc = r.boundary((double)steps / (double)n, wh.data(), loss, gn, dm, k == 0 || gn == 0.0, di, daux);
@@ -1037,7 +1064,7 @@ static int run_lm(halp_problem* p, const halp_config* cfg, halp_record* rec) {
       break;
     }
     // h = Q_inner(alpha g~) (widen_range keeps the codes); its D draws follow Q_m(0)'s D
-    CU(copy_sync(gh.data(), p->g, sizeof(double) * D, cudaMemcpyDeviceToHost, p->stream));
+    CU(p_d2h(p, gh.data(), p->g, sizeof(double) * D));
     std::vector<long long> hh(D);
     uint64_t st = jt.jump(s_round, (uint64_t)k * per_epoch + (uint64_t)D);
     for (int64_t q = 0; q < D; ++q) {
@@ -1049,7 +1076,7 @@ static int run_lm(halp_problem* p, const halp_config* cfg, halp_record* rec) {
       (void)maxb;
       (void)minb;
     }
-    CU(cudaMemcpyAsync(p->hdev, hh.data(), sizeof(long long) * D, cudaMemcpyHostToDevice, p->stream));
+    CU(p_h2d(p, p->hdev, hh.data(), sizeof(long long) * D));
     const uint64_t sbase = jt.jump(s_sample, (uint64_t)k * (uint64_t)T);
     CU(cudaEventRecord(p->ev_smp.a, p->stream));
     CU(launch_samples(sbase, T, 0, (uint64_t)T, (uint64_t)n, p->pow_tab, p->idx, nullptr, p->stream));
@@ -1064,7 +1091,7 @@ static int run_lm(halp_problem* p, const halp_config* cfg, halp_record* rec) {
     p->timing.kernel_launches += 2;
     p->timing.inner_launches += 1;
     int bad = 0;
-    CU(copy_sync(&bad, p->lm_bad, sizeof(int), cudaMemcpyDeviceToHost, p->stream));
+    CU(p_d2h(p, &bad, p->lm_bad, sizeof(int)));
     float ms = 0;
     CU(cudaEventElapsedTime(&ms, p->ev_in.a, p->ev_in.b));
     p->timing.inner_ms += ms;
@@ -1087,13 +1114,13 @@ static int run_lm(halp_problem* p, const halp_config* cfg, halp_record* rec) {
     double gn, loss, dm, di, daux;
     int rc = stats(&gn, &loss);
     if (rc) return rc;
-    CU(copy_sync(wh.data(), p->w, sizeof(double) * D, cudaMemcpyDeviceToHost, p->stream));
+    CU(p_d2h(p, wh.data(), p->w, sizeof(double) * D));
     lm_scales(gn, cfg, p->qdelta, &dm, &di, &daux, false);
     rc = r.boundary((double)steps / (double)n, wh.data(), loss, gn, dm, true, di, daux);
     if (rc) return rc;
     if (gn == 0.0) rec->status = HALP_STATUS_CONVERGED;
   } else {
-    CU(copy_sync(wh.data(), p->w, sizeof(double) * D, cudaMemcpyDeviceToHost, p->stream));
+    CU(p_d2h(p, wh.data(), p->w, sizeof(double) * D));
   }
   if (rec->final_iterate) std::memcpy(rec->final_iterate, wh.data(), sizeof(double) * D);
   rec->steps_taken = steps;
@@ -1145,12 +1172,12 @@ int halp_run(halp_problem* p, const halp_config* cfg, halp_record* rec) {
   } else if (!halp) {
     z0 = wh;
   }
-  CU(cudaMemcpyAsync(p->w, wh.data(), sizeof(double) * D, cudaMemcpyHostToDevice, p->stream));
+  CU(p_h2d(p, p->w, wh.data(), sizeof(double) * D));
   p->timing.h2d_bytes += sizeof(double) * D;
   double* zin = p->zb0;
   double* zout = p->zb1;
   if (!halp) {
-    CU(cudaMemcpyAsync(zin, z0.data(), sizeof(double) * D, cudaMemcpyHostToDevice, p->stream));
+    CU(p_h2d(p, zin, z0.data(), sizeof(double) * D));
     p->timing.h2d_bytes += sizeof(double) * D;
   }
 
@@ -1184,7 +1211,7 @@ int halp_run(halp_problem* p, const halp_config* cfg, halp_record* rec) {
     double gn, delta, loss;
     rc = full_pass(p, &gn, &delta, &loss, mu, bits, cfg->delta_min);
     if (rc) return rc;
-    CU(copy_sync(wh.data(), p->w, sizeof(double) * D, cudaMemcpyDeviceToHost, p->stream));
+    CU(p_d2h(p, wh.data(), p->w, sizeof(double) * D));
     p->timing.d2h_bytes += sizeof(double) * D;
     const double row_delta = halp ? delta : lp ? cfg->delta : 0.0;
     rc = r.boundary((double)steps / (double)n, wh.data(), loss, gn, row_delta, k == 0 || (halp && gn == 0.0));
@@ -1226,9 +1253,8 @@ int halp_run(halp_problem* p, const halp_config* cfg, halp_record* rec) {
     ++p->timing.inner_launches;
     CU(cudaEventRecord(p->ev_in.b, p->stream));
     long long blow = -1;
-    CU(cudaMemcpyAsync(&blow, p->blow, sizeof(long long), cudaMemcpyDeviceToHost, p->stream));
+    CU(p_d2h(p, &blow, p->blow, sizeof(long long)));
     p->timing.d2h_bytes += sizeof(long long);
-    CU(cudaStreamSynchronize(p->stream));
     float ms = 0;
     CU(cudaEventElapsedTime(&ms, p->ev_in.a, p->ev_in.b));
     p->timing.inner_ms += ms;
@@ -1246,7 +1272,7 @@ int halp_run(halp_problem* p, const halp_config* cfg, halp_record* rec) {
       // Recorder::blowup (optimizers.cpp:156-160; HALP :432-434, LP-SVRG :370-372)
       p->timing.inner_steps += blow + 1;
       std::vector<double> u(D);
-      CU(copy_sync(u.data(), p->u_out, sizeof(double) * D, cudaMemcpyDeviceToHost, p->stream));
+      CU(p_d2h(p, u.data(), p->u_out, sizeof(double) * D));
       return r.boundary((double)(steps + blow + 1) / (double)n, u.data(), INFINITY, INFINITY, kdelta, true);
     }
     p->timing.inner_steps += T;
@@ -1259,13 +1285,13 @@ int halp_run(halp_problem* p, const halp_config* cfg, halp_record* rec) {
     double gn, delta, loss;
     rc = full_pass(p, &gn, &delta, &loss, mu, bits, cfg->delta_min);
     if (rc) return rc;
-    CU(copy_sync(wh.data(), p->w, sizeof(double) * D, cudaMemcpyDeviceToHost, p->stream));
+    CU(p_d2h(p, wh.data(), p->w, sizeof(double) * D));
     p->timing.d2h_bytes += sizeof(double) * D;
     rc = r.boundary((double)steps / (double)n, wh.data(), loss, gn, halp ? delta : lp ? cfg->delta : 0.0, true);
     if (rc) return rc;
     if (halp && gn == 0.0) rec->status = HALP_STATUS_CONVERGED;
   } else {
-    CU(copy_sync(wh.data(), p->w, sizeof(double) * D, cudaMemcpyDeviceToHost, p->stream));
+    CU(p_d2h(p, wh.data(), p->w, sizeof(double) * D));
   }
   if (rec->final_iterate) std::memcpy(rec->final_iterate, wh.data(), sizeof(double) * D);
   rec->steps_taken = steps;

@@ -229,7 +229,7 @@ __global__ void __launch_bounds__(256, 1) k3_inner(InParams p) {
     off_rest = q_first * NSLOT + slot_rest;
   }
 
-  double wt[M], gt[M], l2w[M], up[M], Ua[M];
+  double wt[M], gt[M], l2w[M], up[M], upp[M], Ua[M];  // up: u of this step, upp: of the previous one
   Tx xa[M], xb[M];
   double code[M], snap[M];  // z codes as exact doubles (|code| <= 2^(bits-1))
   const bool wide = p.hi > 0x1.0p53;
@@ -249,6 +249,7 @@ __global__ void __launch_bounds__(256, 1) k3_inner(InParams p) {
     code[i] = (BASE0 && valid[i] && p.z0) ? p.z0[k] : 0.0;
     snap[i] = code[i];
     up[i] = 0.0;
+    upp[i] = 0.0;
     Ua[i] = 0.0;
   }
   const int cA = cls[0];
@@ -438,7 +439,7 @@ __global__ void __launch_bounds__(256, 1) k3_inner(InParams p) {
 
     const double* xbp = xbuf_dyn + par * PAR_STRIDE;
     // blowup of step t-1?  Tested after this step's update (a blowup leaves
-    // code[] dead, and u of step t-1 is already in u_out).  KIND 0/1: a lane
+    // code[] dead; u of step t-1 is kept in upp[] and stored only then).  KIND 0/1: a lane
     // whose partial sums came out NaN raises `cand`, and the records are then
     // scanned for the flag pattern (a NaN of this step's own is not a flag).
     auto flagged = [&]() -> bool {
@@ -463,6 +464,7 @@ __global__ void __launch_bounds__(256, 1) k3_inner(InParams p) {
     }
     if (last) {
       if (flagged()) {
+        store_m<M>(p.u_out + k0, up, valid, allv);  // u of step T-1 (no update at t == T)
         if (rank == 0 && tid == 0) *p.blow_step = (long long)(t - 1);
         if (CL) cluster_sync_all();  // nobody leaves while remote stores may target it
         return;
@@ -498,9 +500,17 @@ __global__ void __launch_bounds__(256, 1) k3_inner(InParams p) {
       fl = isnan(sa) || isnan(sb);
       K3_MARK(8);
       // lanes >= NREC hold +0.0: butterfly levels that only add zeros are skipped
-      for (int o = (NREC >= 32 ? 16 : NREC > 1 ? (1 << (31 - __clz(NREC - 1))) : 0); o >= 1; o >>= 1) {
-        sa = sa + __shfl_xor_sync(0xffffffffu, sa, o);
-        sb = sb + __shfl_xor_sync(0xffffffffu, sb, o);
+      if (NREC >= 32) {  // every lane holds records: the full butterfly, unrolled (no loop branches)
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1) {
+          sa = sa + __shfl_xor_sync(0xffffffffu, sa, o);
+          sb = sb + __shfl_xor_sync(0xffffffffu, sb, o);
+        }
+      } else {
+        for (int o = NREC > 1 ? (1 << (31 - __clz(NREC - 1))) : 0; o >= 1; o >>= 1) {
+          sa = sa + __shfl_xor_sync(0xffffffffu, sa, o);
+          sb = sb + __shfl_xor_sync(0xffffffffu, sb, o);
+        }
       }
       if (NREC < 32) {
         sa = __shfl_sync(0xffffffffu, sa, 0);
@@ -590,6 +600,7 @@ __global__ void __launch_bounds__(256, 1) k3_inner(InParams p) {
       const double g1 = __dmul_rn(pp1, xc[i]) + __dmul_rn(l2, wz);
       const double g2 = __dmul_rn(pp2, xc[i]) + l2w[i];
       const double u = plain ? z - __dmul_rn(alpha, g1) : z - __dmul_rn(alpha, (g1 - g2) + gt[i]);
+      upp[i] = up[i];
       up[i] = u;
       bad |= valid[i] && !isfinite(u);
       code[i] = fp_inner ? u : quantize_fast(u, delta, rcp, p.hi, p.lo, Ua[i], slow[i]);
@@ -603,12 +614,12 @@ __global__ void __launch_bounds__(256, 1) k3_inner(InParams p) {
           code[i] = (double)quantize_code(up[i], delta, p.hi, p.lo, p.maxc, p.minc, Ua[i]);
     }
     if (__any_sync(0xffffffffu, fl) && (KIND == 2 || flagged())) {
+      // the failing update is step t-1's, still in registers (no per-step store)
+      store_m<M>(p.u_out + k0, upp, valid, allv);
       if (rank == 0 && tid == 0) *p.blow_step = (long long)(t - 1);
       if (CL) cluster_sync_all();  // nobody leaves while remote stores may target it
       return;
     }
-    // u of this step, kept for a blowup report at step t+1
-    store_m<M>(p.u_out + k0, up, valid, allv);
     bad_prev = bad ? 1 : 0;
     K3_MARK(6);
     if (t < p.trace_steps) {

@@ -248,7 +248,10 @@ class Objective:
     def __del__(self):
         h = getattr(self, "_h", None)
         if h:
-            A.lib().halp_problem_destroy(h)
+            try:
+                A.lib().halp_problem_destroy(h)
+            except Exception:  # interpreter shutdown: the module globals may be gone
+                pass
             self._h = None
 
     # ---- lpopt::Objective accessors ----
@@ -811,7 +814,10 @@ class BatchProblems:
     def __del__(self):
         h = getattr(self, "_h", None)
         if h:
-            A.lib().halp_batch_destroy(h)
+            try:
+                A.lib().halp_batch_destroy(h)
+            except Exception:
+                pass
             self._h = None
 
     def plan(self) -> dict:
