@@ -78,7 +78,8 @@ typedef struct {
                                   2: no NCCL, the caller moves the rank sums (test hook:
                                   halp_rank_partial / halp_finalize_gathered only); ABI >= 4 */
   /* lpopt::QuantizedExamples (objectives.hpp): the dataset's LM-HALP codes,
-   * int64 [n][d] at one scale (halp_quantize_dataset), or NULL; ABI >= 4 */
+   * int64 [n][d] in HOST memory (also when mem == HALP_MEM_DEVICE) at one
+   * scale (halp_quantize_dataset), or NULL; ABI >= 4 */
   const int64_t* qcodes;
   int32_t        qbits;
   double         qdelta;

@@ -740,13 +740,21 @@ int halp_problem_create(const halp_problem_desc* desc, halp_problem** out) {
     // async on the problem's stream (a DMA straight from pinned host memory); a
     // plain 1-D copy when the rows need no padding
     const cudaMemcpyKind kind = dev_in ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
-    // (in 256 MiB pieces, so other problems' copies interleave on the copy engine)
+    // In 256 MiB pieces with at most 1 GiB queued: the copy engine serves the
+    // queued copies in order, so another problem's small per-epoch copies (a
+    // solve running while this one uploads) wait for one GiB, not for all of X.
     cudaError_t ce2 = cudaSuccess;
     if (p->ld == p->d) {
       constexpr size_t kChunk = (size_t)256 << 20;
-      for (size_t off = 0; off < bytes && ce2 == cudaSuccess; off += kChunk)
+      int queued = 0;
+      for (size_t off = 0; off < bytes && ce2 == cudaSuccess; off += kChunk) {
         ce2 = cudaMemcpyAsync(static_cast<char*>(p->X) + off, static_cast<const char*>(desc->X) + off,
                               std::min(kChunk, bytes - off), kind, p->stream);
+        if (ce2 == cudaSuccess && ++queued == 4 && !dev_in) {
+          ce2 = cudaStreamSynchronize(p->stream);
+          queued = 0;
+        }
+      }
     } else {
       ce2 = cudaMemcpy2DAsync(p->X, (size_t)p->ld * es, desc->X, (size_t)p->d * es, (size_t)p->d * es, (size_t)p->n,
                               kind, p->stream);
@@ -787,14 +795,7 @@ int halp_problem_create(const halp_problem_desc* desc, halp_problem** out) {
     p->qdelta = desc->qdelta;
     if (desc->qbits <= 16) {  // wider codes: kept as metadata only (halp_run reports UNSUPPORTED)
       const size_t cnt = (size_t)p->n * p->d;
-      std::vector<int64_t> qh;
-      const int64_t* src = desc->qcodes;
-      if (dev_in) {
-        qh.resize(cnt);
-        if (copy_sync(qh.data(), desc->qcodes, cnt * 8, cudaMemcpyDeviceToHost, p->stream) != cudaSuccess)
-          return bail(fail(HALP_CUDA_ERROR, "copy of the quantized codes failed"));
-        src = qh.data();
-      }
+      const int64_t* src = desc->qcodes;  // host memory whatever desc->mem says (halp_quantize_dataset output)
       const int64_t lo = -(1LL << (desc->qbits - 1)), hi = (1LL << (desc->qbits - 1)) - 1;
       p->qbytes = desc->qbits <= 8 ? 1 : 2;
       std::vector<char> packed(cnt * p->qbytes);

@@ -179,14 +179,15 @@ struct BatchParams {
   double* w_out;         // [nprob][d] final iterate (the failing update on blow-up)
 };
 cudaError_t launch_batch(const BatchParams& p, int threads, cudaStream_t st);
-// K5 plan: 1 = one warp per problem (k5_batch_w1, M = D/32 per lane), 4 = four
-// warps (k5_batch, M = D/128 per thread); HALP_K5_WARPS overrides.  Measured on
-// B200 (tools/gpu_r2_lm.sh): the 663-run 1000 x 64 grid 20.5 ms (1 warp) vs
-// 35.9 ms (4 warps); C5's 512 x (4096 x 128) 135 ms (1 warp) vs 84.6 ms (4 warps)
+// K5 plan: 1 = one warp per problem (k5_batch_w1, M = D/32 per lane), 2 / 4 =
+// two / four warps (k5_batch, M = D/64 or D/128 per thread); HALP_K5_WARPS
+// overrides.  Measured on B200 (tools/gpu_r2_lm.sh, gpu_r2_e2e.sh, gpu_r2_k3opt.sh):
+// the 663-run 1000 x 64 grid 20.5-22.0 ms (1 warp) vs 27.0 (2) vs 35.9 (4); C5's
+// 512 x (4096 x 128) 135 ms (1) vs 82.0 (2) vs 84.6 (4)
 inline int batch_warps_per_problem(int d) {
   const char* e = std::getenv("HALP_K5_WARPS");
   if (e && (std::atoi(e) == 1 || std::atoi(e) == 2 || std::atoi(e) == 4)) return std::atoi(e);
-  return d <= 64 ? 1 : 4;
+  return d <= 64 ? 1 : d <= 128 ? 2 : 4;
 }
 
 }  // namespace halp

@@ -120,3 +120,20 @@ def test_lm_in_experiment(H, tmp_path):
     assert res.runs[1].status == "diverged"
     rows = HR.read_run_csv(str(tmp_path / res.runs[1].csv_path))
     assert not math.isfinite(rows[-1].loss) or rows[-1].loss > 1e8
+
+
+def test_lm_device_resident_dataset(H, oracle):
+    """X already in HBM (torch): the codes stay host arrays; same run as host X"""
+    import torch
+
+    X, y = oracle.make_regression(500, 16, 0.1, 3)
+    ds_h = H.Dataset(X, targets=y)
+    H.quantize_dataset(ds_h, 8, 2)
+    ds_d = H.Dataset(torch.as_tensor(X, device="cuda"), targets=torch.as_tensor(y, device="cuda"))
+    H.quantize_dataset(ds_d, 8, 2)
+    assert np.array_equal(ds_d.quantized.codes, ds_h.quantized.codes)
+    cfg = H.OptimizerConfig(algorithm=H.Algorithm.LmHalp, alpha=0.02, epochs=2, inner_steps=600, bits=8, mu=3.0, seed=1)
+    a = H.run_lm_halp(H.Objective(ds_h, H.LossFamily.Squared, 0.0), cfg)
+    b = H.run_lm_halp(H.Objective(ds_d, H.LossFamily.Squared, 0.0), cfg)
+    assert [r.iterate_hash for r in a.rows] == [r.iterate_hash for r in b.rows]
+    assert np.array_equal(a.final_iterate, b.final_iterate)
