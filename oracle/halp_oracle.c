@@ -708,8 +708,42 @@ static double mirror_norm(const double* g, int D) {
  * class; lanes are combined by the warp butterfly; the warp sums are then
  * added sequentially in global warp order (cta-major), which is the same as
  * skipping the warps that hold no coordinate of class c (their sum is +0). */
+/* K3's fixed-point exchange (plan in_levels 3, squared loss, HALP): every
+ * thread partial rounded to an integer at 2^S, the integers summed exactly
+ * (the order no longer matters), the sum scaled back once; a non-finite
+ * partial makes the dot NaN.  S from oq_fx_exponent. */
+static __thread double g_fx_scale = 0.0, g_fx_inv = 0.0; /* 0: not in use (per thread: tests run oracles concurrently) */
+
+int oq_fx_exponent(double xmax, const double* w, int64_t D, double delta, int bits) {
+  double l1 = 0.0;
+  for (int64_t j = 0; j < D; ++j) l1 += fabs(w[j]);
+  const double B = xmax * (l1 + (double)D * delta * ldexp(1.0, bits - 1));
+  if (!(B > 0.0) || !isfinite(B)) return 0;
+  const int S = 59 - ilogb(B);
+  return S < -1000 ? -1000 : S > 1000 ? 1000 : S;
+}
+
 static void mirror_inner_dots(const double* x, const double* wa, const double* wb, int d, int C,
                               const oq_plan* pl, double* la, double* lb) {
+  if (C == 1 && g_fx_scale != 0.0) {
+    const int D = d, T = pl->in_threads, m = pl->in_per, NC = pl->in_ctas;
+    const int64_t nthr = (int64_t)NC * T;
+    uint64_t sa = 0, sb = 0;
+    int nanp = 0;
+    for (int64_t tau = 0; tau < nthr; ++tau) {
+      double aa = 0.0, ab = 0.0;
+      for (int64_t k = tau * m; k < (tau + 1) * m && k < D; ++k) {
+        aa = fma(x[k], wa[k], aa);
+        ab = fma(x[k], wb[k], ab);
+      }
+      if (!(isfinite(aa) && isfinite(ab))) { nanp = 1; continue; }
+      sa += (uint64_t)llrint(aa * g_fx_scale);
+      sb += (uint64_t)llrint(ab * g_fx_scale);
+    }
+    la[0] = nanp ? NAN : (double)(int64_t)sa * g_fx_inv;
+    lb[0] = nanp ? NAN : (double)(int64_t)sb * g_fx_inv;
+    return;
+  }
   const int D = d * C, T = pl->in_threads, m = pl->in_per, NC = pl->in_ctas;
   const int ngw = NC * (T / 32);
   double wsa[512], wsb[512];
@@ -1002,12 +1036,28 @@ int oq_run_halp(const oq_objective* o, const oq_config* cfg, const oq_plan* plan
   const int fgth = rec->fullgrad_threads > 0 ? rec->fullgrad_threads : 1;
   rc = OQ_OK;
 
+  const int fx = plan && plan->in_levels == 3 && C == 1;
+  double xmax = 0.0;
+  if (fx) {
+    for (int64_t i = 0; i < n; ++i) {
+      load_row(o, i, x);
+      for (int j = 0; j < d; ++j) {
+        const double v = fabs(x[j]);
+        if (v > xmax || v != v) xmax = v;
+      }
+    }
+  }
   for (int k = 0; k < cfg->epochs && !converged; ++k) {
     double gn, delta, loss;
     measure(o, wt, cfg, plan, fgth, gt, &gn, &delta, &loss, &rec->fullgrad_seconds);
     rc = rec_boundary(&r, (double)steps / (double)n, wt, loss, gn, delta, k == 0 || gn == 0.0);
     if (rc) goto done;
     if (gn == 0.0) { rec->status = OQ_STATUS_CONVERGED; converged = 1; break; }
+    if (fx) {
+      const int S = oq_fx_exponent(xmax, wt, D, delta, cfg->bits);
+      g_fx_scale = ldexp(1.0, S);
+      g_fx_inv = ldexp(1.0, -S);
+    }
     /* z = Q(0): D draws, all codes 0 (optimizers.cpp:414-417) */
     for (int q = 0; q < D; ++q) {
       const double uu = oq_next_uniform(&rounder);
@@ -1085,6 +1135,7 @@ int oq_run_halp(const oq_objective* o, const oq_config* cfg, const oq_plan* plan
   memcpy(rec->final_iterate, wt, sizeof(double) * (size_t)D);
   rec->steps_taken = steps;
 done:
+  g_fx_scale = g_fx_inv = 0.0;
   /* a DivergenceError's partial record keeps steps_taken == 0: the
    * reference only assigns it after the loop (optimizers.cpp:457) */
   if (rc == OQ_DIVERGED) rec->steps_taken = 0;

@@ -204,6 +204,9 @@ typedef struct {
 int oq_datagen(const oq_datagen_desc* g, int64_t row0, int64_t nrows, int nthreads, void* X, double* y,
                int32_t* labels);
 
+/* exponent S of K3's fixed-point exchange (plan in_levels 3) for an epoch */
+int oq_fx_exponent(double xmax, const double* w, int64_t D, double delta, int bits);
+
 /* mirror-mode exp/log (identical operation sequence to the device code) */
 double oq_mexp(double x);
 /* REF-mode Eigen packet width (1, 2 or 4); default pinned by golden traces */

@@ -248,6 +248,7 @@ struct halp_problem {
   // copy engine and stall this solve (e2e streaming of consecutive problems)
   double* pin = nullptr;
   size_t pin_bytes = 0;
+  double xmax = -1.0;  // max |x| (fixed-point exchange bound), computed on first use
   Events ev_fg, ev_fin, ev_in, ev_smp;
 
   ~halp_problem() {
@@ -420,7 +421,8 @@ int plan_for(int64_t n, int d, int C, int dtype, KernelPlan* kp) {
   {
     const int lv = (int)env_int("HALP_IN_LEVELS", 0);
     const bool can = C == 1 && NC > 1 && T3 >= 64;
-    kp->in.levels = can ? (lv == 1 ? 1 : lv == 2 ? 2 : kDefaultInLevels) : 1;
+    const bool can_fx = C == 1 && NC > 1;
+    kp->in.levels = lv == 3 && can_fx ? 3 : can && lv == 2 ? 2 : lv == 1 ? 1 : (can_fx && kDefaultInLevels == 3) ? 3 : 1;
   }
   return HALP_OK;
 }
@@ -613,6 +615,19 @@ int validate(const halp_problem* p, const halp_config* c) {
   return HALP_OK;
 }
 
+// Scale exponent of the fixed-point exchange (k_inner.cu FX; oracle oq_fx_exponent):
+// every |x_j (w~_j + z_j)| <= xmax (|w~_j| + delta 2^(b-1)), so all partial and
+// total sums stay below B = xmax (|w~|_1 + D delta 2^(b-1)); S = 59 - ilogb(B) keeps
+// B 2^S < 2^60 (3 bits of headroom below int64's 2^63)
+int fx_exponent(double xmax, const double* w, int64_t D, double delta, int bits) {
+  double l1 = 0.0;
+  for (int64_t j = 0; j < D; ++j) l1 += std::fabs(w[j]);
+  const double B = xmax * (l1 + (double)D * delta * std::ldexp(1.0, bits - 1));
+  if (!(B > 0.0) || !std::isfinite(B)) return 0;
+  const int S = 59 - std::ilogb(B);
+  return S < -1000 ? -1000 : S > 1000 ? 1000 : S;
+}
+
 // LM-HALP scale chain (optimizers.cpp:509-521; theory.cpp:93-102)
 int lm_scales(double gn, const halp_config* c, double delta_d, double* dm, double* di, double* daux, bool check) {
   *dm = *di = *daux = 0.0;
@@ -745,16 +760,27 @@ int halp_problem_create(const halp_problem_desc* desc, halp_problem** out) {
     // solve running while this one uploads) wait for one GiB, not for all of X.
     cudaError_t ce2 = cudaSuccess;
     if (p->ld == p->d) {
+      // groups of 4 chunks; the host waits for group g-1 after queueing group g,
+      // so 1-2 GiB stay queued (no bubble) and never all of X
       constexpr size_t kChunk = (size_t)256 << 20;
-      int queued = 0;
+      cudaEvent_t ev[2] = {nullptr, nullptr};
+      if (!dev_in) {
+        ce2 = cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming);
+        if (ce2 == cudaSuccess) ce2 = cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming);
+      }
+      int queued = 0, group = 0;
       for (size_t off = 0; off < bytes && ce2 == cudaSuccess; off += kChunk) {
         ce2 = cudaMemcpyAsync(static_cast<char*>(p->X) + off, static_cast<const char*>(desc->X) + off,
                               std::min(kChunk, bytes - off), kind, p->stream);
-        if (ce2 == cudaSuccess && ++queued == 4 && !dev_in) {
-          ce2 = cudaStreamSynchronize(p->stream);
+        if (ce2 == cudaSuccess && !dev_in && ++queued == 4) {
           queued = 0;
+          ce2 = cudaEventRecord(ev[group & 1], p->stream);
+          if (ce2 == cudaSuccess && group > 0) ce2 = cudaEventSynchronize(ev[(group - 1) & 1]);
+          ++group;
         }
       }
+      for (cudaEvent_t e : ev)
+        if (e) cudaEventDestroy(e);
     } else {
       ce2 = cudaMemcpy2DAsync(p->X, (size_t)p->ld * es, desc->X, (size_t)p->d * es, (size_t)p->d * es, (size_t)p->n,
                               kind, p->stream);
@@ -1244,10 +1270,24 @@ int halp_run(halp_problem* p, const halp_config* cfg, halp_record* rec) {
     const uint64_t r0 = jt.jump(s_round, rdraws);
     CU(cudaMemsetAsync(p->blow, 0xFF, sizeof(long long), p->stream));
     const double rcp = 1.0 / kdelta;
+    // fixed-point exchange (levels 3, HALP): S such that D max|x| (|w~|_1/D + delta 2^(b-1)) 2^S < 2^60
+    double fx_scale = 1.0, fx_inv = 1.0;
+    if (halp && p->in.levels == 3) {
+      if (p->xmax < 0.0) {
+        double* dm = nullptr;
+        CU(dalloc(&dm, sizeof(double), p->stream));
+        CU(launch_absmax(p->X, p->dtype, p->n * (int64_t)p->ld, dm, p->stream));
+        CU(p_d2h(p, &p->xmax, dm, sizeof(double)));
+        CU(cudaFreeAsync(dm, p->stream));
+      }
+      const int S = fx_exponent(p->xmax, wh.data(), D, kdelta, bits);
+      fx_scale = std::ldexp(1.0, S);
+      fx_inv = std::ldexp(1.0, -S);
+    }
     InParams ip{p->X, p->ld, p->d, p->C, (int)D, p->loss, n, p->y, p->labels, p->l2, cfg->alpha, kdelta, hi, lo, maxc,
                 minc, std::isfinite(rcp) && rcp != 0.0 && env_int("HALP_IEEE_DIV", 0) == 0 ? rcp : 0.0, p->w, p->w2,
                 p->g, p->idx, T, t_pick, r0, p->pow_tab, p->jump_tab, p->codes, tr_steps > 0 ? p->trace_dev : nullptr,
-                tr_steps, p->blow, p->u_out, mode, halp ? nullptr : zin, halp ? nullptr : zout};
+                tr_steps, p->blow, p->u_out, mode, halp ? nullptr : zin, halp ? nullptr : zout, fx_scale, fx_inv};
     CU(cudaEventRecord(p->ev_in.a, p->stream));
     CU(launch_inner(p->in, ip, p->stream));
     ++p->timing.kernel_launches;

@@ -34,6 +34,7 @@
 // then a lane butterfly; softmax (C >= 2): sequential over the warps holding
 // the class, in global warp order; the softmax denominator is a pairwise tree
 // over 16 class slots (zero padded).
+#include <algorithm>
 #include <cstdio>
 
 #include "halp_device.cuh"
@@ -84,6 +85,13 @@ __device__ __forceinline__ void st_async_f64(uint32_t raddr, double v, uint32_t 
 __device__ __forceinline__ void st_async_v2f64(uint32_t raddr, double a, double b, uint32_t rbar) {
   asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];" ::"r"(raddr),
                "d"(a), "d"(b), "r"(rbar)
+               : "memory");
+}
+
+__device__ __forceinline__ void red_async_u64(uint32_t raddr, unsigned long long v, uint32_t rbar) {
+  asm volatile("red.async.relaxed.cluster.shared::cluster.mbarrier::complete_tx::bytes.add.u64 [%0], %1, [%2];" ::"r"(
+                   raddr),
+               "l"(v), "r"(rbar)
                : "memory");
 }
 
@@ -143,9 +151,10 @@ struct K3Layout {
 // (arithmetic never produces it; NaN logits make receivers rescan for it).
 constexpr long long kFlagBits = 0x7FF4A1B2C3D4E5F6LL;
 
-template <class Tx, int M, bool CL, int KIND, bool BASE0, bool LV2>
+template <class Tx, int M, bool CL, int KIND, bool BASE0, bool LV2, bool FX>
 __global__ void __launch_bounds__(256, 1) k3_inner(InParams p) {
   static_assert(!LV2 || (KIND == 0 && CL), "two-level exchange: squared loss on a cluster");
+  static_assert(!FX || (KIND == 0 && CL && !BASE0 && !LV2), "fixed-point exchange: HALP squared loss on a cluster");
   constexpr int NSLOT = K3Layout<KIND>::NSLOT;
   constexpr int FLAG = K3Layout<KIND>::FLAG;
   constexpr bool SQ = KIND == 0;
@@ -153,6 +162,7 @@ __global__ void __launch_bounds__(256, 1) k3_inner(InParams p) {
   __shared__ __align__(8) uint64_t mbar[2];
   __shared__ __align__(16) double gsc[2][8][32];  // softmax gathers: [parity][warp][lane]
   __shared__ __align__(16) double ctar[2][8][2];  // LV2: this CTA's warp records [parity][warp]
+  __shared__ __align__(8) unsigned long long fxacc[2][4];  // FX: running sums [parity]: a, b, flags
   extern __shared__ __align__(16) double xbuf_dyn[];  // [2][NGW][NSLOT]
 
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, NW = blockDim.x >> 5;
@@ -168,11 +178,12 @@ __global__ void __launch_bounds__(256, 1) k3_inner(InParams p) {
   const int WC = 32 * M;  // coordinates per warp
   const int PAR_STRIDE = NGW * NSLOT;  // doubles between the two parity buffers
   auto XB = [&](int par_, int q_, int slot_) -> double& { return xbuf_dyn[par_ * PAR_STRIDE + q_ * NSLOT + slot_]; };
-  const uint32_t bytes_step = KIND == 0 ? (uint32_t)NREC * 16u
+  const uint32_t bytes_step = FX ? (uint32_t)NGW * 24u : KIND == 0 ? (uint32_t)NREC * 16u
                               : KIND == 1 ? (uint32_t)NGW * 32u
                                           : (uint32_t)NGW * (uint32_t)(2 * C + 1) * 8u;
 
   for (int i = tid; i < 2048; i += blockDim.x) jt[i] = p.jump_tab[i];
+  if (tid < 8) (&fxacc[0][0])[tid] = 0ull;
   if (CL && tid == 0) {
     mbar_init(&mbar[0], 1);
     mbar_init(&mbar[1], 1);
@@ -190,7 +201,8 @@ __global__ void __launch_bounds__(256, 1) k3_inner(InParams p) {
   if (CL && KIND == 0) {
     const int r0 = lane & 15;
     s0ok = lane < 16 && r0 < NC;
-    ra0 = mapa_u32(&XB(0, LV2 ? (int)rank : gw, 0), (uint32_t)(s0ok ? r0 : 0));
+    ra0 = FX ? mapa_u32(&fxacc[0][0], (uint32_t)(s0ok ? r0 : 0))
+             : mapa_u32(&XB(0, LV2 ? (int)rank : gw, 0), (uint32_t)(s0ok ? r0 : 0));
     rb0 = mapa_u32(&mbar[0], (uint32_t)(s0ok ? r0 : 0));
   } else if (CL && KIND == 1) {
     const int slot = 2 * (lane >> 4);
@@ -282,6 +294,7 @@ __global__ void __launch_bounds__(256, 1) k3_inner(InParams p) {
   if (CL) cluster_sync_all();
 
   int bad_prev = 0;
+  unsigned long long fx_pa0 = 0, fx_pa1 = 0, fx_pb0 = 0, fx_pb1 = 0, fx_pf0 = 0, fx_pf1 = 0;  // FX totals seen
 #ifdef HALP_K3_PROF
   const bool prof_on = rank == 0 && tid == 0;
   long long prof_acc[16] = {}, prof_last = clock64();
@@ -334,7 +347,30 @@ __global__ void __launch_bounds__(256, 1) k3_inner(InParams p) {
     const bool flag = __any_sync(0xffffffffu, bad_prev);
     const double flagv = flag ? 1.0 : 0.0;
     const double fnan = __longlong_as_double(kFlagBits);
-    if constexpr (KIND == 0) {
+    if constexpr (FX) {
+      // fixed point: every thread's partials rounded to integers at 2^S (S from a
+      // bound on |x| |w~ + z| chosen per epoch so no sum can reach 2^61), the warp
+      // sums by REDUX on 21-bit limbs, one remote integer reduction per CTA
+      // (red.async) -- integer sums are exact, so the order of arrival is irrelevant
+      const bool nanp = !(isfinite(a0) && isfinite(b0));
+      const long long A = nanp ? 0 : __double2ll_rn(__dmul_rn(a0, p.fx_scale));
+      const long long B = nanp ? 0 : __double2ll_rn(__dmul_rn(b0, p.fx_scale));
+      const int a_lo = __reduce_add_sync(0xffffffffu, (int)(A & 0x1FFFFF));
+      const int a_mi = __reduce_add_sync(0xffffffffu, (int)((A >> 21) & 0x1FFFFF));
+      const int a_hi = __reduce_add_sync(0xffffffffu, (int)(A >> 42));
+      const int b_lo = __reduce_add_sync(0xffffffffu, (int)(B & 0x1FFFFF));
+      const int b_mi = __reduce_add_sync(0xffffffffu, (int)((B >> 21) & 0x1FFFFF));
+      const int b_hi = __reduce_add_sync(0xffffffffu, (int)(B >> 42));
+      const long long SA = (long long)a_hi * (1LL << 42) + (long long)a_mi * (1LL << 21) + (long long)a_lo;
+      const long long SB = (long long)b_hi * (1LL << 42) + (long long)b_mi * (1LL << 21) + (long long)b_lo;
+      const unsigned long long F = (flag ? 1ull : 0ull) + (__any_sync(0xffffffffu, nanp) ? (1ull << 32) : 0ull);
+      if (s0ok) {
+        const uint32_t xo = par ? 32u : 0u, mo = par ? mb_par_off : 0u;
+        red_async_u64(ra0 + xo, (unsigned long long)SA, rb0 + mo);
+        red_async_u64(ra0 + xo + 8u, (unsigned long long)SB, rb0 + mo);
+        red_async_u64(ra0 + xo + 16u, F, rb0 + mo);
+      }
+    } else if constexpr (KIND == 0) {
       // all-reduce butterfly of a0 on lanes 0..15 and of b0 on lanes 16..31
       const bool u16 = (lane & 16) != 0;
       double v = (u16 ? b0 : a0) + __shfl_xor_sync(0xffffffffu, u16 ? a0 : b0, 16);
@@ -438,6 +474,24 @@ __global__ void __launch_bounds__(256, 1) k3_inner(InParams p) {
     K3_MARK(3);
 
     const double* xbp = xbuf_dyn + par * PAR_STRIDE;
+    double fxa = 0.0, fxb = 0.0;
+    if constexpr (FX) {
+      // this step's sums = running totals minus the totals two steps ago (mod 2^64: exact)
+      const unsigned long long ca = fxacc[par][0], cb = fxacc[par][1], cf = fxacc[par][2];
+      const unsigned long long da = ca - (par ? fx_pa1 : fx_pa0), db = cb - (par ? fx_pb1 : fx_pb0);
+      const unsigned long long df = cf - (par ? fx_pf1 : fx_pf0);
+      if (par) { fx_pa1 = ca; fx_pb1 = cb; fx_pf1 = cf; } else { fx_pa0 = ca; fx_pb0 = cb; fx_pf0 = cf; }
+      if ((uint32_t)df != 0u) {  // some warp's previous update was non-finite: blow-up of step t-1
+        store_m<M>(p.u_out + k0, up, valid, allv);  // no update yet at step t: up holds u of step t-1
+        if (rank == 0 && tid == 0) *p.blow_step = (long long)(t - 1);
+        cluster_sync_all();
+        return;
+      }
+      if (last) break;
+      const bool nanstep = (df >> 32) != 0ull;  // a partial was not finite: the reference's dot is NaN
+      fxa = nanstep ? __longlong_as_double(0x7FF8000000000000LL) : __dmul_rn(__ll2double_rn((long long)da), p.fx_inv);
+      fxb = nanstep ? __longlong_as_double(0x7FF8000000000000LL) : __dmul_rn(__ll2double_rn((long long)db), p.fx_inv);
+    }
     // blowup of step t-1?  Tested after this step's update (a blowup leaves
     // code[] dead; u of step t-1 is kept in upp[] and stored only then).  KIND 0/1: a lane
     // whose partial sums came out NaN raises `cand`, and the records are then
@@ -486,7 +540,10 @@ __global__ void __launch_bounds__(256, 1) k3_inner(InParams p) {
 
     // loss derivative at wz (p1) and at w~ (p2) for this thread's classes
     double p1A, p2A, p1B, p2B;
-    if constexpr (SQ) {
+    if constexpr (FX) {
+      p1A = p1B = fxa - yi;
+      p2A = p2B = fxb - yi;
+    } else if constexpr (SQ) {
       double sa = 0.0, sb = 0.0;
 #pragma unroll
       for (int j = 0; j < kMaxWarpsPerCluster / 32; ++j) {
@@ -656,7 +713,7 @@ static cudaError_t launch_in_b(const InLaunch& L, const InParams& p, cudaStream_
   if (L.ctas * L.threads / 32 > kMaxWarpsPerCluster) return cudaErrorInvalidConfiguration;
   const size_t smem = sizeof(double) * 2 * (size_t)(L.ctas * L.threads / 32) * K3Layout<KIND>::NSLOT;
   if (L.ctas == 1) {
-    auto kern = k3_inner<Tx, M, false, KIND, BASE0, false>;
+    auto kern = k3_inner<Tx, M, false, KIND, BASE0, false, false>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     if (L.dry) return cudaSuccess;
@@ -664,9 +721,12 @@ static cudaError_t launch_in_b(const InLaunch& L, const InParams& p, cudaStream_
     return cudaGetLastError();
   }
   if (L.ctas > 16) return cudaErrorInvalidConfiguration;
-  auto kern = k3_inner<Tx, M, true, KIND, BASE0, false>;
-  if constexpr (KIND == 0)
-    if (L.levels == 2) kern = k3_inner<Tx, M, true, KIND, BASE0, true>;
+  auto kern = k3_inner<Tx, M, true, KIND, BASE0, false, false>;
+  if constexpr (KIND == 0) {
+    if (L.levels == 2) kern = k3_inner<Tx, M, true, KIND, BASE0, true, false>;
+    if constexpr (!BASE0)
+      if (L.levels == 3) kern = k3_inner<Tx, M, true, KIND, BASE0, false, true>;
+  }
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   if (e != cudaSuccess) return e;
   e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -717,6 +777,38 @@ cudaError_t launch_inner(const InLaunch& L, const InParams& p, cudaStream_t st) 
     case 1: return launch_in_dt<float>(L, p, st);
     default: return launch_in_dt<__nv_bfloat16>(L, p, st);
   }
+}
+
+}  // namespace halp
+
+namespace halp {
+
+// max |x| of a matrix (FX exchange bound), one block-reduced atomic max on the
+// double's bit pattern (non-negative doubles order like their integer bits)
+template <class Tx>
+__global__ void k_absmax(const Tx* __restrict__ X, int64_t elems, unsigned long long* out) {
+  double m = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < elems; i += (int64_t)gridDim.x * blockDim.x) {
+    const double v = fabs(to_d<Tx>(X[i]));
+    m = (v > m || v != v) ? v : m;  // NaN wins (its bits sort above +inf's)
+  }
+  for (int o = 16; o >= 1; o >>= 1) {
+    const double q = __shfl_xor_sync(0xffffffffu, m, o);
+    m = (q > m || q != q) ? q : m;
+  }
+  if ((threadIdx.x & 31) == 0) atomicMax(out, (unsigned long long)__double_as_longlong(m));
+}
+
+cudaError_t launch_absmax(const void* X, int dtype, int64_t elems, double* out, cudaStream_t st) {
+  cudaError_t e = cudaMemsetAsync(out, 0, sizeof(double), st);
+  if (e != cudaSuccess) return e;
+  int blocks = (int)std::min<int64_t>((elems + 255) / 256, 148 * 8);
+  if (blocks < 1) blocks = 1;
+  auto* o = reinterpret_cast<unsigned long long*>(out);
+  if (dtype == 0) k_absmax<double><<<blocks, 256, 0, st>>>(reinterpret_cast<const double*>(X), elems, o);
+  else if (dtype == 1) k_absmax<float><<<blocks, 256, 0, st>>>(reinterpret_cast<const float*>(X), elems, o);
+  else k_absmax<__nv_bfloat16><<<blocks, 256, 0, st>>>(reinterpret_cast<const __nv_bfloat16*>(X), elems, o);
+  return cudaGetLastError();
 }
 
 }  // namespace halp

@@ -91,13 +91,19 @@ struct InParams {
   int mode;
   const double* z0;          // [D] initial z values (code * delta units: codes) or null = 0
   double* zc_out;            // [D] codes of the epoch's result (snapshot under option II) or null
+  // fixed-point exchange (InLaunch::levels == 3, HALP squared loss on a cluster):
+  // thread partials rounded to integers at 2^fx_s, summed exactly as int64
+  double fx_scale, fx_inv;   // 2^S, 2^-S
 };
 struct InLaunch {
   int dtype, ctas, threads, per, nslot_pow2;
   int dry;     // 1: load + configure the kernel only (see FgLaunch::dry)
-  int levels;  // 1: warp records exchanged across the cluster; 2: combined per CTA first (k_inner.cu)
+  int levels;  // 1: warp records exchanged across the cluster; 2: combined per CTA first;
+               // 3: fixed-point records summed by remote integer reductions (k_inner.cu FX)
 };
 cudaError_t launch_inner(const InLaunch& L, const InParams& p, cudaStream_t st);
+// max |x| over an n x ld matrix of the stored dtype -> *out (one double)
+cudaError_t launch_absmax(const void* X, int dtype, int64_t elems, double* out, cudaStream_t st);
 
 // ---- LM-HALP (k_lm.cu): K7 epoch stats over the quantized rows, K8 integer inner loop ----
 constexpr int kLmMaxD = 4096;  // d*C over one 256-thread CTA, <= 16 coordinates per thread

@@ -25,7 +25,7 @@ def sig(rec):
     return [(r.loss, r.grad_norm, r.delta, r.iterate_hash) for r in rec.rows], rec.final_iterate.tobytes()
 
 
-@pytest.mark.parametrize("plan", ["0:0:1", "4:2:1", "16:2:1", "16:2:2", "8:4:2"])
+@pytest.mark.parametrize("plan", ["0:0:1", "4:2:1", "16:2:1", "16:2:2", "8:4:2", "16:2:3", "8:4:3"])
 def test_k1_k3_repeatable(H, oracle, monkeypatch, plan):
     nc, m, lv = plan.split(":")
     monkeypatch.setenv("HALP_IN_NC", nc)

@@ -1,7 +1,10 @@
-"""K3's two-level exchange (squared loss on a cluster: each CTA's warps
-pre-reduced in shared memory, one DSMEM record per CTA; plan in_levels = 2)
-bit-identical to the oracle's MIRROR order with that plan, including a
-mid-epoch blow-up (the in-band flag survives the CTA combine)."""
+"""K3's alternative exchanges for squared loss on a cluster, each bit-identical
+to the oracle's MIRROR order for its plan, including a mid-epoch blow-up:
+in_levels = 2: each CTA's warps pre-reduced in shared memory, one DSMEM
+record per CTA (the in-band flag survives the CTA combine);
+in_levels = 3: fixed point -- thread partials rounded to integers at 2^S,
+warp sums by REDUX, remote integer reductions (red.async) into running
+totals, so the sum is exact and order-free."""
 import os
 
 import numpy as np
@@ -19,15 +22,16 @@ def H():
     return H
 
 
+@pytest.mark.parametrize("lv", [2, 3])
 @pytest.mark.parametrize("nc,m", [(16, 2), (8, 4), (4, 4)])
-def test_two_level_bitexact(H, oracle, monkeypatch, nc, m):
-    monkeypatch.setenv("HALP_IN_LEVELS", "2")
+def test_two_level_bitexact(H, oracle, monkeypatch, nc, m, lv):
+    monkeypatch.setenv("HALP_IN_LEVELS", str(lv))
     monkeypatch.setenv("HALP_IN_NC", str(nc))
     monkeypatch.setenv("HALP_IN_M", str(m))
     X, y = oracle.generate("regression", 4096, 4096, dtype="f32", noise_sd=0.1, seed=3)
     g = H.Objective(H.Dataset(X, targets=y), H.LossFamily.Squared, 1e-5)
     plan = g.oracle_plan()
-    assert plan["in_levels"] == 2 and plan["in_ctas"] == nc
+    assert plan["in_levels"] == lv and plan["in_ctas"] == nc
     cfg = dict(alpha=2e-4, epochs=2, inner_steps=1500, bits=16, mu=1.0, seed=7)
     steps = 300
     tr = np.zeros(steps * 4096, dtype=np.int64)
@@ -45,3 +49,20 @@ def test_two_level_bitexact(H, oracle, monkeypatch, nc, m):
     orec = oracle.run_halp(o, oracle.OracleConfig(**bad), plan=plan)
     assert [(r.pass_, r.iterate_hash) for r in e.value.partial.rows] == \
         [(r["pass_"], r["iterate_hash"]) for r in orec.rows]
+
+
+def test_fixed_point_nan_data_blows_up_like_oracle(H, oracle, monkeypatch):
+    """a non-finite x makes the reference's dot NaN: same blow-up row"""
+    monkeypatch.setenv("HALP_IN_LEVELS", "3")
+    monkeypatch.setenv("HALP_IN_NC", "4")
+    monkeypatch.setenv("HALP_IN_M", "2")
+    X, y = oracle.generate("regression", 2000, 1024, dtype="f32", noise_sd=0.1, seed=5)
+    X[777, 5] = np.inf
+    g = H.Objective(H.Dataset(X, targets=y), H.LossFamily.Squared, 0.0)
+    cfg = dict(alpha=1e-4, epochs=1, inner_steps=3000, bits=8, mu=1.0, seed=2)
+    o = oracle.OracleObjective(X, y=y)
+    orec = oracle.run_halp(o, oracle.OracleConfig(**cfg), plan=g.oracle_plan())
+    with pytest.raises(H.DivergenceError) as e:
+        H.run_halp(g, H.OptimizerConfig(algorithm=H.Algorithm.Halp, **cfg))
+    assert [(r.pass_, r.loss, r.iterate_hash) for r in e.value.partial.rows] == \
+        [(r["pass_"], r["loss"], r["iterate_hash"]) for r in orec.rows]
