@@ -51,7 +51,7 @@ sys.path.insert(0, ROOT)
 
 C3 = dict(n=4194304, d=4096, dtype="f32", noise_sd=0.1, seed=3, bits=16, T=4194304 // 8, alpha=5e-5, mu=1.0, l2=0.0)
 C2 = dict(n=60000, d=784, C=10, density=0.2, l2=1e-4, bits=8, alpha=0.01, mu=2.5)
-C4 = dict(n=16777216, d=1024, dtype="bf16")
+C4 = dict(n=16777216, d=1024, dtype="bf16", epochs=3)
 C5 = dict(nprob=512, n=4096, d=128, epochs=10, mu=3.0)  # per GPU; T = 2N (reference default)
 # CPU sample of the C3 epoch: rows / steps divisors (the epoch cost is linear in both)
 CPU_ROWS_DIV, CPU_STEPS_DIV = 64, 64
@@ -144,6 +144,52 @@ def cpu_c3_sample(O, threads: int, rows_div: int = CPU_ROWS_DIV, steps_div: int 
     return epoch_s, measured, data
 
 
+def cpu_c4_fullgrad(O, threads: int, rows_div: int = 256):
+    """C4's full-gradient + loss pass on the host: the REF-order oracle (the
+    reference's 1024-row blocks on `threads` threads, objectives.cpp:289-301) over
+    the first N/rows_div rows of the C4 dataset, extrapolated linearly in rows."""
+    n, d = C4["n"], C4["d"]
+    ns = n // rows_div
+    X, lab = O.generate("logistic", n, d, dtype="bf16", x_scale=d ** -0.5, seed=4, rows=(0, ns), threads=threads)
+    o = O.OracleObjective(X, labels=lab, num_classes=2, l2=1e-5)
+    w = np.random.default_rng(7).standard_normal(2 * d)
+    o.full_gradient(w, num_threads=threads)
+    t = time.perf_counter()
+    reps = 3
+    for _ in range(reps):
+        o.full_gradient(w, num_threads=threads)
+        o.loss_value(w)
+    s = (time.perf_counter() - t) / reps
+    return {"ms_per_pass": 1000.0 * s * rows_div, "cores": threads, "kind": "port",
+            "sample": f"REF-order oracle full_gradient + loss on rows [0, N/{rows_div}) = {ns} rows of the C4 dataset, "
+                      f"{threads} threads, x{rows_div} (linear in rows)", "measured_seconds": s * reps}
+
+
+def cpu_c5_batch(O, threads: int):
+    """C5 on the host: `threads` of the batch's problems solved concurrently, one
+    REF-order oracle run_halp (K = 10, T = 2N) per thread; problems are independent,
+    so the batch of 512 costs 512 / threads such rounds."""
+    import concurrent.futures as cf
+
+    n, d = C5["n"], C5["d"]
+    rng = np.random.default_rng(0)
+    probs = []
+    for q in range(threads):
+        X, y = O.generate("regression", n, d, dtype="f32", noise_sd=0.1, seed=10_000 + q)
+        probs.append((O.OracleObjective(X, y=y, l2=0.0),
+                      O.OracleConfig(alpha=float(10 ** rng.uniform(-4, -2)), epochs=C5["epochs"],
+                                     bits=8 if q % 2 == 0 else 16, mu=C5["mu"], seed=q)))
+    t = time.perf_counter()
+    with cf.ThreadPoolExecutor(threads) as ex:
+        list(ex.map(lambda pc: O.run_halp(pc[0], pc[1]), probs))
+    s = time.perf_counter() - t
+    per_batch = s * C5["nprob"] / threads
+    return {"ms_per_batch": 1000.0 * per_batch, "problem_epochs_per_s": C5["nprob"] * C5["epochs"] / per_batch,
+            "cores": threads, "kind": "port",
+            "sample": f"{threads} of the 512 problems, one REF-order oracle run_halp per host thread concurrently; "
+                      f"batch = measured x 512/{threads}", "measured_seconds": s}
+
+
 def cpu_sample_text(threads):
     return (f"REF-order oracle run_halp, 1 epoch on rows [0, N/{CPU_ROWS_DIV}) of the C3 dataset with "
             f"T/{CPU_STEPS_DIV} = {C3['T'] // CPU_STEPS_DIV} inner steps, full gradient on {threads} threads "
@@ -210,7 +256,16 @@ def fullgrad_c4(H, device, reps, world, rank, nccl_id):
     ms = obj.bench_full_gradient(reps)
     pl = obj.plan()
     rows = int(n * (pl["fg_split_end"] - pl["fg_split_begin"]) // pl["fg_splits"])
-    return ms, rows * d * 2 + rows * 4, pl
+    # the same pass as it runs in the solver: K1 once per HALP epoch, the inner loop between
+    # two passes (b = 8, alpha = 0.05, mu = 2.5 as in tests/test_gpu_baseline_configs.py; T = N/64)
+    cfg = H.OptimizerConfig(algorithm=H.Algorithm.Halp, alpha=0.05, epochs=C4["epochs"], inner_steps=n // 64, bits=8,
+                            mu=2.5, seed=0)
+    rec = H.run_halp(obj, cfg)
+    tim = obj.timing()
+    in_epoch = {"ms_per_pass": tim["fullgrad_ms"] / (C4["epochs"] + 1),
+                "inner_ns_per_step": 1e6 * tim["inner_ms"] / (C4["epochs"] * (n // 64)),
+                "epochs": C4["epochs"], "T": n // 64, "loss_first_last": [rec.rows[0].loss, rec.rows[-1].loss]}
+    return ms, rows * d * 2 + rows * 4, pl, in_epoch
 
 
 def c2_epochs(H, device, rank, epochs):
@@ -486,16 +541,22 @@ def main():
         del o3, X3, y3
         torch.cuda.empty_cache()
         barrier()
-        ms4, b4, _ = fullgrad_c4(H, local, args.fg_reps, world, rank, nccl_id)
+        ms4, b4, _, c4_epoch = fullgrad_c4(H, local, args.fg_reps, world, rank, nccl_id)
         ms4 = max_over_ranks(ms4)
         gbs4 = b4 * world / (ms4 / 1000.0) / 1e9
+        c4_epoch["ms_per_pass"] = max_over_ranks(c4_epoch["ms_per_pass"])
+        c4_epoch["GB_per_s"] = b4 * world / (c4_epoch["ms_per_pass"] / 1000.0) / 1e9
+        c4_epoch["frac_of_hbm_peak"] = c4_epoch["GB_per_s"] / world / pk["hbm_gbs"]
+        c4_epoch["what"] = ("K1 (+ split tree) timed by CUDA events inside a C4 HALP run (b=8, T=N/64, alpha=0.05, "
+                            "mu=2.5): one pass per epoch between inner loops, as the solver runs it")
         torch.cuda.empty_cache()
         extras["fullgrad"] = {
             "C3": {"shape": "4194304x4096 f32", "ms_per_pass": ms3, "GB_per_s": gbs3,
                    "frac_of_hbm_peak": gbs3 / world / pk["hbm_gbs"], "algorithmic_bytes_per_gpu": algo_bytes,
                    "includes": "K1 + split tree" + (" + NCCL all-gather + finalize" if world > 1 else "")},
             "C4": {"shape": "16777216x1024 bf16 (softmax C=2)", "ms_per_pass": ms4, "GB_per_s": gbs4,
-                   "frac_of_hbm_peak": gbs4 / world / pk["hbm_gbs"], "algorithmic_bytes_per_gpu": b4}}
+                   "frac_of_hbm_peak": gbs4 / world / pk["hbm_gbs"], "algorithmic_bytes_per_gpu": b4,
+                   "timed": f"{args.fg_reps} passes back to back", "in_epoch": c4_epoch}}
         # ---------------- C2 epochs (MNIST-shaped softmax) ----------------
         barrier()
         extras["c2"] = c2_epochs(H, local, rank, 5)
@@ -525,6 +586,12 @@ def main():
         ep2, meas2, _ = cpu_c3_sample(O, threads, data=data)
         cpu = {"value": 2.0 / (ep + ep2), "unit": UNIT, "cores": threads, "kind": "port",
                "sample": cpu_sample_text(threads) + " (mean of 2 samples)", "measured_seconds": meas + meas2}
+        if not args.no_extras:
+            del data
+            if "fullgrad" in extras:
+                extras["fullgrad"]["C4"]["cpu_baseline"] = cpu_c4_fullgrad(O, threads)
+            if "batch" in extras:
+                extras["batch"]["cpu_baseline"] = cpu_c5_batch(O, threads)
 
     if rank == 0:
         line = {

@@ -88,11 +88,19 @@ __device__ __forceinline__ void st_async_v2f64(uint32_t raddr, double a, double 
                : "memory");
 }
 
-__device__ __forceinline__ void red_async_u64(uint32_t raddr, unsigned long long v, uint32_t rbar) {
-  asm volatile("red.async.relaxed.cluster.shared::cluster.mbarrier::complete_tx::bytes.add.u64 [%0], %1, [%2];" ::"r"(
-                   raddr),
-               "l"(v), "r"(rbar)
+__device__ __forceinline__ void st_async_v2s64(uint32_t raddr, long long a, long long b, uint32_t rbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.s64 [%0], {%1, %2}, [%3];" ::"r"(raddr),
+               "l"(a), "l"(b), "r"(rbar)
                : "memory");
+}
+
+// exact warp sum of one int64 per lane whose absolute values sum to < 2^61 over
+// the warp: three 21-bit limbs through REDUX.SUM (32-bit), recombined
+__device__ __forceinline__ long long warp_sum_s64(long long v) {
+  const int lo = __reduce_add_sync(0xffffffffu, (int)(v & 0x1FFFFF));
+  const int mi = __reduce_add_sync(0xffffffffu, (int)((v >> 21) & 0x1FFFFF));
+  const int hi = __reduce_add_sync(0xffffffffu, (int)(v >> 42));
+  return (long long)hi * (1LL << 42) + (long long)mi * (1LL << 21) + (long long)lo;
 }
 
 // the M raw elements x[fj[i]] of a row (one vector load when they are
@@ -150,11 +158,14 @@ struct K3Layout {
 // non-finite sends this signalling-NaN pattern in place of all its partials
 // (arithmetic never produces it; NaN logits make receivers rescan for it).
 constexpr long long kFlagBits = 0x7FF4A1B2C3D4E5F6LL;
+// FX records (integer sums, |sum| < 2^60) carry it as values no sum can take:
+// the sender's previous update was non-finite / one of its partials is not finite
+constexpr long long kFxFlag = (long long)0x8000000000000001ULL, kFxNan = (long long)0x8000000000000002ULL;
 
 template <class Tx, int M, bool CL, int KIND, bool BASE0, bool LV2, bool FX>
 __global__ void __launch_bounds__(256, 1) k3_inner(InParams p) {
   static_assert(!LV2 || (KIND == 0 && CL), "two-level exchange: squared loss on a cluster");
-  static_assert(!FX || (KIND == 0 && CL && !BASE0 && !LV2), "fixed-point exchange: HALP squared loss on a cluster");
+  static_assert(!FX || (KIND == 0 && !BASE0 && !LV2), "fixed-point exchange: HALP squared loss");
   constexpr int NSLOT = K3Layout<KIND>::NSLOT;
   constexpr int FLAG = K3Layout<KIND>::FLAG;
   constexpr bool SQ = KIND == 0;
@@ -162,7 +173,6 @@ __global__ void __launch_bounds__(256, 1) k3_inner(InParams p) {
   __shared__ __align__(8) uint64_t mbar[2];
   __shared__ __align__(16) double gsc[2][8][32];  // softmax gathers: [parity][warp][lane]
   __shared__ __align__(16) double ctar[2][8][2];  // LV2: this CTA's warp records [parity][warp]
-  __shared__ __align__(8) unsigned long long fxacc[2][4];  // FX: running sums [parity]: a, b, flags
   extern __shared__ __align__(16) double xbuf_dyn[];  // [2][NGW][NSLOT]
 
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, NW = blockDim.x >> 5;
@@ -178,12 +188,11 @@ __global__ void __launch_bounds__(256, 1) k3_inner(InParams p) {
   const int WC = 32 * M;  // coordinates per warp
   const int PAR_STRIDE = NGW * NSLOT;  // doubles between the two parity buffers
   auto XB = [&](int par_, int q_, int slot_) -> double& { return xbuf_dyn[par_ * PAR_STRIDE + q_ * NSLOT + slot_]; };
-  const uint32_t bytes_step = FX ? (uint32_t)NGW * 24u : KIND == 0 ? (uint32_t)NREC * 16u
+  const uint32_t bytes_step = KIND == 0 ? (uint32_t)NREC * 16u
                               : KIND == 1 ? (uint32_t)NGW * 32u
                                           : (uint32_t)NGW * (uint32_t)(2 * C + 1) * 8u;
 
   for (int i = tid; i < 2048; i += blockDim.x) jt[i] = p.jump_tab[i];
-  if (tid < 8) (&fxacc[0][0])[tid] = 0ull;
   if (CL && tid == 0) {
     mbar_init(&mbar[0], 1);
     mbar_init(&mbar[1], 1);
@@ -201,8 +210,7 @@ __global__ void __launch_bounds__(256, 1) k3_inner(InParams p) {
   if (CL && KIND == 0) {
     const int r0 = lane & 15;
     s0ok = lane < 16 && r0 < NC;
-    ra0 = FX ? mapa_u32(&fxacc[0][0], (uint32_t)(s0ok ? r0 : 0))
-             : mapa_u32(&XB(0, LV2 ? (int)rank : gw, 0), (uint32_t)(s0ok ? r0 : 0));
+    ra0 = mapa_u32(&XB(0, LV2 ? (int)rank : gw, 0), (uint32_t)(s0ok ? r0 : 0));
     rb0 = mapa_u32(&mbar[0], (uint32_t)(s0ok ? r0 : 0));
   } else if (CL && KIND == 1) {
     const int slot = 2 * (lane >> 4);
@@ -294,7 +302,6 @@ __global__ void __launch_bounds__(256, 1) k3_inner(InParams p) {
   if (CL) cluster_sync_all();
 
   int bad_prev = 0;
-  unsigned long long fx_pa0 = 0, fx_pa1 = 0, fx_pb0 = 0, fx_pb1 = 0, fx_pf0 = 0, fx_pf1 = 0;  // FX totals seen
 #ifdef HALP_K3_PROF
   const bool prof_on = rank == 0 && tid == 0;
   long long prof_acc[16] = {}, prof_last = clock64();
@@ -349,26 +356,21 @@ __global__ void __launch_bounds__(256, 1) k3_inner(InParams p) {
     const double fnan = __longlong_as_double(kFlagBits);
     if constexpr (FX) {
       // fixed point: every thread's partials rounded to integers at 2^S (S from a
-      // bound on |x| |w~ + z| chosen per epoch so no sum can reach 2^61), the warp
-      // sums by REDUX on 21-bit limbs, one remote integer reduction per CTA
-      // (red.async) -- integer sums are exact, so the order of arrival is irrelevant
+      // bound on |x| |w~ + z| chosen per epoch so no sum can reach 2^60), the warp
+      // sums by REDUX on 21-bit limbs, one integer record per warp to every CTA --
+      // integer sums are exact, so the order of the combine is irrelevant
       const bool nanp = !(isfinite(a0) && isfinite(b0));
       const long long A = nanp ? 0 : __double2ll_rn(__dmul_rn(a0, p.fx_scale));
       const long long B = nanp ? 0 : __double2ll_rn(__dmul_rn(b0, p.fx_scale));
-      const int a_lo = __reduce_add_sync(0xffffffffu, (int)(A & 0x1FFFFF));
-      const int a_mi = __reduce_add_sync(0xffffffffu, (int)((A >> 21) & 0x1FFFFF));
-      const int a_hi = __reduce_add_sync(0xffffffffu, (int)(A >> 42));
-      const int b_lo = __reduce_add_sync(0xffffffffu, (int)(B & 0x1FFFFF));
-      const int b_mi = __reduce_add_sync(0xffffffffu, (int)((B >> 21) & 0x1FFFFF));
-      const int b_hi = __reduce_add_sync(0xffffffffu, (int)(B >> 42));
-      const long long SA = (long long)a_hi * (1LL << 42) + (long long)a_mi * (1LL << 21) + (long long)a_lo;
-      const long long SB = (long long)b_hi * (1LL << 42) + (long long)b_mi * (1LL << 21) + (long long)b_lo;
-      const unsigned long long F = (flag ? 1ull : 0ull) + (__any_sync(0xffffffffu, nanp) ? (1ull << 32) : 0ull);
-      if (s0ok) {
-        const uint32_t xo = par ? 32u : 0u, mo = par ? mb_par_off : 0u;
-        red_async_u64(ra0 + xo, (unsigned long long)SA, rb0 + mo);
-        red_async_u64(ra0 + xo + 8u, (unsigned long long)SB, rb0 + mo);
-        red_async_u64(ra0 + xo + 16u, F, rb0 + mo);
+      long long SA = warp_sum_s64(A);
+      const long long SB = warp_sum_s64(B);
+      if (__any_sync(0xffffffffu, nanp)) SA = kFxNan;
+      if (flag) SA = kFxFlag;
+      if (CL) {
+        const uint32_t xo = par ? xb_par_off : 0u, mo = par ? mb_par_off : 0u;
+        if (s0ok) st_async_v2s64(ra0 + xo, SA, SB, rb0 + mo);
+      } else {
+        if (lane == 0) *reinterpret_cast<longlong2*>(&XB(par, gw, 0)) = make_longlong2(SA, SB);
       }
     } else if constexpr (KIND == 0) {
       // all-reduce butterfly of a0 on lanes 0..15 and of b0 on lanes 16..31
@@ -476,21 +478,32 @@ __global__ void __launch_bounds__(256, 1) k3_inner(InParams p) {
     const double* xbp = xbuf_dyn + par * PAR_STRIDE;
     double fxa = 0.0, fxb = 0.0;
     if constexpr (FX) {
-      // this step's sums = running totals minus the totals two steps ago (mod 2^64: exact)
-      const unsigned long long ca = fxacc[par][0], cb = fxacc[par][1], cf = fxacc[par][2];
-      const unsigned long long da = ca - (par ? fx_pa1 : fx_pa0), db = cb - (par ? fx_pb1 : fx_pb0);
-      const unsigned long long df = cf - (par ? fx_pf1 : fx_pf0);
-      if (par) { fx_pa1 = ca; fx_pb1 = cb; fx_pf1 = cf; } else { fx_pa0 = ca; fx_pb0 = cb; fx_pf0 = cf; }
-      if ((uint32_t)df != 0u) {  // some warp's previous update was non-finite: blow-up of step t-1
+      // every lane sums its records (integers), the warp by REDUX; flag values are counted apart
+      long long pa = 0, pb = 0;
+      int fb = 0;
+#pragma unroll
+      for (int j = 0; j < kMaxWarpsPerCluster / 32; ++j) {
+        const int q = lane + 32 * j;
+        if (q < NREC) {
+          const longlong2 v = *reinterpret_cast<const longlong2*>(xbp + q * NSLOT);
+          const bool isf = v.x == kFxFlag, isn = v.x == kFxNan;
+          fb |= (isf ? 1 : 0) | (isn ? 2 : 0);
+          pa += (isf || isn) ? 0 : v.x;
+          pb += v.y;
+        }
+      }
+      fb = (int)__reduce_or_sync(0xffffffffu, (unsigned)fb);
+      if (fb & 1) {  // some warp's previous update was non-finite: blow-up of step t-1
         store_m<M>(p.u_out + k0, up, valid, allv);  // no update yet at step t: up holds u of step t-1
         if (rank == 0 && tid == 0) *p.blow_step = (long long)(t - 1);
-        cluster_sync_all();
+        if (CL) cluster_sync_all();
         return;
       }
       if (last) break;
-      const bool nanstep = (df >> 32) != 0ull;  // a partial was not finite: the reference's dot is NaN
-      fxa = nanstep ? __longlong_as_double(0x7FF8000000000000LL) : __dmul_rn(__ll2double_rn((long long)da), p.fx_inv);
-      fxb = nanstep ? __longlong_as_double(0x7FF8000000000000LL) : __dmul_rn(__ll2double_rn((long long)db), p.fx_inv);
+      const long long da = warp_sum_s64(pa), db = warp_sum_s64(pb);
+      const bool nanstep = (fb & 2) != 0;  // a partial was not finite: the reference's dot is NaN
+      fxa = nanstep ? __longlong_as_double(0x7FF8000000000000LL) : __dmul_rn(__ll2double_rn(da), p.fx_inv);
+      fxb = nanstep ? __longlong_as_double(0x7FF8000000000000LL) : __dmul_rn(__ll2double_rn(db), p.fx_inv);
     }
     // blowup of step t-1?  Tested after this step's update (a blowup leaves
     // code[] dead; u of step t-1 is kept in upp[] and stored only then).  KIND 0/1: a lane
@@ -714,6 +727,8 @@ static cudaError_t launch_in_b(const InLaunch& L, const InParams& p, cudaStream_
   const size_t smem = sizeof(double) * 2 * (size_t)(L.ctas * L.threads / 32) * K3Layout<KIND>::NSLOT;
   if (L.ctas == 1) {
     auto kern = k3_inner<Tx, M, false, KIND, BASE0, false, false>;
+    if constexpr (KIND == 0 && !BASE0)
+      if (L.levels == 3) kern = k3_inner<Tx, M, false, KIND, BASE0, false, true>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     if (L.dry) return cudaSuccess;
