@@ -466,7 +466,7 @@ def main():
         Xn = Xh.numpy()
         del obj, X, y
         torch.cuda.empty_cache()
-        e_steps = max(1, min(args.steps, 3))
+        e_steps = max(1, min(args.steps, 6))  # streamed solves: the first upload is not overlapped, amortise it
         mk = lambda: H.Objective(H.Dataset(Xn, targets=yh), H.LossFamily.Squared, C3["l2"], device=local)
         # untimed warm-up: the first problems grow the device pool by two 68.7 GB
         # copies of X (later problems reuse them), like the headline's warm-up epochs

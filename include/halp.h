@@ -156,7 +156,7 @@ typedef struct {
   int32_t in_ctas, in_threads, in_per;
   int32_t fg_rows_per_stage, fg_stages;
   int64_t fg_split_begin, fg_split_end; /* this rank's splits */
-  int32_t in_levels;                    /* K3 cross-warp combine: 1 warps of the cluster, 2 CTA then cluster */
+  int32_t in_levels;                    /* K3 cross-warp combine: 1 warp records (fp64), 2 CTA records then cluster, 3 fixed-point integer records (HALP_IN_LEVELS overrides the default 1) */
 } halp_plan;
 
 const char* halp_last_error(void);

@@ -162,8 +162,12 @@ constexpr long long kFlagBits = 0x7FF4A1B2C3D4E5F6LL;
 // the sender's previous update was non-finite / one of its partials is not finite
 constexpr long long kFxFlag = (long long)0x8000000000000001ULL, kFxNan = (long long)0x8000000000000002ULL;
 
-template <class Tx, int M, bool CL, int KIND, bool BASE0, bool LV2, bool FX>
+// FAST (HALP, squared loss, plain exchange): every coordinate slot is a real coordinate
+// (D = threads * M), no option-II snapshot, no code trace, the reciprocal quantizer applies --
+// the launcher checks it; the per-step predicates and selects of those cases compile away.
+template <class Tx, int M, bool CL, int KIND, bool BASE0, bool LV2, bool FX, bool FAST = false>
 __global__ void __launch_bounds__(256, 1) k3_inner(InParams p) {
+  static_assert(!FAST || (KIND == 0 && !BASE0 && !LV2 && !FX), "fast path: HALP squared loss, fp64 records");
   static_assert(!LV2 || (KIND == 0 && CL), "two-level exchange: squared loss on a cluster");
   static_assert(!FX || (KIND == 0 && !BASE0 && !LV2), "fixed-point exchange: HALP squared loss");
   constexpr int NSLOT = K3Layout<KIND>::NSLOT;
@@ -259,7 +263,7 @@ __global__ void __launch_bounds__(256, 1) k3_inner(InParams p) {
 #pragma unroll
   for (int i = 0; i < M; ++i) {
     const int64_t k = k0 + i;
-    valid[i] = k < D;
+    valid[i] = FAST || k < D;
     allv = allv && valid[i];
     cls[i] = valid[i] ? (int)(k / d) : 0;
     fj[i] = valid[i] ? (int)(k % d) : 0;
@@ -308,13 +312,43 @@ __global__ void __launch_bounds__(256, 1) k3_inner(InParams p) {
 #endif
   for (int64_t t = 0; t <= T; ++t) {
     K3_MARK(7);
-    const bool last = (t == T);
+    if constexpr (FAST) {
+      // the exchange after the last step only carries step T-1's blow-up flag: handled here,
+      // so `last` is a compile-time false in the step below
+      if (t == T) {
+        const int parL = (int)(t & 1);
+        if (CL && tid == 0) mbar_expect_tx(&mbar[parL], bytes_step);
+        const double vL = __any_sync(0xffffffffu, bad_prev) ? __longlong_as_double(kFlagBits) : 0.0;
+        if (CL) {
+          if (s0ok) st_async_v2f64(ra0 + (parL ? xb_par_off : 0u), vL, vL, rb0 + (parL ? mb_par_off : 0u));
+          mbar_wait_cluster(&mbar[parL], (uint32_t)((t >> 1) & 1));
+        } else {
+          if (lane == 0) *reinterpret_cast<double2*>(&XB(parL, gw, 0)) = make_double2(vL, vL);
+          __syncthreads();
+        }
+        const double* xbL = xbuf_dyn + parL * PAR_STRIDE;
+        int f = 0;
+#pragma unroll
+        for (int j = 0; j < kMaxWarpsPerCluster / 32; ++j) {
+          const int q = lane + 32 * j;
+          if (q < NREC) f |= __double_as_longlong(xbL[q * NSLOT]) == kFlagBits;
+        }
+        if (__any_sync(0xffffffffu, f)) {
+          store_m<M>(p.u_out + k0, up, valid, allv);  // u of step T-1
+          if (rank == 0 && tid == 0) *p.blow_step = (long long)(t - 1);
+          if (CL) cluster_sync_all();
+          return;
+        }
+        break;
+      }
+    }
+    const bool last = FAST ? false : (t == T);
     const int par = (int)(t & 1);
     if (CL && tid == 0) mbar_expect_tx(&mbar[par], bytes_step);
     double xc[M];
     double a0 = 0.0, b0 = 0.0, a1 = 0.0, b1 = 0.0;
     if (!last) {
-      if (t == p.t_pick) {
+      if (!FAST && t == p.t_pick) {
 #pragma unroll
         for (int i = 0; i < M; ++i) snap[i] = code[i];
       }
@@ -677,10 +711,10 @@ __global__ void __launch_bounds__(256, 1) k3_inner(InParams p) {
       slow_any |= !fp_inner && valid[i] && slow[i];
     }
     if (fp_inner) bad = false;  // SVRG / SGD: no finiteness check inside the epoch (optimizers.cpp:244-246, 283-286)
-    if (!fp_inner && (slow_any || wide || rcp == 0.0)) {  // IEEE-division path for the rare operands
+    if (!fp_inner && (slow_any || (!FAST && (wide || rcp == 0.0)))) {  // IEEE-division path for the rare operands
 #pragma unroll
       for (int i = 0; i < M; ++i)
-        if (valid[i] && (slow[i] || wide || rcp == 0.0))
+        if (valid[i] && (slow[i] || (!FAST && (wide || rcp == 0.0))))
           code[i] = (double)quantize_code(up[i], delta, p.hi, p.lo, p.maxc, p.minc, Ua[i]);
     }
     if (__any_sync(0xffffffffu, fl) && (KIND == 2 || flagged())) {
@@ -692,7 +726,7 @@ __global__ void __launch_bounds__(256, 1) k3_inner(InParams p) {
     }
     bad_prev = bad ? 1 : 0;
     K3_MARK(6);
-    if (t < p.trace_steps) {
+    if (!FAST && t < p.trace_steps) {
 #pragma unroll
       for (int i = 0; i < M; ++i)
         if (valid[i]) p.trace[t * D + k0 + i] = __double2ll_rn(code[i]);
@@ -701,7 +735,7 @@ __global__ void __launch_bounds__(256, 1) k3_inner(InParams p) {
 #pragma unroll
   for (int i = 0; i < M; ++i) {
     if (!valid[i]) continue;
-    const double zc = p.t_pick >= 0 ? snap[i] : code[i];
+    const double zc = (!FAST && p.t_pick >= 0) ? snap[i] : code[i];
     const double zr = __dmul_rn(zc, delta);
     p.w_out[k0 + i] = base0 ? zr : wt[i] + zr;
     p.codes_out[k0 + i] = fp_inner ? 0 : __double2ll_rn(code[i]);
@@ -725,10 +759,18 @@ template <class Tx, int M, int KIND, bool BASE0>
 static cudaError_t launch_in_b(const InLaunch& L, const InParams& p, cudaStream_t st) {
   if (L.ctas * L.threads / 32 > kMaxWarpsPerCluster) return cudaErrorInvalidConfiguration;
   const size_t smem = sizeof(double) * 2 * (size_t)(L.ctas * L.threads / 32) * K3Layout<KIND>::NSLOT;
+  // the common HALP least-squares launch: no dead slots, no snapshot, no trace, reciprocal quantizer.
+  // Measured on B200 (profiles/r02_s4_k3_experiments.txt): 6-8% faster on cluster plans and on one
+  // CTA with M = 4, 11% slower on one CTA with M = 2 (C1's plan), which keeps the general kernel.
+  const bool fast = KIND == 0 && !BASE0 && L.levels <= 1 && (int64_t)p.D == (int64_t)L.ctas * L.threads * M &&
+                    p.t_pick < 0 && p.trace_steps == 0 && !(p.hi > 0x1.0p53) && p.rcp != 0.0 &&
+                    (L.ctas > 1 || M >= 4);
   if (L.ctas == 1) {
     auto kern = k3_inner<Tx, M, false, KIND, BASE0, false, false>;
-    if constexpr (KIND == 0 && !BASE0)
+    if constexpr (KIND == 0 && !BASE0) {
       if (L.levels == 3) kern = k3_inner<Tx, M, false, KIND, BASE0, false, true>;
+      else if (fast) kern = k3_inner<Tx, M, false, KIND, BASE0, false, false, true>;
+    }
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     if (L.dry) return cudaSuccess;
@@ -739,8 +781,10 @@ static cudaError_t launch_in_b(const InLaunch& L, const InParams& p, cudaStream_
   auto kern = k3_inner<Tx, M, true, KIND, BASE0, false, false>;
   if constexpr (KIND == 0) {
     if (L.levels == 2) kern = k3_inner<Tx, M, true, KIND, BASE0, true, false>;
-    if constexpr (!BASE0)
+    if constexpr (!BASE0) {
       if (L.levels == 3) kern = k3_inner<Tx, M, true, KIND, BASE0, false, true>;
+      else if (fast) kern = k3_inner<Tx, M, true, KIND, BASE0, false, false, true>;
+    }
   }
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   if (e != cudaSuccess) return e;

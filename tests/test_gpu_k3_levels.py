@@ -67,3 +67,54 @@ def test_fixed_point_nan_data_blows_up_like_oracle(H, oracle, monkeypatch):
     # float.hex: NaN rows compare equal (nan != nan as floats)
     assert [(r.pass_, float(r.loss).hex(), r.iterate_hash) for r in e.value.partial.rows] == \
         [(r["pass_"], float(r["loss"]).hex(), r["iterate_hash"]) for r in orec.rows]
+
+
+def test_fixed_point_one_cta(H, oracle, monkeypatch):
+    """in_levels = 3 on a single CTA (records through shared memory + __syncthreads)"""
+    monkeypatch.setenv("HALP_IN_LEVELS", "3")
+    monkeypatch.setenv("HALP_IN_NC", "1")
+    monkeypatch.setenv("HALP_IN_M", "2")
+    X, y = oracle.generate("regression", 4096, 256, dtype="f32", noise_sd=0.01, seed=11)
+    g = H.Objective(H.Dataset(X, targets=y), H.LossFamily.Squared, 0.0)
+    plan = g.oracle_plan()
+    assert plan["in_levels"] == 3 and plan["in_ctas"] == 1
+    cfg = dict(alpha=1e-3, epochs=2, inner_steps=2000, bits=8, mu=10.0, seed=3)
+    steps = 400
+    tr = np.zeros(steps * 256, dtype=np.int64)
+    rec = H.run_halp(g, H.OptimizerConfig(algorithm=H.Algorithm.Halp, **cfg), trace=tr)
+    o = oracle.OracleObjective(X, y=y)
+    orec = oracle.run_halp(o, oracle.OracleConfig(**cfg), plan=plan, trace_steps=steps)
+    assert [(r.loss, r.grad_norm, r.delta, r.iterate_hash) for r in rec.rows] == \
+        [(r["loss"], r["grad_norm"], r["delta"], r["iterate_hash"]) for r in orec.rows]
+    assert np.array_equal(tr.reshape(steps, 256), orec.trace)
+
+
+@pytest.mark.parametrize("d,nc,m", [(4096, 16, 2), (4096, 8, 4), (256, 1, 2), (250, 1, 2)])
+def test_untraced_launch_equals_traced(H, oracle, monkeypatch, d, nc, m):
+    """The launch without a code trace (the specialised FAST instantiation when
+    every coordinate slot is real: d = 4096 / 256; d = 250 leaves dead slots and
+    stays on the general kernel) gives the rows, hashes and iterate of the traced
+    launch and of the oracle, including a mid-epoch blow-up."""
+    monkeypatch.setenv("HALP_IN_NC", str(nc))
+    monkeypatch.setenv("HALP_IN_M", str(m))
+    X, y = oracle.generate("regression", 3000, d, dtype="f32", noise_sd=0.1, seed=5)
+    g = H.Objective(H.Dataset(X, targets=y), H.LossFamily.Squared, 1e-6)
+    plan = g.oracle_plan()
+    assert plan["in_ctas"] == nc and plan["in_per"] == m
+    cfg = dict(alpha=0.3 / d, epochs=3, inner_steps=1200, bits=16, mu=2.0, seed=9)
+    tr = np.zeros(50 * d, dtype=np.int64)
+    traced = H.run_halp(g, H.OptimizerConfig(algorithm=H.Algorithm.Halp, **cfg), trace=tr)
+    plain = H.run_halp(g, H.OptimizerConfig(algorithm=H.Algorithm.Halp, **cfg))
+    o = oracle.OracleObjective(X, y=y, l2=1e-6)
+    orec = oracle.run_halp(o, oracle.OracleConfig(**cfg), plan=plan)
+    key = lambda r: (r.loss, r.grad_norm, r.delta, r.iterate_hash)
+    assert [key(r) for r in plain.rows] == [key(r) for r in traced.rows]
+    assert [key(r) for r in plain.rows] == [(r["loss"], r["grad_norm"], r["delta"], r["iterate_hash"]) for r in orec.rows]
+    assert np.array_equal(plain.final_iterate, traced.final_iterate)
+    assert np.array_equal(plain.final_iterate, orec.final_iterate)
+    bad = dict(cfg, alpha=1e308)
+    with pytest.raises(H.DivergenceError) as e:
+        H.run_halp(g, H.OptimizerConfig(algorithm=H.Algorithm.Halp, **bad))
+    orec = oracle.run_halp(o, oracle.OracleConfig(**bad), plan=plan)
+    assert [(r.pass_, r.iterate_hash) for r in e.value.partial.rows] == \
+        [(r["pass_"], r["iterate_hash"]) for r in orec.rows]
