@@ -423,6 +423,7 @@ int plan_for(int64_t n, int d, int C, int dtype, KernelPlan* kp) {
     const bool can = C == 1 && NC > 1 && T3 >= 64;
     const bool can_fx = C == 1;
     kp->in.levels = lv == 3 && can_fx ? 3 : can && lv == 2 ? 2 : lv == 1 ? 1 : (can_fx && kDefaultInLevels == 3) ? 3 : 1;
+    kp->in.pf2 = (int)env_int("HALP_K3_PF2", -1);
   }
   return HALP_OK;
 }

@@ -60,7 +60,19 @@ constexpr int kMaxWarpsPerCluster = 128;
   } while (0)
 #endif
 
+#ifndef HALP_K3_WAIT
+#define HALP_K3_WAIT 0  // 0: relaxed cluster-scope wait + shared::cluster acquire fence; 1: default (acquire, CTA scope) wait
+#endif
 __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+#if HALP_K3_WAIT == 1
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "W_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra W_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+#else
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "W_%=:\n\t"
@@ -71,6 +83,7 @@ __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity
   // the payload arrived by st.async into OUR shared memory: an acquire restricted
   // to shared::cluster suffices (a plain .acquire.cluster wait also invalidates L1)
   asm volatile("fence.acquire.sync_restrict::shared::cluster.cluster;" ::: "memory");
+#endif
 }
 __device__ __forceinline__ uint32_t mapa_u32(const void* p, uint32_t rank) {
   uint32_t ra;
@@ -788,7 +801,7 @@ static cudaError_t launch_in_b(const InLaunch& L, const InParams& p, cudaStream_
                     p.t_pick < 0 && p.trace_steps == 0 && !(p.hi > 0x1.0p53) && p.rcp != 0.0 &&
                     (L.ctas > 1 || M >= 4);
   // a dataset well beyond the 126 MB L2: pull the sampled rows into L2 a step early
-  const bool pf2 = (double)p.n * p.ld * sizeof(Tx) > 256e6;
+  const bool pf2 = L.pf2 < 0 ? (double)p.n * p.ld * sizeof(Tx) > 256e6 : L.pf2 != 0;
   if (L.ctas == 1) {
     auto kern = k3_inner<Tx, M, false, KIND, BASE0, false, false>;
     if constexpr (KIND == 0 && !BASE0) {

@@ -99,7 +99,8 @@ struct InLaunch {
   int dtype, ctas, threads, per, nslot_pow2;
   int dry;     // 1: load + configure the kernel only (see FgLaunch::dry)
   int levels;  // 1: warp records exchanged across the cluster; 2: combined per CTA first;
-               // 3: fixed-point records summed by remote integer reductions (k_inner.cu FX)
+               // 3: fixed-point integer records (k_inner.cu FX)
+  int pf2;     // fast path L2 prefetch of the sampled rows: -1 by dataset size, 0 off, 1 on (HALP_K3_PF2)
 };
 cudaError_t launch_inner(const InLaunch& L, const InParams& p, cudaStream_t st);
 // max |x| over an n x ld matrix of the stored dtype -> *out (one double)
