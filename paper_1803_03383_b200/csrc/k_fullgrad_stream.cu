@@ -124,7 +124,10 @@ __device__ __forceinline__ void load_group_scaled(const Tx* p, double* out) {
 // ends with the full warp sum of slot l >> (5 - log2 NV).  The pairs added at
 // every level are the butterfly's, so each slot's value equals a plain
 // xor-butterfly all-reduce (addition is commutative).
-template <int NV>
+// PRE: the first PRE levels need no selects because the caller filled the slots in a
+// lane-dependent order (slot i of a lane holds row i ^ p, p = the lane's bits 4.. mapped
+// to the slot's top bits), so every lane keeps its low half and sends its high half.
+template <int NV, int PRE = 0>
 __device__ __forceinline__ void reduce_scatter_k(double (&v)[NV], int lane) {
 #pragma unroll
   for (int st = 0; st < 5; ++st) {
@@ -135,9 +138,13 @@ __device__ __forceinline__ void reduce_scatter_k(double (&v)[NV], int lane) {
       const bool up = (lane & off) != 0;
 #pragma unroll
       for (int i = 0; i < h; ++i) {
-        const double send = up ? v[i] : v[i + h];
-        const double keep = up ? v[i + h] : v[i];
-        v[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+        if (st < PRE) {
+          v[i] = v[i] + __shfl_xor_sync(0xffffffffu, v[i + h], off);
+        } else {
+          const double send = up ? v[i] : v[i + h];
+          const double keep = up ? v[i + h] : v[i];
+          v[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+        }
       }
     } else {
       v[0] = v[0] + __shfl_xor_sync(0xffffffffu, v[0], off);
@@ -174,6 +181,21 @@ __global__ void __launch_bounds__(NW * 32, (K1MinBlocks<Tx, CC, NW, R>::value)) 
   // RR: tiles of 16+ rows keep x in shared memory only and re-read it for the
   // gradient phase (registers for the row dots instead of an R x 8 fp64 slice)
   constexpr bool RR = R >= 16;
+  // DW: two classes on several warps: ONE warp per tile (rotating) evaluates the rows'
+  // softmax derivative (exp + division) and publishes it through shared memory behind a
+  // second barrier, another one the loss terms (log), instead of every warp repeating
+  // both for the same R rows -- the sweep is issue-bound
+#ifndef HALP_K1_DW
+#define HALP_K1_DW 1
+#endif
+  constexpr bool DW = HALP_K1_DW && CC == 2 && NW > 1;
+  // RL: 16-row tiles fill the dot slots in a lane-dependent row order (slot i = row
+  // i ^ p, p = 8 * lane bit 4 + 4 * lane bit 3), which makes the first two levels of the
+  // reduce-scatter select-free; four lane-dependent row bases keep the offsets immediate
+#ifndef HALP_K1_RELABEL
+#define HALP_K1_RELABEL 1
+#endif
+  constexpr bool RL = HALP_K1_RELABEL && RR && NV == 16;
   static_assert(CC == 1 || CC == 2, "least squares or two classes");
   static_assert((NV & (NV - 1)) == 0 && NV <= 32, "R must be a power of two <= 32");
   extern __shared__ __align__(128) unsigned char smem[];
@@ -186,7 +208,8 @@ __global__ void __launch_bounds__(NW * 32, (K1MinBlocks<Tx, CC, NW, R>::value)) 
   Tx* stages = reinterpret_cast<Tx*>(smem);
   double* red = reinterpret_cast<double*>(smem + (size_t)STAGES * stage_elems * sizeof(Tx));  // [2][NW][NV]
   double* lts = red + 2 * NW * NV;  // [2][NW][R] per-row losses (two classes), parity double-buffered
-  uint64_t* bars = reinterpret_cast<uint64_t*>(lts + 2 * NW * R);
+  double* dsh = lts + 2 * NW * R;  // [R][2] {dl, dl * 2^896} + [R][2] {a, 1 + q} (two classes, DW)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(dsh + 4 * R);
   const Tx* X = reinterpret_cast<const Tx*>(p.X);
   const unsigned long long nn = (unsigned long long)p.n, SS = (unsigned long long)p.S;
 
@@ -293,18 +316,26 @@ __global__ void __launch_bounds__(NW * 32, (K1MinBlocks<Tx, CC, NW, R>::value)) 
       auto body = [&](auto full_tag) {
         constexpr bool FULL = decltype(full_tag)::value;
         // row r's x slice of this thread, upcast exactly (zeros past the tile / row end)
-        auto load_row = [&](int r, double (&xg)[NG][V]) {
+        auto load_row_at = [&](const Tx* rowp, bool valid, double (&xg)[NG][V]) {
 #pragma unroll
           for (int k = 0; k < NG; ++k) {
-            if ((FULL || r < nr) && gval[k]) {
-              if constexpr (SC) load_group_scaled<Tx>(xs + (int64_t)r * ld + (tid + k * T1) * V, xg[k]);
-              else load_group_k<Tx>(xs + (int64_t)r * ld + (tid + k * T1) * V, xg[k]);
+            if ((FULL || valid) && gval[k]) {
+              if constexpr (SC) load_group_scaled<Tx>(rowp + (tid + k * T1) * V, xg[k]);
+              else load_group_k<Tx>(rowp + (tid + k * T1) * V, xg[k]);
             } else {
 #pragma unroll
               for (int q = 0; q < V; ++q) xg[k][q] = 0.0;
             }
           }
         };
+        auto load_row = [&](int r, double (&xg)[NG][V]) { load_row_at(xs + (int64_t)r * ld, r < nr, xg); };
+        // RL: slot r's row is r ^ p = r +- p8 +- p4 (signs by slot bits 3, 2): base[bits] + r * ld
+        const int p8 = (lane & 16) ? 8 : 0, p4 = (lane & 8) ? 4 : 0;
+        const Tx* xb[4];
+        if constexpr (RL) {
+#pragma unroll
+          for (int bi = 0; bi < 4; ++bi) xb[bi] = xs + (int64_t)(((bi & 2) ? -p8 : p8) + ((bi & 1) ? -p4 : p4)) * ld;
+        }
         double xr[RR ? 1 : R][NG][V];
         double acc[NV];
 #pragma unroll
@@ -315,13 +346,14 @@ __global__ void __launch_bounds__(NW * 32, (K1MinBlocks<Tx, CC, NW, R>::value)) 
         }
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-          if constexpr (RR) load_row(r, xr[0]);
+          if constexpr (RL) load_row_at(xb[((r >> 3) & 1) * 2 + ((r >> 2) & 1)] + (int64_t)r * ld, (r ^ (p8 | p4)) < nr, xr[0]);
+          else if constexpr (RR) load_row(r, xr[0]);
 #pragma unroll
           for (int k = 0; k < NG; ++k)
 #pragma unroll
             for (int q = 0; q < V; ++q) acc[r] = fma(xr[RR ? 0 : r][k][q], wr[k][q], acc[r]);
         }
-        reduce_scatter_k<NV>(acc, lane);
+        reduce_scatter_k<NV, RL ? 2 : 0>(acc, lane);
         if ((lane & ((32 >> LG) - 1)) == 0) rb[wid * NV + (lane >> (5 - LG))] = acc[0];
         __syncthreads();
         // x in registers: this tile's stage can be refilled now; x re-read in the
@@ -335,58 +367,78 @@ __global__ void __launch_bounds__(NW * 32, (K1MinBlocks<Tx, CC, NW, R>::value)) 
         }
 
         // logit of slot (fr, fc): the NW warp partials summed in warp order
-        double lg = 0.0;
-        if (lane < NV) {
-          double pv[NW];
+        auto row_logit = [&]() {
+          double lg = 0.0;
+          if (lane < NV) {
+            double pv[NW];
 #pragma unroll
-          for (int w2 = 0; w2 < NW; ++w2) pv[w2] = rb[w2 * NV + lane];
-          lg = pv[0];
+            for (int w2 = 0; w2 < NW; ++w2) pv[w2] = rb[w2 * NV + lane];
+            lg = pv[0];
 #pragma unroll
-          for (int w2 = 1; w2 < NW; ++w2) lg = lg + pv[w2];
-        }
-        double pr, lt = 0.0;
-        if constexpr (CC == 1) {
+            for (int w2 = 1; w2 < NW; ++w2) lg = lg + pv[w2];
+          }
+          return lg;
+        };
+        double pr = 0.0, lt = 0.0;
+        if constexpr (DW) {
+          if (wid == (int)(jseq & (NW - 1))) {
+            // two-class softmax, logistic form (mirror_logistic_row): s = lg
+            const double lg = row_logit();
+            const int lab = (int)tcur;
+            const double q = hexp_nonpos(-fabs(lg));  // = hexp, branch-free
+            const double den = 1.0 + q;
+            const double p0 = (lg > 0.0 ? q : 1.0) / den;
+            const double prw = lab == 0 ? p0 - 1.0 : p0;
+            if (lane < NV) {
+              *reinterpret_cast<double2*>(dsh + 2 * lane) = make_double2(prw, __dmul_rn(prw, 0x1.0p896));  // |prw| <= 1: exact
+              *reinterpret_cast<double2*>(dsh + 2 * R + 2 * lane) = make_double2(lab == 0 ? lg : -lg, den);
+            }
+          }
+          __syncthreads();
+          if (wid == (int)((jseq + NW / 2) & (NW - 1))) {
+            // the loss terms (a log per row) on another warp, summed by warp 0 in row order one tile later
+            if (lane < NV) {
+              const double2 ad = *reinterpret_cast<const double2*>(dsh + 2 * R + 2 * lane);
+              lts[(jseq & 1) * R + lane] = (ad.x > 0.0 ? ad.x : 0.0) + hlog_1to2(ad.y);  // = hlog on [1, 2]
+            }
+          }
+          if (wid == 0 && i > 0) {
+            const double* lp = lts + ((jseq - 1) & 1) * R;  // previous tile: full
+#pragma unroll
+            for (int r = 0; r < R; ++r) la = la + lp[r];
+          }
+        } else if constexpr (CC == 1) {
+          const double lg = row_logit();
           pr = lg - tcur;
           lt = __dmul_rn(__dmul_rn(0.5, pr), pr);
         } else {
           // two-class softmax, logistic form (mirror_logistic_row): s = lg
+          const double lg = row_logit();
           const int lab = (int)tcur;
-#ifdef HALP_K1_NOEXP
-          const double q = __dmul_rn(lg, 0.25);
-          const double den = 1.0 + q;
-          const double p0 = __dmul_rn(q, den);
-#else
           const double q = hexp_nonpos(-fabs(lg));  // = hexp, branch-free
           const double den = 1.0 + q;
           const double p0 = (lg > 0.0 ? q : 1.0) / den;
-#endif
           pr = lab == 0 ? p0 - 1.0 : p0;
           if constexpr (SC && !MIXED) pr = __dmul_rn(pr, 0x1.0p896);  // |pr| <= 1: exact
-          // the loss terms (a log per row): every warp evaluates them (straight-line
-          // code the scheduler overlaps with the gradient phase; a branch on one
-          // rotating warp made the others wait for it at the next barrier) into
-          // its own slot; warp 0 sums its copy in row order one tile later
           {
             const double a = lab == 0 ? lg : -lg;
-#ifdef HALP_K1_NOLOSS
-            const double lterm = (a > 0.0 ? a : 0.0) + den;
-#else
             const double lterm = (a > 0.0 ? a : 0.0) + hlog_1to2(den);  // = hlog on [1, 2]
-#endif
-            if (lane < NV) lts[((jseq & 1) * NW + wid) * R + lane] = lterm;
+            if (lane < NV) lts[(jseq & 1) * R + lane] = lterm;
           }
           if (wid == 0 && i > 0) {
-            const double* lp = lts + ((jseq - 1) & 1) * NW * R;  // previous tile, warp 0's copy: full
+            const double* lp = lts + ((jseq - 1) & 1) * R;  // previous tile: full
 #pragma unroll
             for (int r = 0; r < R; ++r) la = la + lp[r];
           }
         }
-        double dlr[NV], dls[SC && MIXED ? NV : 1];
+        double dlr[DW ? 1 : NV], dls[!DW && SC && MIXED ? NV : 1];
+        if constexpr (!DW) {
 #pragma unroll
-        for (int v = 0; v < NV; ++v) dlr[v] = __shfl_sync(0xffffffffu, pr, v);
-        if constexpr (SC && MIXED) {
+          for (int v = 0; v < NV; ++v) dlr[v] = __shfl_sync(0xffffffffu, pr, v);
+          if constexpr (SC && MIXED) {
 #pragma unroll
-          for (int v = 0; v < NV; ++v) dls[v] = __dmul_rn(dlr[v], 0x1.0p896);  // odd features: scaled domain
+            for (int v = 0; v < NV; ++v) dls[v] = __dmul_rn(dlr[v], 0x1.0p896);  // odd features: scaled domain
+          }
         }
         if (CC == 1 && wid == 0) {
 #pragma unroll
@@ -399,12 +451,21 @@ __global__ void __launch_bounds__(NW * 32, (K1MinBlocks<Tx, CC, NW, R>::value)) 
         for (int r = 0; r < R; ++r) {
           if (FULL || r < nr) {
             if constexpr (RR) load_row(r, xr[0]);
+            double dl_r, dl_s;  // row r's derivative, plain and in the 2^896-scaled domain (odd features)
+            if constexpr (DW) {
+              const double2 t2 = *reinterpret_cast<const double2*>(dsh + 2 * r);  // broadcast
+              dl_r = t2.x;
+              dl_s = t2.y;
+            } else {
+              dl_r = dlr[r];
+              dl_s = dls[SC && MIXED ? r : 0];
+            }
 #pragma unroll
             for (int k = 0; k < NG; ++k)
 #pragma unroll
               for (int q = 0; q < V; ++q)
-                gacc[k][q] = fma((SC && MIXED && k1_scaled_feature(q)) ? dls[SC && MIXED ? r : 0] : dlr[r],
-                                 xr[RR ? 0 : r][k][q], gacc[k][q]);
+                gacc[k][q] = fma((SC && MIXED && k1_scaled_feature(q)) ? dl_s : dl_r, xr[RR ? 0 : r][k][q],
+                                 gacc[k][q]);
           }
         }
       };
@@ -415,7 +476,7 @@ __global__ void __launch_bounds__(NW * 32, (K1MinBlocks<Tx, CC, NW, R>::value)) 
       __syncthreads();
       if (wid == 0 && ntile > 0) {
         const int nr_last = (int)(r1 - (r0 + (ntile - 1) * R));
-        const double* lp = lts + ((jseq - 1) & 1) * NW * R;
+        const double* lp = lts + ((jseq - 1) & 1) * R;
         for (int r = 0; r < nr_last; ++r) la = la + lp[r];
       }
     }
@@ -447,7 +508,7 @@ size_t stream_smem_bytes(int ld, int elem, int warps, int R, int CC, int stages)
   size_t b = (size_t)stages * R * ld * elem;
   b = (b + 15) / 16 * 16;
   (void)CC;
-  b += (size_t)2 * warps * R * 8 + (size_t)2 * warps * R * 8 + (size_t)stages * 8;
+  b += (size_t)2 * warps * R * 8 + (size_t)2 * warps * R * 8 + (size_t)4 * R * 8 + (size_t)stages * 8;
   return b;
 }
 
