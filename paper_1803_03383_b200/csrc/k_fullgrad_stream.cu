@@ -181,21 +181,24 @@ __global__ void __launch_bounds__(NW * 32, (K1MinBlocks<Tx, CC, NW, R>::value)) 
   // RR: tiles of 16+ rows keep x in shared memory only and re-read it for the
   // gradient phase (registers for the row dots instead of an R x 8 fp64 slice)
   constexpr bool RR = R >= 16;
-  // DW: two classes on several warps: ONE warp per tile (rotating) evaluates the rows'
-  // softmax derivative (exp + division) and publishes it through shared memory behind a
-  // second barrier, another one the loss terms (log), instead of every warp repeating
-  // both for the same R rows -- the sweep is issue-bound
+  // DW: two classes on several warps: ONE warp per tile (rotating over warps 1..) evaluates
+  // the rows' softmax derivative (exp + division) and publishes it through shared memory
+  // behind a second barrier, instead of every warp repeating it for the same R rows -- the
+  // sweep is issue-bound; the loss terms (log) and their running sum
+  // trail by one / two tiles and run in the same window on other warps
 #ifndef HALP_K1_DW
 #define HALP_K1_DW 1
 #endif
   constexpr bool DW = HALP_K1_DW && CC == 2 && NW > 1;
   // RL: 16-row tiles fill the dot slots in a lane-dependent row order (slot i = row
-  // i ^ p, p = 8 * lane bit 4 + 4 * lane bit 3), which makes the first two levels of the
-  // reduce-scatter select-free; four lane-dependent row bases keep the offsets immediate
+  // i ^ p, p = 8 * lane bit 4 + 4 * lane bit 3 [+ 2 * lane bit 2]), which makes the first
+  // two [three] levels of the reduce-scatter select-free; four [eight] lane-dependent row
+  // bases keep the shared-memory offsets immediate
 #ifndef HALP_K1_RELABEL
-#define HALP_K1_RELABEL 1
+#define HALP_K1_RELABEL 2  // relabeled levels (0: off; 3 uses eight row bases)
 #endif
-  constexpr bool RL = HALP_K1_RELABEL && RR && NV == 16;
+  constexpr bool RL = HALP_K1_RELABEL > 0 && RR && NV == 16;
+  constexpr int RLN = RL ? HALP_K1_RELABEL : 0;
   static_assert(CC == 1 || CC == 2, "least squares or two classes");
   static_assert((NV & (NV - 1)) == 0 && NV <= 32, "R must be a power of two <= 32");
   extern __shared__ __align__(128) unsigned char smem[];
@@ -208,8 +211,8 @@ __global__ void __launch_bounds__(NW * 32, (K1MinBlocks<Tx, CC, NW, R>::value)) 
   Tx* stages = reinterpret_cast<Tx*>(smem);
   double* red = reinterpret_cast<double*>(smem + (size_t)STAGES * stage_elems * sizeof(Tx));  // [2][NW][NV]
   double* lts = red + 2 * NW * NV;  // [2][NW][R] per-row losses (two classes), parity double-buffered
-  double* dsh = lts + 2 * NW * R;  // [R][2] {dl, dl * 2^896} + [R][2] {a, 1 + q} (two classes, DW)
-  uint64_t* bars = reinterpret_cast<uint64_t*>(dsh + 4 * R);
+  double* dsh = lts + 2 * NW * R;  // [R][2] {dl, dl * 2^896} + [2][R][2] {a, 1 + q} by tile parity (two classes, DW)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(dsh + 6 * R);
   const Tx* X = reinterpret_cast<const Tx*>(p.X);
   const unsigned long long nn = (unsigned long long)p.n, SS = (unsigned long long)p.S;
 
@@ -283,6 +286,7 @@ __global__ void __launch_bounds__(NW * 32, (K1MinBlocks<Tx, CC, NW, R>::value)) 
   const int fr = lane;
   int64_t jseq = 0;  // consumer position in the CTA's tile sequence
 
+  int rot = 0;  // DW: rotation of the derivative / loss-term warps over warps 1 .. NW - 1
   auto run = [&](auto scaled_tag) {
   constexpr bool SC = SCALE_OK && decltype(scaled_tag)::value;
 #pragma unroll 1
@@ -330,11 +334,19 @@ __global__ void __launch_bounds__(NW * 32, (K1MinBlocks<Tx, CC, NW, R>::value)) 
         };
         auto load_row = [&](int r, double (&xg)[NG][V]) { load_row_at(xs + (int64_t)r * ld, r < nr, xg); };
         // RL: slot r's row is r ^ p = r +- p8 +- p4 (signs by slot bits 3, 2): base[bits] + r * ld
-        const int p8 = (lane & 16) ? 8 : 0, p4 = (lane & 8) ? 4 : 0;
-        const Tx* xb[4];
+        const int pl = RL ? ((lane >> 1) & (16 - (16 >> RLN))) : 0;  // lane bits 4.. -> slot bits 3..
+        const Tx* xb[RL ? (1 << RLN) : 1];
         if constexpr (RL) {
 #pragma unroll
-          for (int bi = 0; bi < 4; ++bi) xb[bi] = xs + (int64_t)(((bi & 2) ? -p8 : p8) + ((bi & 1) ? -p4 : p4)) * ld;
+          for (int bi = 0; bi < (1 << RLN); ++bi) {
+            int off = 0;
+#pragma unroll
+            for (int b = 0; b < RLN; ++b) {
+              const int pb = pl & (8 >> b);  // the lane's flip of slot bit 3 - b
+              off += ((bi >> (RLN - 1 - b)) & 1) ? -pb : pb;
+            }
+            xb[bi] = xs + (int64_t)off * ld;
+          }
         }
         double xr[RR ? 1 : R][NG][V];
         double acc[NV];
@@ -346,14 +358,14 @@ __global__ void __launch_bounds__(NW * 32, (K1MinBlocks<Tx, CC, NW, R>::value)) 
         }
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-          if constexpr (RL) load_row_at(xb[((r >> 3) & 1) * 2 + ((r >> 2) & 1)] + (int64_t)r * ld, (r ^ (p8 | p4)) < nr, xr[0]);
+          if constexpr (RL) load_row_at(xb[RL ? (r >> (4 - RLN)) : 0] + (int64_t)r * ld, (r ^ pl) < nr, xr[0]);
           else if constexpr (RR) load_row(r, xr[0]);
 #pragma unroll
           for (int k = 0; k < NG; ++k)
 #pragma unroll
             for (int q = 0; q < V; ++q) acc[r] = fma(xr[RR ? 0 : r][k][q], wr[k][q], acc[r]);
         }
-        reduce_scatter_k<NV, RL ? 2 : 0>(acc, lane);
+        reduce_scatter_k<NV, RLN>(acc, lane);
         if ((lane & ((32 >> LG) - 1)) == 0) rb[wid * NV + (lane >> (5 - LG))] = acc[0];
         __syncthreads();
         // x in registers: this tile's stage can be refilled now; x re-read in the
@@ -381,7 +393,13 @@ __global__ void __launch_bounds__(NW * 32, (K1MinBlocks<Tx, CC, NW, R>::value)) 
         };
         double pr = 0.0, lt = 0.0;
         if constexpr (DW) {
-          if (wid == (int)(jseq & (NW - 1))) {
+          // Between the two barriers every warp but one would idle: the tile's derivative
+          // (warp dw), the loss terms of the PREVIOUS tile (warp lw) and the running loss
+          // sum over the tile before that (warp 0, which also issued the refill above) all
+          // go there, so that after the second barrier the warps carry equal work.
+          const int ip = (int)(i & 1);
+          const int dw = 1 + rot, lw = 1 + (rot + 1 == NW - 1 ? 0 : rot + 1);
+          if (wid == dw) {
             // two-class softmax, logistic form (mirror_logistic_row): s = lg
             const double lg = row_logit();
             const int lab = (int)tcur;
@@ -391,22 +409,20 @@ __global__ void __launch_bounds__(NW * 32, (K1MinBlocks<Tx, CC, NW, R>::value)) 
             const double prw = lab == 0 ? p0 - 1.0 : p0;
             if (lane < NV) {
               *reinterpret_cast<double2*>(dsh + 2 * lane) = make_double2(prw, __dmul_rn(prw, 0x1.0p896));  // |prw| <= 1: exact
-              *reinterpret_cast<double2*>(dsh + 2 * R + 2 * lane) = make_double2(lab == 0 ? lg : -lg, den);
+              *reinterpret_cast<double2*>(dsh + 2 * R + ip * 2 * R + 2 * lane) = make_double2(lab == 0 ? lg : -lg, den);
             }
           }
-          __syncthreads();
-          if (wid == (int)((jseq + NW / 2) & (NW - 1))) {
-            // the loss terms (a log per row) on another warp, summed by warp 0 in row order one tile later
-            if (lane < NV) {
-              const double2 ad = *reinterpret_cast<const double2*>(dsh + 2 * R + 2 * lane);
-              lts[(jseq & 1) * R + lane] = (ad.x > 0.0 ? ad.x : 0.0) + hlog_1to2(ad.y);  // = hlog on [1, 2]
-            }
+          if (wid == lw && i > 0 && lane < NV) {
+            const double2 ad = *reinterpret_cast<const double2*>(dsh + 2 * R + (ip ^ 1) * 2 * R + 2 * lane);
+            lts[(ip ^ 1) * R + lane] = (ad.x > 0.0 ? ad.x : 0.0) + hlog_1to2(ad.y);  // = hlog on [1, 2]
           }
-          if (wid == 0 && i > 0) {
-            const double* lp = lts + ((jseq - 1) & 1) * R;  // previous tile: full
+          if (wid == 0 && i > 1) {
+            const double* lp = lts + ip * R;  // tile i - 2: full, its terms written one tile ago
 #pragma unroll
             for (int r = 0; r < R; ++r) la = la + lp[r];
           }
+          rot = rot + 1 == NW - 1 ? 0 : rot + 1;
+          __syncthreads();
         } else if constexpr (CC == 1) {
           const double lg = row_logit();
           pr = lg - tcur;
@@ -472,7 +488,27 @@ __global__ void __launch_bounds__(NW * 32, (K1MinBlocks<Tx, CC, NW, R>::value)) 
       if (nr == R) body(BoolTag<true>{});
       else body(BoolTag<false>{});
     }
-    if constexpr (CC == 2) {  // the split's last tile's loss terms
+    if constexpr (DW) {  // drain: the last tile's loss terms, the sums over the last two tiles
+      __syncthreads();
+      const int lp1 = (int)((ntile - 1) & 1);
+      if (ntile > 0) {
+        if (wid == 1 && lane < NV) {
+          const double2 ad = *reinterpret_cast<const double2*>(dsh + 2 * R + lp1 * 2 * R + 2 * lane);
+          lts[lp1 * R + lane] = (ad.x > 0.0 ? ad.x : 0.0) + hlog_1to2(ad.y);
+        }
+        if (wid == 0 && ntile > 1) {
+          const double* lp = lts + (lp1 ^ 1) * R;
+#pragma unroll
+          for (int r = 0; r < R; ++r) la = la + lp[r];
+        }
+      }
+      __syncthreads();
+      if (wid == 0 && ntile > 0) {
+        const int nr_last = (int)(r1 - (r0 + (ntile - 1) * R));
+        const double* lp = lts + lp1 * R;
+        for (int r = 0; r < nr_last; ++r) la = la + lp[r];
+      }
+    } else if constexpr (CC == 2) {  // the split's last tile's loss terms
       __syncthreads();
       if (wid == 0 && ntile > 0) {
         const int nr_last = (int)(r1 - (r0 + (ntile - 1) * R));
@@ -508,7 +544,7 @@ size_t stream_smem_bytes(int ld, int elem, int warps, int R, int CC, int stages)
   size_t b = (size_t)stages * R * ld * elem;
   b = (b + 15) / 16 * 16;
   (void)CC;
-  b += (size_t)2 * warps * R * 8 + (size_t)2 * warps * R * 8 + (size_t)4 * R * 8 + (size_t)stages * 8;
+  b += (size_t)2 * warps * R * 8 + (size_t)2 * warps * R * 8 + (size_t)6 * R * 8 + (size_t)stages * 8;
   return b;
 }
 

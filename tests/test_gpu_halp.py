@@ -103,6 +103,29 @@ def test_fullgrad_two_class_bf16_integer_conversion(H, oracle, d, n):
         assert gl == o.loss_value(w, plan=plan)
 
 
+@pytest.mark.parametrize("dtype,d", [("bf16", 512), ("bf16", 1024), ("bf16", 2048), ("f32", 300), ("f32", 1024),
+                                     ("f32", 2048), ("f64", 512)])
+def test_fullgrad_two_class_warp_counts(H, oracle, dtype, d):
+    """Two-class K1 on 2, 4, 8 and 16 warps per CTA: one rotating warp evaluates the
+    tile's softmax derivative and another its loss terms behind a second barrier
+    (k_fullgrad_stream.cu DW), 16-row tiles fill their dot slots in a lane-dependent row
+    order (RL).  Partial last tiles (n not a multiple of the tile) are included (CTAs
+    walking several splits: test_gpu_baseline_configs C4); loss and gradient
+    bit-identical to the oracle."""
+    rng = np.random.default_rng(d)
+    n = 20011
+    X = rng.standard_normal((n, d)) / np.sqrt(d)
+    Xd = {"f64": X, "f32": X.astype(np.float32), "bf16": bf16_bits(X)}[dtype]
+    lab = rng.integers(0, 2, n).astype(np.int32)
+    g, o = objs(H, oracle, Xd, labels=lab, C=2, l2=1e-5)
+    plan = g.oracle_plan()
+    assert g.plan()["fg_threads"] >= 64
+    for w in (rng.standard_normal(2 * d) * 0.5, rng.standard_normal(2 * d) * 20.0):
+        gg, gl = g._fullpass(w)
+        assert np.array_equal(gg, o.full_gradient(w, plan=plan))
+        assert gl == o.loss_value(w, plan=plan)
+
+
 def test_fullgrad_two_class_bf16_nonfinite_x(H, oracle):
     """A non-finite x disables the integer conversion (checked at creation):
     results follow IEEE arithmetic exactly like the oracle's (NaN / inf)."""
