@@ -162,8 +162,8 @@ template <bool B> struct BoolTag { static constexpr bool value = B; };
 // Minimum resident CTAs per SM the register allocator must allow.  The bf16 two-class
 // 16-row shape (C4: 4 warps) fits 168 registers with no spills, so 3 CTAs per SM
 // (12 warps) instead of 2 at 243 registers: same-box A/B 8.29 -> 7.60 ms per C4 pass
-// (profiles/r01_k1_minb3_ab.txt), bit-identical; the round-2 bench measures 7.42 ms =
-// 72% of HBM.  Forcing 3 on the 256-thread fp32 shapes spills (C3 86% -> 32%).
+// (profiles/r01_k1_minb3_ab.txt), bit-identical.  Forcing 3 on the 256-thread fp32
+// shapes spills (C3 86% -> 32%).  Current C4 figures: DESIGN.md section 7.
 #ifndef HALP_K1_MINB_BF16_2C
 #define HALP_K1_MINB_BF16_2C 3
 #endif

@@ -1,6 +1,7 @@
 #!/bin/bash
 # round 2 end-to-end check: GPU suite, smoke, bench (driver flags), reference arm, ncu launch list + K1 captures
 mkdir -p gpurun_out/final
+rm -f gpurun_out/final/*
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/final/build.log 2>&1
 timeout 2400 python -m pytest tests -m gpu -q --durations=25 > gpurun_out/final/pytest_gpu.log 2>&1
 echo "rc=$?" >> gpurun_out/final/pytest_gpu.log
