@@ -200,6 +200,30 @@ def test_codes_match_reference_order(H, oracle):
     assert np.count_nonzero(tr.reshape(steps, 100) != orec.trace) == 0
 
 
+@pytest.mark.parametrize("every", [0.0, 0.5, 2.0, 5.0])
+def test_halp_init_and_metric_gating(H, oracle, every):
+    """run_halp from a caller-supplied initial iterate (initial_iterate,
+    optimizers.cpp:209-216) with the Recorder's metric_every_passes gating
+    (optimizers.cpp:104-167) through halp_run: the same rows (count, pass
+    values, losses, hashes) and final iterate as the oracle."""
+    X, y = oracle.make_regression(800, 96, 0.05, 17)
+    g, o = objs(H, oracle, X.astype(np.float32), y, l2=1e-4)
+    init = np.random.default_rng(5).standard_normal(96) * 0.3
+    kw = dict(alpha=4e-3, epochs=6, inner_steps=800, bits=8, mu=2.0, seed=11, metric_every_passes=every)
+    rec = H.run_halp(g, H.OptimizerConfig(algorithm=H.Algorithm.Halp, init=init, **kw))
+    orec = oracle.run_halp(o, oracle.OracleConfig(init=init, **kw), plan=g.oracle_plan())
+    rows_equal(rec.rows, orec.rows)
+    assert np.array_equal(rec.final_iterate, orec.final_iterate)
+    assert rec.steps_taken == orec.steps_taken == 4800
+    # the first row is the initial iterate's: its loss is f(init), not f(0)
+    g0, l0 = g._fullpass(init)
+    assert rec.rows[0].loss == l0
+    if every >= 2.0:
+        assert len(rec.rows) < 7
+    with pytest.raises(H.InvalidInputError):
+        H.run_halp(g, H.OptimizerConfig(algorithm=H.Algorithm.Halp, init=init[:-1], **kw))
+
+
 @pytest.mark.parametrize("nc,m", [(1, 1), (2, 2), (4, 1), (3, 4), (16, 1), (8, 4), (1, 8), (16, 2)])
 def test_cluster_plans_bitexact(H, oracle, nc, m, monkeypatch):
     monkeypatch.setenv("HALP_IN_NC", str(nc))
