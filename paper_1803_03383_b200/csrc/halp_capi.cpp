@@ -322,9 +322,16 @@ bool plan_stream(int d, int C, int dtype, FgLaunch* out) {
     const int reg_cap = std::min(255, 65536 / T1);
     // one effective column for both losses (two classes: the logistic form)
     auto regs = [&](int r) { return 2 * (r * NG * V + 2 * NG * V + r) + 48; };
-    while (R > 1 && (R * NG * V > 64 || regs(R) > reg_cap || (int64_t)R * row_bytes > 32 * 1024 ||
-                     !stream_shape_ok(T1 / 32, NG, R, stages)))
-      R /= 2;
+    // tiles up to 32 KB in a 4-deep ring; 64 KB tiles in a 3-deep ring where that shape is
+    // instantiated (C3's 16 KB rows: 4-row tiles halve the per-tile barrier / reduce cost,
+    // measured on B200 12.35 -> 10.55 ms per pass, tools/fg_sweep.py, profiles/r02_s5_k1_c3_rows4.txt)
+    const bool free_stages = env_int("HALP_FG_STAGES", 0) == 0;
+    auto tile_ok = [&](int r) {
+      if ((int64_t)r * row_bytes <= 32 * 1024 && stream_shape_ok(T1 / 32, NG, r, stages)) return true;
+      return free_stages && (int64_t)r * row_bytes <= 64 * 1024 && stream_shape_ok(T1 / 32, NG, r, 3);
+    };
+    while (R > 1 && (R * NG * V > 64 || regs(R) > reg_cap || !tile_ok(R))) R /= 2;
+    if (free_stages && (int64_t)R * row_bytes > 32 * 1024) stages = 3;
     // bf16 two-class rows (C4): 16-row tiles with x re-read from shared memory
     // for the gradient phase, double-buffered (measured on B200, tools/fg_sweep.py:
     // 51% vs 48% of HBM for 8-row register tiles; the gradient is bit-identical)

@@ -180,7 +180,10 @@ __global__ void __launch_bounds__(NW * 32, (K1MinBlocks<Tx, CC, NW, R>::value)) 
   constexpr int LG = Log2<NV>::v;
   // RR: tiles of 16+ rows keep x in shared memory only and re-read it for the
   // gradient phase (registers for the row dots instead of an R x 8 fp64 slice)
-  constexpr bool RR = R >= 16;
+#ifndef HALP_K1_RR_MIN
+#define HALP_K1_RR_MIN 16
+#endif
+  constexpr bool RR = R >= HALP_K1_RR_MIN;
   // DW: two classes on several warps: ONE warp per tile (rotating over warps 1..) evaluates
   // the rows' softmax derivative (exp + division) and publishes it through shared memory
   // behind a second barrier, instead of every warp repeating it for the same R rows -- the

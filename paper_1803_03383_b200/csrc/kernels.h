@@ -37,13 +37,13 @@ cudaError_t launch_fullgrad_smx(const FgLaunch& L, const FgParams& p, cudaStream
 // Instantiated shapes (NW warps, NG groups/thread, R rows/tile, ring depth);
 // plan_for only picks shapes from this list.
 #ifdef HALP_STREAM_DEV_SHAPES  // developer builds: the C4 and C3 shapes only (fast SASS experiments)
-#define HALP_STREAM_SHAPES(X) X(4, 1, 16, 2) X(8, 1, 2, 4)
+#define HALP_STREAM_SHAPES(X) X(4, 1, 16, 2) X(8, 4, 2, 4) X(8, 4, 4, 3) X(8, 2, 2, 4) X(8, 2, 4, 4) X(8, 2, 8, 3) X(8, 1, 4, 4)
 #else
 #define HALP_STREAM_SHAPES(X) \
   X(1, 1, 4, 4) X(1, 1, 8, 4) X(2, 1, 4, 4) X(2, 1, 8, 4) X(4, 1, 4, 4) X(4, 1, 8, 4) X(8, 1, 2, 4) \
   X(8, 1, 4, 4) X(16, 1, 2, 4) X(16, 1, 4, 4) X(8, 2, 2, 4) X(16, 2, 1, 4) X(16, 2, 2, 4) X(8, 4, 1, 4) \
   X(8, 4, 2, 4) X(16, 4, 1, 4) X(16, 2, 2, 6) X(8, 2, 2, 6) X(8, 4, 2, 6) X(4, 1, 4, 6) \
-  X(4, 1, 16, 2) X(2, 1, 16, 2) X(1, 1, 16, 2)
+  X(4, 1, 16, 2) X(2, 1, 16, 2) X(1, 1, 16, 2) X(8, 4, 4, 3) X(8, 2, 4, 4) X(8, 2, 8, 3)
 #endif
 size_t stream_smem_bytes(int ld, int elem, int warps, int R, int CC, int stages);
 cudaError_t launch_fullgrad_stream(const FgLaunch& L, const FgParams& p, cudaStream_t st);

@@ -63,6 +63,24 @@ def test_fullgrad_squared_bitexact(H, oracle, dtype, shape):
     assert abs(gl - o.loss_value(w)) <= 1e-12 * abs(gl)
 
 
+@pytest.mark.parametrize("dtype,n,d", [("f32", 1501, 4096), ("f32", 1111, 3500), ("f64", 900, 2048), ("bf16", 700, 4096)])
+def test_fullgrad_squared_wide_rows(H, oracle, dtype, n, d):
+    """Rows of 16 KB (BASELINE C3's d = 4096 fp32): K1 streams them as 4-row, 64 KB
+    tiles through a 3-deep ring (halp_capi.cpp plan_stream); bit-identical to the
+    oracle, including a partial last tile and rows narrower than the thread tile."""
+    X, y = oracle.make_regression(n, d, 0.1, 13)
+    Xd = {"f64": X, "f32": X.astype(np.float32), "bf16": bf16_bits(X)}[dtype]
+    g, o = objs(H, oracle, Xd, y, l2=1e-4)
+    pl = g.plan()
+    if dtype in ("f32", "f64"):
+        assert pl["fg_rows_per_stage"] == 4 and pl["fg_stages"] == 3, pl
+    w = np.random.default_rng(2).standard_normal(d)
+    gg, gl = g._fullpass(w)
+    plan = g.oracle_plan()
+    assert np.array_equal(gg, o.full_gradient(w, plan=plan))
+    assert gl == o.loss_value(w, plan=plan)
+
+
 @pytest.mark.parametrize("C,d,n", [(2, 40, 3000), (3, 17, 500), (10, 784, 2000), (15, 33, 700)])
 def test_fullgrad_softmax_bitexact(H, oracle, C, d, n):
     rng = np.random.default_rng(C)

@@ -13,6 +13,10 @@ if w == "c3":
     n, d = 4194304, 4096
     X, y = H.generate("regression", n, d, dtype="f32", noise_sd=0.1, seed=3)
     obj = H.Objective(H.Dataset(X, targets=y), H.LossFamily.Squared, 0.0); b = n * d * 4 + n * 8
+elif w.startswith("sq:"):  # sq:<n>:<d>:<dtype>  least squares of any shape
+    _, n, d, dt = w.split(":"); n, d = int(n), int(d)
+    X, y = H.generate("regression", n, d, dtype=dt, noise_sd=0.1, seed=3)
+    obj = H.Objective(H.Dataset(X, targets=y), H.LossFamily.Squared, 0.0); b = n * d * {"f32": 4, "f64": 8, "bf16": 2}[dt] + n * 8
 elif w == "c1":
     n, d = 8192, 256
     X, y = H.generate("regression", n, d, dtype="f32", noise_sd=0.01, seed=0)
