@@ -448,8 +448,11 @@ def main():
                 "algorithmic_bytes_per_launch": algo_bytes, "launch_ms": fg_ms,
                 "bytes_model": "rows*d*4 (x, fp32) + rows*8 (y, fp64) per pass; rows = this rank's row shard",
                 "timed": f"K1 time inside the timed region ({fg_passes} passes, CUDA events on the solver stream)",
+                "frac_of_nominal_8000": achieved / 8000.0,
                 "note": "K1 is the HBM-bound kernel; the epoch's dominant kernel is K3 (latency-bound serial "
-                        "chain, see inner_loop)"}
+                        "chain, see inner_loop).  peak is a torch copy (read + write) figure: a read-only "
+                        "stream can exceed it, so frac may pass 1; frac_of_nominal_8000 is against HBM3e's "
+                        "nominal 8 TB/s"}
     inner = {"kernel": "k3_inner", "bound": "latency (one serial chain per step)", "ns_per_step": inner_ns,
              "steps_per_s": 1e9 / inner_ns, "cycles_per_step_at_sm_clock": inner_ns * (clocks.get("sm_mhz") or 0) / 1e3,
              "share_of_epoch": tim["inner_ms"] / ms_total if world == 1 else None,
