@@ -25,9 +25,11 @@ LIB = os.path.join(HERE, "libhalp_b200.so")
 CUDA = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 NVCC = os.path.join(CUDA, "bin", "nvcc")
 
-CU_SOURCES = ["k_fullgrad.cu", "k_fullgrad_smx.cu", "k_fullgrad_stream.cu", "k_inner.cu", "k_batch.cu", "k_datagen.cu", "k_lm.cu"]
+# k_fullgrad_stream.cu is compiled as three translation units (one per element type) in parallel
+CU_SOURCES = ["k_fullgrad.cu", "k_fullgrad_smx.cu", "k_fullgrad_stream_bf16.cu", "k_fullgrad_stream_f32.cu",
+              "k_fullgrad_stream_f64.cu", "k_inner.cu", "k_batch.cu", "k_datagen.cu", "k_lm.cu"]
 CXX_SOURCES = ["halp_capi.cpp", "halp_datasets.cpp"]
-HEADERS = ["halp_device.cuh", "kernels.h", "rng_jump.hpp"]
+HEADERS = ["halp_device.cuh", "kernels.h", "rng_jump.hpp", "k_fullgrad_stream.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-fmad=false", "-std=c++17", "-Xcompiler", "-fPIC",
                      "-Xptxas", "-v", "-I", os.path.join(ROOT, "include")]

@@ -543,14 +543,6 @@ __global__ void __launch_bounds__(NW * 32, (K1MinBlocks<Tx, CC, NW, R>::value)) 
 }
 
 // ------------------------------------------------------------------ dispatch
-size_t stream_smem_bytes(int ld, int elem, int warps, int R, int CC, int stages) {
-  size_t b = (size_t)stages * R * ld * elem;
-  b = (b + 15) / 16 * 16;
-  (void)CC;
-  b += (size_t)2 * warps * R * 8 + (size_t)2 * warps * R * 8 + (size_t)6 * R * 8 + (size_t)stages * 8;
-  return b;
-}
-
 namespace {
 
 template <class Tx, int CC, int NW, int NG, int R, int STAGES, bool FULLG>
@@ -595,16 +587,50 @@ cudaError_t launch_stream_cc(const FgLaunch& L, const FgParams& p, cudaStream_t 
 
 }  // namespace
 
+// The instantiations are split by element type over three translation units
+// (k_fullgrad_stream_{f64,f32,bf16}.cu define HALP_STREAM_TU = 0 / 1 / 2 and include this
+// file) so that they compile in parallel; without the macro this file is the whole kernel.
+cudaError_t launch_stream_f64(const FgLaunch& L, const FgParams& p, cudaStream_t st);
+cudaError_t launch_stream_f32(const FgLaunch& L, const FgParams& p, cudaStream_t st);
+cudaError_t launch_stream_bf16(const FgLaunch& L, const FgParams& p, cudaStream_t st);
+
+#if !defined(HALP_STREAM_TU) || HALP_STREAM_TU == 0
+cudaError_t launch_stream_f64(const FgLaunch& L, const FgParams& p, cudaStream_t st) {
+  if (p.C == 1) return launch_stream_cc<double, 1>(L, p, st);
+  if (p.C == 2) return launch_stream_cc<double, 2>(L, p, st);
+  return cudaErrorInvalidConfiguration;
+}
+#endif
+#if !defined(HALP_STREAM_TU) || HALP_STREAM_TU == 2
+cudaError_t launch_stream_bf16(const FgLaunch& L, const FgParams& p, cudaStream_t st) {
+  if (p.C == 1) return launch_stream_cc<__nv_bfloat16, 1>(L, p, st);
+  if (p.C == 2) return launch_stream_cc<__nv_bfloat16, 2>(L, p, st);
+  return cudaErrorInvalidConfiguration;
+}
+#endif
+#if !defined(HALP_STREAM_TU) || HALP_STREAM_TU == 1
+cudaError_t launch_stream_f32(const FgLaunch& L, const FgParams& p, cudaStream_t st) {
+  if (p.C == 1) return launch_stream_cc<float, 1>(L, p, st);
+  if (p.C == 2) return launch_stream_cc<float, 2>(L, p, st);
+  return cudaErrorInvalidConfiguration;
+}
+
+size_t stream_smem_bytes(int ld, int elem, int warps, int R, int CC, int stages) {
+  size_t b = (size_t)stages * R * ld * elem;
+  b = (b + 15) / 16 * 16;
+  (void)CC;
+  b += (size_t)2 * warps * R * 8 + (size_t)2 * warps * R * 8 + (size_t)6 * R * 8 + (size_t)stages * 8;
+  return b;
+}
+
 cudaError_t launch_fullgrad_stream(const FgLaunch& L, const FgParams& p, cudaStream_t st) {
-  switch (L.dtype * 10 + p.C) {
-    case 1: return launch_stream_cc<double, 1>(L, p, st);
-    case 2: return launch_stream_cc<double, 2>(L, p, st);
-    case 11: return launch_stream_cc<float, 1>(L, p, st);
-    case 12: return launch_stream_cc<float, 2>(L, p, st);
-    case 21: return launch_stream_cc<__nv_bfloat16, 1>(L, p, st);
-    case 22: return launch_stream_cc<__nv_bfloat16, 2>(L, p, st);
+  switch (L.dtype) {
+    case 0: return launch_stream_f64(L, p, st);
+    case 1: return launch_stream_f32(L, p, st);
+    case 2: return launch_stream_bf16(L, p, st);
     default: return cudaErrorInvalidConfiguration;
   }
 }
+#endif
 
 }  // namespace halp
