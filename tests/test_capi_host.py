@@ -69,6 +69,19 @@ def test_shard_plan_partitions_rows(H):
 def test_plan_for_configs(H):
     p = H.plan_for(4194304, 4096, 1, "f32")
     assert p["fg_threads"] in (256, 512) and p["fg_vec"] == 4 and p["fg_splits"] == 4096
+    # C3's 16 KB rows: 4-row 64 KB tiles in a 3-deep ring (measured)
+    assert (p["fg_rows_per_stage"], p["fg_stages"]) == (4, 3)
+    p = H.plan_for(16777216, 1024, 2, "bf16")  # C4: 16-row tiles re-read from shared memory
+    assert (p["fg_threads"], p["fg_rows_per_stage"], p["fg_stages"]) == (128, 16, 2)
+    # streaming plans (up to 4 feature groups per thread): a tile never exceeds 64 KB, a ring never 220 KB
+    for dt, es in (("f32", 4), ("f64", 8), ("bf16", 2)):
+        for d in (24, 256, 1000, 1024, 2048, 3500, 4096):
+            if (d * es + 15) // 16 > 4 * 256:
+                continue  # wider rows take the generic kernel
+            q = H.plan_for(100000, d, 1, dt)
+            row = (d * es + 15) // 16 * 16
+            assert q["fg_rows_per_stage"] * row <= 64 * 1024, (dt, d, q)
+            assert q["fg_rows_per_stage"] * row * q["fg_stages"] <= 220 * 1024, (dt, d, q)
     p = H.plan_for(60000, 784, 10, "f32")
     assert p["in_ctas"] * p["in_threads"] * p["in_per"] >= 7840
     with pytest.raises(H.UnsupportedError):
