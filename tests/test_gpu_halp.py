@@ -144,6 +144,25 @@ def test_fullgrad_two_class_warp_counts(H, oracle, dtype, d):
         assert gl == o.loss_value(w, plan=plan)
 
 
+@pytest.mark.parametrize("dtype,n,d", [("bf16", 150001, 512), ("f32", 60001, 1024)])
+def test_fullgrad_two_class_multi_split(H, oracle, dtype, n, d):
+    """More splits than resident CTAs on 2 and 8 warps per CTA: every CTA walks several
+    splits, so the two-class window's loss-term / loss-sum pipeline is drained and
+    restarted at split boundaries while the copy ring runs across them."""
+    rng = np.random.default_rng(n)
+    X = (rng.standard_normal((n, d), dtype=np.float32) / np.float32(np.sqrt(d))).astype(np.float32)
+    Xd = X if dtype == "f32" else bf16_bits(X)
+    lab = rng.integers(0, 2, n).astype(np.int32)
+    g, o = objs(H, oracle, Xd, labels=lab, C=2, l2=1e-5)
+    pl = g.plan()
+    assert pl["fg_splits"] >= 1024 and pl["fg_threads"] in (64, 256), pl
+    w = rng.standard_normal(2 * d) * 0.7
+    gg, gl = g._fullpass(w)
+    plan = g.oracle_plan()
+    assert np.array_equal(gg, o.full_gradient(w, plan=plan))
+    assert gl == o.loss_value(w, plan=plan)
+
+
 def test_fullgrad_two_class_bf16_nonfinite_x(H, oracle):
     """A non-finite x disables the integer conversion (checked at creation):
     results follow IEEE arithmetic exactly like the oracle's (NaN / inf)."""
