@@ -1,6 +1,6 @@
 """Inner-loop (K3) plan sweep: us/step for cluster size NC and coords/thread M.
 
-    python tools/sweep_inner.py c2|c3|c1 [T] [NC:M,NC:M,...] [VAR=VALUE ...]
+    python tools/sweep_inner.py c2|c3|c4|c1 [T] [NC:M,NC:M,...] [VAR=VALUE ...]
 """
 import itertools
 import os
@@ -22,6 +22,10 @@ elif which == "c3":
     X, y = H.generate("regression", 65536, 4096, dtype="f32", noise_sd=0.1, seed=3)
     obj = H.Objective(H.Dataset(X, targets=y), H.LossFamily.Squared, 0.0)
     cfg = dict(alpha=5e-5, mu=1.0, bits=16)
+elif which == "c4":  # two-class bf16 d = 1024 on a 1 Mi-row slice of C4's generator (2 GiB > L2)
+    X, lab = H.generate("logistic", 1048576, 1024, dtype="bf16", x_scale=1024 ** -0.5, seed=4)
+    obj = H.Objective(H.Dataset(X, labels=lab, num_classes=2), H.LossFamily.Softmax, 1e-5)
+    cfg = dict(alpha=0.05, mu=2.5, bits=8)
 elif which.startswith("r"):
     X, y = H.generate("regression", 8192, int(which[1:]), dtype="f32", noise_sd=0.01, seed=0)
     obj = H.Objective(H.Dataset(X, targets=y), H.LossFamily.Squared, 0.0)
@@ -43,6 +47,7 @@ def main():
     rgrid = [(0, 0)] + [(1, m) for m in (1, 2, 4, 8)] + [(nc, m) for nc in (2, 4, 8, 16) for m in (1, 2, 4)]
     grids = {"c2": [(nc, m) for nc in (4, 8, 16) for m in (1, 2, 4, 8)],
              "c3": [(nc, m) for nc in (1, 2, 4, 8, 16) for m in (1, 2, 4, 8)],
+             "c4": [(0, 0)] + [(nc, m) for nc in (2, 4, 8, 16) for m in (1, 2, 4, 8) if 2048 <= nc * 256 * m <= 8192 * 2],
              "c1": [(nc, m) for nc in (1, 2, 4) for m in (1, 2, 4, 8)]}.get(which, rgrid)
     env = dict(os.environ, ROOT=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     tag = ""
